@@ -1,0 +1,225 @@
+"""Seeded synthetic lattices shaped like the paper's workloads (Sec. 6,
+Table 1: uniform cells, graded radii, irregular high-degree node mixes).
+
+Every generator returns a `Lattice`: float32 node positions, int64 strut index
+pairs, float32 node (sphere) radii and the per-end strut radii derived from them
+(struts are tangent to the nodal spheres, Sec. 4.1 last paragraph, so a
+strut's radius at an end is that node's sphere radius).
+
+Node order is lattice (spatially coherent) order; struts are sorted by
+(min endpoint, max endpoint).  Nothing here computes any meta-mesh quantity.
+"""
+from __future__ import annotations
+
+import dataclasses
+
+import numpy as np
+
+
+@dataclasses.dataclass
+class Lattice:
+    xyz: np.ndarray      # float32 [N, 3]
+    ends: np.ndarray     # int64   [S, 2]
+    node_r: np.ndarray   # float32 [N]
+    name: str = "lattice"
+
+    @property
+    def n_nodes(self) -> int:
+        return int(self.xyz.shape[0])
+
+    @property
+    def n_struts(self) -> int:
+        return int(self.ends.shape[0])
+
+    @property
+    def r_end(self) -> np.ndarray:
+        """Per-end strut radii, float32 [S, 2] (r_i^0, r_i^1 of PAPER.md Sec. 4.3.1)."""
+        return self.node_r[self.ends].astype(np.float32)
+
+    def degrees(self) -> np.ndarray:
+        return np.bincount(self.ends.ravel(), minlength=self.n_nodes)
+
+    def genus(self) -> int:
+        """Cycle rank S - N + C of the strut graph = genus of the lattice's boundary
+        surface (the boundary of a thickened connected graph is a closed surface of
+        genus equal to the graph's first Betti number)."""
+        n = self.n_nodes
+        parent = np.arange(n)
+
+        def find(a):
+            while parent[a] != a:
+                parent[a] = parent[parent[a]]
+                a = parent[a]
+            return a
+        used = np.zeros(n, dtype=bool)
+        for a, b in self.ends:
+            used[a] = used[b] = True
+            ra, rb = find(a), find(b)
+            if ra != rb:
+                parent[ra] = rb
+        comps = len({find(i) for i in range(n) if used[i]})
+        return int(self.n_struts - int(used.sum()) + comps)
+
+
+def _finish(xyz, ends, node_r, name) -> Lattice:
+    ends = np.asarray(ends, dtype=np.int64).reshape(-1, 2)
+    lo = np.minimum(ends[:, 0], ends[:, 1])
+    hi = np.maximum(ends[:, 0], ends[:, 1])
+    order = np.lexsort((hi, lo))
+    ends = np.stack([lo[order], hi[order]], axis=1)
+    return Lattice(np.ascontiguousarray(xyz, dtype=np.float32), np.ascontiguousarray(ends),
+                   np.ascontiguousarray(node_r, dtype=np.float32), name)
+
+
+def _radii(n, radius):
+    return np.full(n, radius, dtype=np.float32)
+
+
+def cubic(nx: int, ny: int, nz: int, pitch: float = 1.0, radius: float = 0.1) -> Lattice:
+    """Simple cubic grid with nx*ny*nz NODES and axis-aligned struts
+    (SPEC.md lattice_io example: grid(3,3,3) -> 27 nodes, 54 struts)."""
+    g = np.stack(np.meshgrid(np.arange(nx), np.arange(ny), np.arange(nz), indexing="ij"), -1).reshape(-1, 3)
+    idx = lambda i, j, k: (i * ny + j) * nz + k
+    ends = []
+    for ax, lim in enumerate((nx, ny, nz)):
+        m = g[:, ax] < lim - 1
+        a = g[m]
+        b = a.copy()
+        b[:, ax] += 1
+        ends.append(np.stack([idx(*a.T), idx(*b.T)], 1))
+    xyz = g.astype(np.float64) * pitch
+    return _finish(xyz, np.concatenate(ends), _radii(len(g), radius), f"cubic{nx}x{ny}x{nz}")
+
+
+def bcc(nx: int, ny: int, nz: int, pitch: float = 1.0, radius: float = 0.05) -> Lattice:
+    """Body-centred cubic lattice of nx*ny*nz CELLS: cell corners plus one centre node
+    per cell, each centre joined to its 8 corners (8 struts per cell; 10x10x10 cells
+    = 8000 struts, BASELINE.json configs[0])."""
+    cx, cy, cz = nx + 1, ny + 1, nz + 1
+    corners = np.stack(np.meshgrid(np.arange(cx), np.arange(cy), np.arange(cz), indexing="ij"), -1).reshape(-1, 3)
+    cells = np.stack(np.meshgrid(np.arange(nx), np.arange(ny), np.arange(nz), indexing="ij"), -1).reshape(-1, 3)
+    n_corner = len(corners)
+    cidx = lambda i, j, k: (i * cy + j) * cz + k
+    ends = []
+    centre_ids = n_corner + np.arange(len(cells))
+    for di in (0, 1):
+        for dj in (0, 1):
+            for dk in (0, 1):
+                ends.append(np.stack([centre_ids, cidx(cells[:, 0] + di, cells[:, 1] + dj, cells[:, 2] + dk)], 1))
+    xyz = np.concatenate([corners.astype(np.float64), cells.astype(np.float64) + 0.5]) * pitch
+    return _finish(xyz, np.concatenate(ends), _radii(len(xyz), radius), f"bcc{nx}x{ny}x{nz}")
+
+
+def bcc_slab(nx: int, ny: int, nz: int, z0: int, z1: int, pitch: float = 1.0, radius: float = 0.05) -> Lattice:
+    """The cells with z-index in [z0, z1) of an nx*ny*nz-cell BCC lattice (a spatial
+    block for multi-GPU partitioning).  Node positions are the global ones."""
+    lat = bcc(nx, ny, z1 - z0, pitch, radius)
+    xyz = lat.xyz.astype(np.float64)
+    xyz[:, 2] += z0 * pitch
+    return Lattice(xyz.astype(np.float32), lat.ends, lat.node_r, f"bccslab{nx}x{ny}x{nz}[{z0}:{z1}]")
+
+
+def octet(nx: int, ny: int, nz: int, pitch: float = 1.0, radius: float = 0.04) -> Lattice:
+    """Octet truss of nx*ny*nz cubic CELLS = FCC points (cell corners + face centres)
+    joined to their 12 nearest neighbours (24 struts per cell; 100^3 cells ~ 24M)."""
+    # FCC points = integer points of [0,2nx]x[0,2ny]x[0,2nz] with even coordinate sum.
+    g = np.stack(np.meshgrid(np.arange(2 * nx + 1), np.arange(2 * ny + 1), np.arange(2 * nz + 1),
+                             indexing="ij"), -1).reshape(-1, 3)
+    g = g[(g.sum(1) % 2) == 0]
+    lut = -np.ones((2 * nx + 1, 2 * ny + 1, 2 * nz + 1), dtype=np.int64)
+    lut[g[:, 0], g[:, 1], g[:, 2]] = np.arange(len(g))
+    offs = np.array([(1, 1, 0), (1, -1, 0), (1, 0, 1), (1, 0, -1), (0, 1, 1), (0, 1, -1)])
+    ends = []
+    lim = np.array([2 * nx, 2 * ny, 2 * nz])
+    for o in offs:
+        q = g + o
+        m = np.all((q >= 0) & (q <= lim), axis=1)
+        ends.append(np.stack([np.nonzero(m)[0], lut[q[m, 0], q[m, 1], q[m, 2]]], 1))
+    xyz = g.astype(np.float64) * (0.5 * pitch)
+    return _finish(xyz, np.concatenate(ends), _radii(len(g), radius), f"octet{nx}x{ny}x{nz}")
+
+
+def star(directions, lengths=1.0, radius: float = 0.1, far_radii=None) -> Lattice:
+    """One centre node (index 0) joined to far nodes along `directions`."""
+    d = np.asarray(directions, dtype=np.float64)
+    d = d / np.linalg.norm(d, axis=1, keepdims=True)
+    ln = np.broadcast_to(np.asarray(lengths, dtype=np.float64), (len(d),))
+    xyz = np.concatenate([np.zeros((1, 3)), d * ln[:, None]])
+    r = np.full(len(xyz), radius, dtype=np.float64)
+    if far_radii is not None:
+        r[1:] = far_radii
+    ends = np.stack([np.zeros(len(d), dtype=np.int64), 1 + np.arange(len(d))], 1)
+    return _finish(xyz, ends, r, f"star{len(d)}")
+
+
+def single_strut(length: float = 1.0, r0: float = 0.1, r1: float = 0.1) -> Lattice:
+    xyz = np.array([[0.0, 0.0, 0.0], [length, 0.0, 0.0]])
+    return _finish(xyz, [[0, 1]], np.array([r0, r1]), "single")
+
+
+def chain(n: int = 3, pitch: float = 1.0, radius: float = 0.1, bend_deg: float = 0.0) -> Lattice:
+    """n nodes on a polyline; each interior node bends the chain by bend_deg."""
+    pts = [np.zeros(3)]
+    ang = 0.0
+    for _ in range(n - 1):
+        pts.append(pts[-1] + pitch * np.array([np.cos(ang), np.sin(ang), 0.0]))
+        ang += np.deg2rad(bend_deg)
+    ends = [[i, i + 1] for i in range(n - 1)]
+    return _finish(np.array(pts), ends, _radii(n, radius), f"chain{n}")
+
+
+def jitter(lat: Lattice, amount: float, seed: int = 0) -> Lattice:
+    """Perturb node positions by uniform noise in [-amount, amount]^3 (seeded)."""
+    rng = np.random.default_rng(seed)
+    xyz = lat.xyz.astype(np.float64) + rng.uniform(-amount, amount, size=lat.xyz.shape)
+    return Lattice(xyz.astype(np.float32), lat.ends.copy(), lat.node_r.copy(), lat.name + f"+jit{amount}")
+
+
+def graded_radii(lat: Lattice, r_min: float, r_max: float, axis: int = 0) -> Lattice:
+    """Node radius graded linearly along `axis` from r_min to r_max (conical struts
+    wherever an edge is not perpendicular to `axis`; BASELINE.json configs[1])."""
+    x = lat.xyz[:, axis].astype(np.float64)
+    span = max(float(x.max() - x.min()), 1e-30)
+    r = r_min + (r_max - r_min) * (x - x.min()) / span
+    return Lattice(lat.xyz.copy(), lat.ends.copy(), r.astype(np.float32), lat.name + "+graded")
+
+
+def voronoi_like(n_nodes: int, seed: int = 0, deg_min: int = 3, deg_max: int = 30,
+                 radius: float = 0.03, min_angle_deg: float = 28.0) -> Lattice:
+    """Stochastic lattice with skewed node degrees (BASELINE.json configs[2] shape).
+
+    Nodes: a jittered grid.  Each node draws a target degree from a Zipf-like
+    distribution on [deg_min, deg_max]; candidate struts are the node's nearest
+    neighbours, accepted greedily (shortest first) while both endpoints stay under
+    their target degree and every pair of struts at a node stays at least
+    `min_angle_deg` apart (so strut pairs meet in bounded conics)."""
+    from scipy.spatial import cKDTree
+    rng = np.random.default_rng(seed)
+    side = int(np.ceil(n_nodes ** (1 / 3)))
+    g = np.stack(np.meshgrid(np.arange(side), np.arange(side), np.arange(side), indexing="ij"), -1).reshape(-1, 3)[:n_nodes]
+    xyz = g + rng.uniform(-0.3, 0.3, size=g.shape)
+    ks = np.arange(deg_min, deg_max + 1)
+    p = 1.0 / (ks - deg_min + 1.0) ** 1.3
+    target = rng.choice(ks, size=n_nodes, p=p / p.sum())
+    tree = cKDTree(xyz)
+    k = min(deg_max + 12, n_nodes)
+    dist, nbr = tree.query(xyz, k=k)
+    cand = [(dist[i, j], i, nbr[i, j]) for i in range(n_nodes) for j in range(1, k) if i < nbr[i, j]]
+    cand.sort()
+    cos_lim = np.cos(np.deg2rad(min_angle_deg))
+    dirs = [[] for _ in range(n_nodes)]
+    deg = np.zeros(n_nodes, dtype=np.int64)
+    ends = []
+    for _, a, b in cand:
+        if deg[a] >= target[a] or deg[b] >= target[b]:
+            continue
+        v = xyz[b] - xyz[a]
+        v = v / np.linalg.norm(v)
+        if any(float(v @ w) > cos_lim for w in dirs[a]) or any(float(-v @ w) > cos_lim for w in dirs[b]):
+            continue
+        dirs[a].append(v)
+        dirs[b].append(-v)
+        deg[a] += 1
+        deg[b] += 1
+        ends.append((a, b))
+    return _finish(xyz, ends, _radii(n_nodes, radius), f"voronoi{n_nodes}")
