@@ -1,0 +1,432 @@
+"""Pins of the CPU oracle against what the paper and mathematics fix (not against itself).
+
+Every check here is independent of the oracle's own formulas: closed forms, hand-worked
+counts (tests/golden/), brute-force inside tests on the convex hull of two spheres
+(the strut solid, Sec. 4.1 "struts ... have tangential relationships with
+nodal spheres"), dense sampling, and mesh invariants (watertight, manifold, Euler
+characteristic 2 - 2g of the thickened graph).
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import synth
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+rng0 = np.random.default_rng(12345)
+
+
+# ---------------------------------------------------------------------------------------
+# independent geometry helpers (no oracle code)
+# ---------------------------------------------------------------------------------------
+def hull_sd(x, v0, r0, v1, r1):
+    """min over lam in [0,1] of f(lam) = |x - c(lam)| - r(lam), c(lam) = v0 + lam (v1 - v0),
+    r(lam) = r0 + lam (r1 - r0): < 0 inside the convex hull of the two balls (the strut
+    solid), 0 on its boundary.  f is convex; its stationary points solve
+    (lam A - B)^2 = dr^2 |p - lam D|^2 (A = |D|^2, B = p.D), a quadratic in lam."""
+    v0, v1, x = (np.asarray(a, np.float64) for a in (v0, v1, x))
+    r0, r1 = float(r0), float(r1)
+    p, D, dr = x - v0, v1 - v0, r1 - r0
+    A, B, P = D @ D, p @ D, p @ p
+    f = lambda lam: math.sqrt(max((p - lam * D) @ (p - lam * D), 0.0)) - (r0 + lam * dr)
+    cands = [0.0, 1.0]
+    k = A - dr * dr                         # > 0: the far sphere does not contain the near one
+    disc = dr * dr * max(A * P - B * B, 0.0) / k
+    if True:
+        for sg in (-1.0, 1.0):
+            lam = (B + sg * math.sqrt(disc)) / A
+            if 0.0 <= lam <= 1.0:
+                cands.append(lam)
+    return min(f(lam) for lam in cands)
+
+
+def mesh_invariants(tris):
+    """tris: float64 [T, 4, 3] (normal, v1, v2, v3).  Weld by exact coordinates."""
+    V = tris[:, 1:, :].reshape(-1, 3)
+    uniq, inv = np.unique(V, axis=0, return_inverse=True)
+    F = inv.reshape(-1, 3)
+    e = np.concatenate([F[:, [0, 1]], F[:, [1, 2]], F[:, [2, 0]]])
+    eu, cnt = np.unique(np.sort(e, axis=1), axis=0, return_counts=True)
+    _, dcnt = np.unique(e, axis=0, return_counts=True)
+    v1, v2, v3 = tris[:, 1], tris[:, 2], tris[:, 3]
+    vol = float(np.sum(np.einsum("ij,ij->i", v1, np.cross(v2, v3))) / 6)
+    area = float(np.sum(np.linalg.norm(np.cross(v2 - v1, v3 - v1), axis=1)) / 2)
+    return dict(V=len(uniq), E=len(eu), F=len(F), chi=len(uniq) - len(eu) + len(F),
+                edge_counts=set(cnt.tolist()), directed_dups=int((dcnt > 1).sum()),
+                degenerate=int(((F[:, 0] == F[:, 1]) | (F[:, 1] == F[:, 2]) | (F[:, 0] == F[:, 2])).sum()),
+                volume=vol, area=area)
+
+
+# ---------------------------------------------------------------------------------------
+# elementary building blocks
+# ---------------------------------------------------------------------------------------
+def test_atan2p_matches_libm(oracle_mod):
+    ys = np.concatenate([rng0.normal(size=4000), [0, 0, 1, -1, 1, -1, 1e-30, 3, -3]])
+    xs = np.concatenate([rng0.normal(size=4000), [1, -1, 0, 0, 1, -1, 1, 3, -3]])
+    err = max(abs(oracle_mod.atan2p(y, x) - math.atan2(np.float32(y), np.float32(x))) for y, x in zip(ys, xs))
+    assert err < 4e-7
+    assert oracle_mod.atan2p(0.0, 0.0) == 0.0
+
+
+def test_eq11_subdivision_counts(oracle_mod):
+    """PAPER.md Eq. 11, N = floor((t2-t1)/(2 acos(1-CE))) + 1."""
+    th = oracle_mod.theta0(1.0)                       # 2 acos(0) = pi
+    assert oracle_mod.subdiv_count(2 * math.pi, th) == 3          # floor(2pi/pi) + 1
+    th = oracle_mod.theta0(1 - math.cos(math.pi / 8))  # = pi/4
+    assert oracle_mod.subdiv_count(math.pi / 2, th) == 3          # floor((pi/2)/(pi/4)) + 1
+    assert oracle_mod.subdiv_count(1e-6, oracle_mod.theta0(0.02)) == 1
+    # the N+1 points of Eq. 12 meet the chord error on a circle: segment angle < th0
+    for ce in (0.2, 0.05, 0.02, 1e-3):
+        th = oracle_mod.theta0(ce)
+        for dt in rng0.uniform(0.01, 2 * math.pi, 50):
+            N = oracle_mod.subdiv_count(dt, th)
+            assert 1 - math.cos(dt / N / 2) <= ce * (1 + 1e-5)
+            if N > 1:   # minimality (Sec. 5 "minimum number of vertices"): N-1 would need a larger step
+                assert dt / (N - 1) >= th * (1 - 1e-6)
+
+
+def test_eq7_special_sections(oracle_mod):
+    R = 0.3
+    u = np.array([0.0, 0.0, 1.0])
+    e1 = np.array([1.0, 0.0, 0.0])
+    # cylinder cut perpendicular to its axis: circle of radius R (SPEC conic_geometry example)
+    o, a, b = oracle_mod.eq7(u, 0.0, R, np.array([0, 0, 1.0]), 0.5, e1)
+    assert np.allclose([np.linalg.norm(a), np.linalg.norm(b)], [R, R], atol=1e-12)
+    assert np.allclose(o, [0, 0, 0.5], atol=1e-12)
+    # 45 degree plane through the node: |a| = R sqrt2, |b| = R
+    o, a, b = oracle_mod.eq7(u, 0.0, R, np.array([1, 0, 1.0]) / math.sqrt(2), 0.0, e1)
+    assert math.isclose(np.linalg.norm(a), R * math.sqrt(2), rel_tol=1e-12)
+    assert math.isclose(np.linalg.norm(b), R, rel_tol=1e-12)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_eq7_random_cone_sections_lie_on_cone_and_plane(oracle_mod, seed):
+    """Eq. 7 with alpha read as -arcsin((R - r_far)/L): every point of the ellipse lies on
+    the strut's surface (hull boundary, brute force) and on the plane."""
+    rng = np.random.default_rng(seed)
+    R = 0.2
+    L = 2.0
+    u = rng.normal(size=3); u /= np.linalg.norm(u)
+    r_far = R * rng.uniform(0.6, 1.4)
+    s = (R - r_far) / L
+    # plane crossing the strut near the node, tilted < 50 deg from the cross-section
+    n = u + 0.8 * rng.normal(size=3) * 0.5
+    n /= np.linalg.norm(n)
+    pc = R * rng.uniform(0.3, 0.9)
+    e1 = np.cross(u, [0.3, 0.2, 0.9]); e1 /= np.linalg.norm(e1)
+    o, a, b = oracle_mod.eq7(u, s, R, n, pc, e1)
+    assert abs(a @ b) < 1e-12 * (a @ a)
+    for t in np.linspace(0, 2 * math.pi, 24, endpoint=False):
+        v = o + a * math.sin(t) + b * math.cos(t)
+        assert abs(n @ v - pc) < 1e-12
+        z = v @ u
+        if 0.05 * L < z < 0.95 * L:   # on the lateral cone between the spheres
+            assert abs(hull_sd(v, np.zeros(3), R, L * u, r_far)) < 1e-9
+
+
+def test_aux_plane_is_bisector_for_equal_cylinders(oracle_mod):
+    n, pc = oracle_mod.aux_plane([1, 0, 0], 0.0, [0, 1, 0], 0.0, 0.25)
+    assert np.allclose(n, np.array([1, -1, 0]) / math.sqrt(2), atol=1e-15) and abs(pc) < 1e-15
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_aux_plane_contains_bruteforce_intersection(oracle_mod, seed):
+    """PAPER.md Sec. 4.3.1: the intersection of two struts tangent to one nodal sphere is
+    planar.  Points where strut a's surface enters strut b (bisection with hull_sd) lie on
+    the plane the oracle derives."""
+    rng = np.random.default_rng(100 + seed)
+    R = 0.25
+    ua, ub = (v / np.linalg.norm(v) for v in rng.normal(size=(2, 3)))
+    while ua @ ub > 0.6:
+        ub = rng.normal(size=3); ub /= np.linalg.norm(ub)
+    La, Lb = 3.0, 2.5
+    ra, rb = R * rng.uniform(0.7, 1.3, 2)
+    sa, sb = (R - ra) / La, (R - rb) / Lb
+    n, pc = oracle_mod.aux_plane(ua, sa, ub, sb, R)
+    ca = math.sqrt(1 - sa * sa)
+    e1 = np.cross(ua, [0.1, 0.7, 0.3]); e1 /= np.linalg.norm(e1)
+    e2 = np.cross(ua, e1)
+    hits = 0
+    for phi in np.linspace(0, 2 * math.pi, 36, endpoint=False):
+        r = math.cos(phi) * e1 + math.sin(phi) * e2
+        F = R * (sa * ua + ca * r)          # tangency point of the generator on the sphere
+        g = ca * ua - sa * r                # generator direction (tangent to the sphere at F)
+        f = lambda s: hull_sd(F + s * g, np.zeros(3), R, Lb * ub, rb)
+        lo, hi = 1e-3, 1.5
+        if not (f(lo) < -1e-6 and f(hi) > 0):
+            continue
+        for _ in range(60):
+            m = 0.5 * (lo + hi)
+            lo, hi = (m, hi) if f(m) < 0 else (lo, m)
+        p = F + lo * g
+        assert abs(n @ p - pc) < 1e-7
+        hits += 1
+    assert hits >= 3
+
+
+@pytest.mark.parametrize("seed", range(5))
+def test_eq9_range_matches_dense_sampling(oracle_mod, seed):
+    rng = np.random.default_rng(200 + seed)
+    a = rng.normal(size=3)
+    b = np.cross(a, rng.normal(size=3)); b *= rng.uniform(0.3, 1.0) * np.linalg.norm(a) / np.linalg.norm(b)
+    o = rng.normal(size=3)
+    n = rng.normal(size=3); n /= np.linalg.norm(n)
+    p = o + 0.5 * rng.normal(size=3)
+    kind, lo, ln = oracle_mod.eq9(o, a, b, n, p)
+    ts = np.linspace(0, 2 * math.pi, 10000, endpoint=False)
+    inside = (np.outer(np.sin(ts), a) + np.outer(np.cos(ts), b) + o - p) @ n <= 0
+    if kind == 1:
+        assert inside.all()
+    elif kind == 0:
+        assert not inside.any()
+    else:
+        pred = ((ts - lo) % (2 * math.pi)) <= ln
+        mism = np.nonzero(pred != inside)[0]
+        for i in mism:   # disagreement only within one sample step of a range end
+            dt = min(abs(((ts[i] - lo + math.pi) % (2 * math.pi)) - math.pi),
+                     abs(((ts[i] - lo - ln + math.pi) % (2 * math.pi)) - math.pi))
+            assert dt <= 2 * math.pi / 10000 * 1.01
+
+
+# ---------------------------------------------------------------------------------------
+# meta-mesh topology
+# ---------------------------------------------------------------------------------------
+def _gold_nodes():
+    with open(os.path.join(GOLD, "hand_worked_nodes.json")) as f:
+        return json.load(f)["nodes"]
+
+
+@pytest.mark.parametrize("case", _gold_nodes(), ids=lambda c: c["name"])
+def test_hand_worked_node_counts(oracle_mod, case):
+    lat = synth.star(case["dirs"], 1.0, 0.1)
+    o = oracle_mod.Oracle.from_lattice(lat)
+    assert o.metamesh() == 0
+    r = o.node(0)
+    assert (r["nv"], r["na"], r["nh"]) == (case["V"], case["A"], case["H"])
+    assert r["nv"] - r["na"] + (len(case["dirs"]) + r["nh"]) == 2
+
+
+@pytest.mark.parametrize("deg", [30.0, 75.0, 110.0, 160.0])
+def test_two_equal_struts_curve_on_bisector(oracle_mod, deg):
+    """North star pin: for two equal-radius struts the intersection curve lies on their
+    bisector plane."""
+    th = math.radians(deg)
+    d = [[1, 0, 0], [math.cos(th), math.sin(th), 0]]
+    lat = synth.star(d, 1.0, 0.1)
+    o = oracle_mod.Oracle.from_lattice(lat)
+    o.metamesh()
+    r = o.node(0)
+    x = lat.xyz.astype(np.float64)          # the float32 inputs, exactly
+    ua, ub = (v / np.linalg.norm(v) for v in (x[1] - x[0], x[2] - x[0]))
+    nb = ua - ub
+    ell = [i for i in range(r["na"]) if r["a_int"][i, 0] > 0]
+    assert len(ell) == 1
+    t0, dt, *g = r["a_f64"][ell[0]]
+    oo, a, b = np.array(g[0:3]), np.array(g[3:6]), np.array(g[6:9])
+    for t in np.linspace(t0, t0 + dt, 50):
+        assert abs((oo + a * math.sin(t) + b * math.cos(t)) @ nb) < 1e-12
+    for q in range(r["nv"]):
+        assert abs(r["v_pos64"][q] @ nb) < 1e-12
+
+
+def _incident(lat, n):
+    return [s for s in range(lat.n_struts) if n in lat.ends[s]]
+
+
+@pytest.mark.parametrize("lat", [
+    synth.jitter(synth.bcc(2, 2, 2), 0.04, 7),
+    synth.graded_radii(synth.jitter(synth.octet(1, 1, 1), 0.03, 3), 0.03, 0.06),
+    synth.voronoi_like(40, seed=5, radius=0.05),
+], ids=["bcc-jitter", "octet-graded-jitter", "voronoi"])
+def test_arc_points_lie_on_the_union_boundary(oracle_mod, lat):
+    """Brute force: every sampled point of every arc lies on the surfaces of both sides it
+    separates and inside no other strut (hull_sd), and junction vertices likewise."""
+    o = oracle_mod.Oracle.from_lattice(lat)
+    assert o.metamesh() == 0
+    off, cs = o.csr()
+    nodes = rng0.choice(lat.n_nodes, size=min(8, lat.n_nodes), replace=False)
+    for n in nodes:
+        r = o.node(int(n))
+        if r["d"] == 0:
+            continue
+        R = float(lat.node_r[n])
+        c = lat.xyz[n].astype(np.float64)
+        sides = [None] + [int(s) for s in cs[off[n]:off[n + 1]]]
+
+        def sd(k, y):
+            s = sides[k]
+            return hull_sd(c + y, lat.xyz[lat.ends[s, 0]], lat.node_r[lat.ends[s, 0]],
+                           lat.xyz[lat.ends[s, 1]], lat.node_r[lat.ends[s, 1]])
+        for i in range(r["na"]):
+            lo, hi = r["a_int"][i, :2]
+            t0, dt, *g = r["a_f64"][i]
+            oo, a, b = np.array(g[0:3]), np.array(g[3:6]), np.array(g[6:9])
+            for t in np.linspace(t0, t0 + dt, 7)[1:-1]:
+                y = oo + a * math.sin(t) + b * math.cos(t)
+                if lo == 0:
+                    assert abs(np.linalg.norm(y) - R) < 1e-9 * R
+                else:
+                    assert abs(sd(lo, y)) < 1e-9
+                assert abs(sd(hi, y)) < 1e-9
+                for k in range(1, len(sides)):
+                    if k not in (lo, hi):
+                        assert sd(k, y) > -1e-9
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_strut_visible_area_matches_monte_carlo(oracle_mod, seed):
+    """The loop bounds the visible part of each strut: the band area at fine resolution
+    equals a Monte-Carlo estimate of the strut's lateral area outside all other struts."""
+    rng = np.random.default_rng(300 + seed)
+    dirs = []
+    while len(dirs) < 5:
+        v = rng.normal(size=3); v /= np.linalg.norm(v)
+        if all(v @ w < math.cos(math.radians(40)) for w in dirs):
+            dirs.append(v)
+    R = 0.15
+    far_r = R * rng.uniform(0.8, 1.2, len(dirs))
+    lat = synth.star(dirs, 1.0, R, far_radii=far_r)
+    o = oracle_mod.Oracle.from_lattice(lat)
+    assert o.metamesh() == 0
+    o.triangulate(2e-5)
+    s = 0                                   # strut 0 = centre -> far node 1
+    tris = o.strut_triangles(s)
+    band = float(np.sum(np.linalg.norm(np.cross(tris[:, 2] - tris[:, 1], tris[:, 3] - tris[:, 1]), axis=1)) / 2)
+    u = np.array(dirs[0]); L = 1.0; rf = far_r[0]
+    sb = (R - rf) / L; cb = math.sqrt(1 - sb * sb)
+    e1 = np.cross(u, [0.31, 0.5, 0.8]); e1 /= np.linalg.norm(e1); e2 = np.cross(u, e1)
+    ell = L * cb                              # generator length between tangency circles
+    rho = lambda t: R * cb - t * sb           # cone radius along the generator
+    n_mc = 6000
+    ts = rng.uniform(0, ell, n_mc)
+    ph = rng.uniform(0, 2 * math.pi, n_mc)
+    w = rho(ts)
+    vis = np.zeros(n_mc)
+    for i in range(n_mc):
+        r = math.cos(ph[i]) * e1 + math.sin(ph[i]) * e2
+        x = R * (sb * u + cb * r) + ts[i] * (cb * u - sb * r)
+        if ts[i] > 0.5:       # far from the centre node nothing else can cover it
+            vis[i] = 1
+            continue
+        vis[i] = all(hull_sd(x, np.zeros(3), R, np.array(dirs[k]), far_r[k]) > 0 for k in range(1, len(dirs)))
+    mc = 2 * math.pi * ell * float(np.mean(w * vis))
+    se = 2 * math.pi * ell * float(np.std(w * vis)) / math.sqrt(n_mc)
+    assert abs(band - mc) < 4 * se + 1e-3 * band
+
+
+# ---------------------------------------------------------------------------------------
+# triangulation
+# ---------------------------------------------------------------------------------------
+LATTICES = {
+    "single": lambda: synth.single_strut(1.0, 0.1, 0.1),
+    "cone": lambda: synth.single_strut(1.0, 0.1, 0.06),
+    "chain-straight": lambda: synth.chain(4, 1.0, 0.1, 0.0),
+    "chain-bent": lambda: synth.chain(4, 1.0, 0.1, 50.0),
+    "cubic3": lambda: synth.cubic(3, 3, 3),
+    "bcc2": lambda: synth.bcc(2, 2, 2),
+    "octet2": lambda: synth.octet(2, 2, 2),
+    "octet2-graded": lambda: synth.graded_radii(synth.octet(2, 2, 2), 0.03, 0.06),
+    "bcc3-jitter": lambda: synth.jitter(synth.bcc(3, 3, 3), 0.05, 1),
+    "cubic4-graded-jitter": lambda: synth.jitter(synth.graded_radii(synth.cubic(4, 4, 4), 0.06, 0.12, 2), 0.04, 2),
+    "voronoi": lambda: synth.voronoi_like(200, seed=3, radius=0.05),
+}
+
+
+@pytest.mark.parametrize("name", list(LATTICES))
+@pytest.mark.parametrize("ce", [0.05, 2e-3])
+def test_triangulation_watertight_manifold_euler(oracle_mod, name, ce):
+    """North star: every edge shared by exactly two triangles, consistent orientation,
+    Euler characteristic 2 - 2g with g the lattice's cycle rank, outward normals."""
+    lat = LATTICES[name]()
+    o = oracle_mod.Oracle.from_lattice(lat)
+    assert o.metamesh() == 0
+    T = o.triangulate(ce)
+    tris = o.write_triangles()
+    assert len(tris) == T
+    inv = mesh_invariants(tris)
+    assert inv["edge_counts"] == {2}
+    assert inv["directed_dups"] == 0
+    assert inv["degenerate"] == 0
+    assert inv["chi"] == 2 - 2 * lat.genus()
+    assert inv["volume"] > 0
+
+
+def _single_strut_area(L, r0, r1):
+    """Analytic area of the single-strut surface the method converges to: the lateral
+    frustum between the two tangency circles plus the two hole fans (cones from each
+    tangency circle to the pole on the far side of its sphere)."""
+    s = (r0 - r1) / L
+    c = math.sqrt(1 - s * s)
+    lateral = math.pi * (r0 * c + r1 * c) * (L * c)
+    fan = lambda R, sg: math.pi * (R * c) * R * math.sqrt(2 + 2 * sg)
+    return lateral + fan(r0, s) + fan(r1, -s)
+
+
+@pytest.mark.parametrize("r1", [0.1, 0.07, 0.13])
+def test_area_converges_to_analytic(oracle_mod, r1):
+    lat = synth.single_strut(1.0, 0.1, r1)
+    o = oracle_mod.Oracle.from_lattice(lat)
+    o.metamesh()
+    exact = _single_strut_area(1.0, 0.1, r1)
+    errs = []
+    for ce in (1e-1, 1e-2, 1e-3, 1e-4):
+        o.triangulate(ce)
+        errs.append(abs(mesh_invariants(o.write_triangles())["area"] - exact) / exact)
+    assert errs[-1] < 2e-4
+    assert all(e2 < e1 for e1, e2 in zip(errs, errs[1:]))
+
+
+def test_bent_joint_band_area_converges(oracle_mod):
+    """Two equal cylinders at angle theta: each band's area is 2 pi R L - 2 R^2 cot(theta/2)
+    (the loop's axial offset is max(0, R cot(theta/2) cos phi), mean R cot(theta/2)/pi)."""
+    th = math.radians(100.0)
+    R, L = 0.1, 1.0
+    lat = synth.star([[1, 0, 0], [math.cos(th), math.sin(th), 0]], L, R)
+    o = oracle_mod.Oracle.from_lattice(lat)
+    o.metamesh()
+    exact = 2 * math.pi * R * L - 2 * R * R / math.tan(th / 2)
+    prev = None
+    for ce in (1e-2, 1e-3, 1e-4):
+        o.triangulate(ce)
+        t = o.strut_triangles(0)
+        area = float(np.sum(np.linalg.norm(np.cross(t[:, 2] - t[:, 1], t[:, 3] - t[:, 1]), axis=1)) / 2)
+        err = abs(area - exact) / exact
+        assert prev is None or err < prev
+        prev = err
+    assert prev < 2e-4
+
+
+def test_triangle_count_monotone_in_chord_error(oracle_mod):
+    lat = synth.jitter(synth.bcc(2, 2, 2), 0.03, 4)
+    o = oracle_mod.Oracle.from_lattice(lat)
+    o.metamesh()
+    counts = [o.triangulate(ce) for ce in (1e-4, 1e-3, 1e-2, 5e-2, 0.2)]
+    assert all(a >= b for a, b in zip(counts, counts[1:]))
+
+
+def test_triangles_per_strut_order_of_magnitude_table2(oracle_mod):
+    """PAPER.md Table 2: Bone, 136,391 struts -> 4.78M triangles at 2 % chord error
+    (~35 per strut).  Order-of-magnitude check on synthetic lattices (SPEC.md
+    acceptance 9: mean within [24, 46])."""
+    for lat in (synth.bcc(3, 3, 3), synth.octet(2, 2, 2), synth.voronoi_like(200, seed=2, radius=0.05)):
+        o = oracle_mod.Oracle.from_lattice(lat)
+        o.metamesh()
+        assert 24 <= o.triangulate(0.02) / lat.n_struts <= 46
+
+
+def test_fan_apex_on_nodal_sphere_and_hole_orientation(oracle_mod):
+    """Eq. 13: the fan centre is projected onto the nodal sphere; fan triangles face away
+    from the node centre."""
+    lat = synth.cubic(2, 2, 2)
+    o = oracle_mod.Oracle.from_lattice(lat)
+    o.metamesh()
+    o.triangulate(0.01)
+    base, M, bp = o.hole_info()
+    assert np.allclose(np.linalg.norm(bp, axis=1), 0.1, rtol=1e-12)
+    for n in range(lat.n_nodes):
+        t = o.node_hole_triangles(n)
+        cen = (t[:, 1] + t[:, 2] + t[:, 3]) / 3 - lat.xyz[n]
+        assert np.all(np.einsum("ij,ij->i", t[:, 0], cen) > 0)
