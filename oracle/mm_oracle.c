@@ -39,6 +39,7 @@
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#include <stdio.h>
 
 #ifndef M_PI
 #define M_PI 3.14159265358979323846
@@ -119,6 +120,7 @@ float orc_atan2p(float y, float x) {
 typedef struct {
   int32_t lo, hi, vs, ve;     /* sides (lo<hi, 0 = sphere), start/end vertex      */
   float t0, dt;               /* binary32 parameter range on the conic (t0, t0+dt) */
+  float tmid;                 /* binary32 tangent length at the interval midpoint      */
   f3 o, a, b;                 /* binary32 conic v(t) = a sin t + b cos t + o     */
   d3 o64, a64, b64;           /* binary64 conic                                  */
   double t064, dt64;          /* binary64 parameter range                        */
@@ -529,6 +531,8 @@ static int node_metamesh(orc_lat *L, int64_t n) {
   int nc = 0;
   for (int j = 0; j < nj; j++) {
     uint32_t bits = (1u << J[j].a) | (1u << J[j].b) | (1u << J[j].c);
+    /* a strut junction at tangent length ~0 lies on the nodal sphere: it ties with side 0 */
+    if (fabsf(J[j].tau) <= delta) bits |= 1u;
     int q;
     for (q = 0; q < nc; q++)
       if (fabsf(J[j].y.x - V[q].y.x) <= dc && fabsf(J[j].y.y - V[q].y.y) <= dc && fabsf(J[j].y.z - V[q].y.z) <= dc) break;
@@ -596,12 +600,13 @@ static int node_metamesh(orc_lat *L, int64_t n) {
           t0 = tq[i]; vs = Q[i]; ve = Q[j];
         }
         f3 y = F3((o.x + av.x * ms) + bv.x * mc, (o.y + av.y * ms) + bv.y * mc, (o.z + av.z * ms) + bv.z * mc);
+        float tmid = a == 0 ? 0.0f : h32(S, a, y);
         int ok = a == 0 ? valid_sphere_pt(S, d, pm, y, delta)
-                        : valid_strut_pt(S, d, pm, y, h32(S, a, y), delta);
+                        : valid_strut_pt(S, d, pm, y, tmid, delta);
         if (!ok) continue;
         if (na >= ORC_MAXA) { free(V); free(A); M->status = ORC_E_ACAP; return M->status; }
         arc_t *E = &A[na];
-        E->lo = a; E->hi = b; E->t0 = t0; E->dt = dt; E->o = o; E->a = av; E->b = bv;
+        E->lo = a; E->hi = b; E->t0 = t0; E->dt = dt; E->o = o; E->a = av; E->b = bv; E->tmid = tmid;
         if (vs < 0) {  /* closed conic without vertex: add its seam (t = 0) */
           V[nv].kind = 1; V[nv].mask = pm; V[nv].seam_arc = na;
           V[nv].y = F3(o.x + bv.x, o.y + bv.y, o.z + bv.z);
@@ -612,6 +617,39 @@ static int node_metamesh(orc_lat *L, int64_t n) {
       }
     }
 
+  /* An AMBIGUOUS strut-strut arc (a,b) -- tangent length at its midpoint within the tie
+   * tolerance of the sphere -- whose two end vertices are also joined by the end-circle
+   * arcs of a AND of b runs under a strictly exposed hole lune: the hole wins and the
+   * arc is dropped (R10).  Seam references are renumbered. */
+  {
+    int w = 0;
+    int remap[ORC_MAXA];
+    for (int i = 0; i < na; i++) {
+      int drop = 0;
+      if (A[i].lo > 0 && A[i].vs != A[i].ve && A[i].tmid < delta) {
+        int ca = 0, cb = 0;
+        for (int j = 0; j < na; j++) {
+          if (A[j].lo != 0) continue;
+          int same = (A[j].vs == A[i].vs && A[j].ve == A[i].ve) || (A[j].vs == A[i].ve && A[j].ve == A[i].vs);
+          if (!same) continue;
+          if (A[j].hi == A[i].lo) ca = 1;
+          if (A[j].hi == A[i].hi) cb = 1;
+        }
+        drop = ca && cb;
+      }
+      remap[i] = drop ? -1 : w;
+      if (!drop) A[w++] = A[i];
+    }
+    for (int q = nc; q < nv; q++) V[q].seam_arc = remap[V[q].seam_arc];
+    na = w;
+  }
+
+  if (getenv("ORC_DEBUG")) {
+    for (int q = 0; q < nv; q++)
+      fprintf(stderr, "node %lld v%d mask %x y/R (%.5f %.5f %.5f)\n", (long long)n, q, V[q].mask, V[q].y.x / R, V[q].y.y / R, V[q].y.z / R);
+    for (int i = 0; i < na; i++)
+      fprintf(stderr, "node %lld arc%d (%d,%d) v%d->v%d t0=%.5f dt=%.5f\n", (long long)n, i, A[i].lo, A[i].hi, A[i].vs, A[i].ve, A[i].t0, A[i].dt);
+  }
   /* every junction vertex must carry arcs */
   for (int q = 0; q < nc; q++) {
     int used = 0;
@@ -653,6 +691,15 @@ static int node_metamesh(orc_lat *L, int64_t n) {
         loop_t t = LE[beg + j]; LE[beg + j] = LE[beg + j - 1]; LE[beg + j - 1] = t;
         float tf = key[j]; key[j] = key[j - 1]; key[j - 1] = tf;
       }
+    if (getenv("ORC_DEBUG")) {
+      fprintf(stderr, "node %lld strut side %d loop:", (long long)n, k);
+      for (int i = 0; i < cnt; i++) {
+        arc_t *E = &A[LE[beg + i].arc];
+        fprintf(stderr, " [arc%d (%d,%d) v%d->v%d fwd%d ps=%.5f dph=%.5f]", LE[beg + i].arc, E->lo, E->hi, E->vs, E->ve,
+                LE[beg + i].fwd, LE[beg + i].phs, LE[beg + i].dph);
+      }
+      fprintf(stderr, "\n");
+    }
     float sum = 0.0f;
     for (int i = 0; i < cnt; i++) {
       loop_t *x = &LE[beg + i], *y = &LE[beg + (i + 1) % cnt];
@@ -730,13 +777,19 @@ static int node_metamesh(orc_lat *L, int64_t n) {
   return ORC_OK;
 }
 
-/* compute the meta-mesh of selected nodes (nodes == NULL: all) */
+/* compute the meta-mesh of selected nodes (nodes == NULL: all); a node in error keeps
+ * only its status (no partial topology) */
 int orc_metamesh(orc_lat *L, const int64_t *nodes, int64_t n_sel) {
   int64_t cnt = nodes ? n_sel : L->n_nodes;
   int64_t bad = 0;
   for (int64_t i = 0; i < cnt; i++) {
     int64_t n = nodes ? nodes[i] : i;
-    if (node_metamesh(L, n) != ORC_OK) bad++;
+    if (node_metamesh(L, n) != ORC_OK) {
+      node_mm *M = &L->mm[n];
+      bad++;
+      for (int k = 0; k <= M->d; k++) M->loop_off[k] = 0;
+      M->nv = M->na = M->nh = 0;
+    }
   }
   L->tri_ready = 0;
   return (int)(bad > 2147483647 ? 2147483647 : bad);

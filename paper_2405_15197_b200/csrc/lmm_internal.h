@@ -1,0 +1,103 @@
+// lmm_internal.h -- host-side context and kernel launch interfaces of liblmm.
+#pragma once
+#include <cstdint>
+#include <vector>
+#include <cuda_runtime.h>
+
+#include "../../include/lmm.h"
+#include "lmm_common.cuh"
+
+#define LMM_NBUCKET 3   // degree buckets 1..8, 9..16, 17..31 (0 and >31 handled apart)
+
+struct DevBuf {
+  void *p = nullptr;
+  size_t bytes = 0;
+};
+
+struct lmm_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int n_sm = 148;
+  int64_t N = 0, S = 0;
+  // lattice
+  DevBuf node;       // float4 [N]  x, y, z, r
+  DevBuf ends;       // int2   [S]
+  DevBuf csr_off;    // int    [N+1]
+  DevBuf csr_ent;    // int2   [2S] strut, far | end<<31
+  DevBuf strut_csr;  // int2   [S]  CSR entry of the strut at i0 and at i1
+  DevBuf deg_hist;   // unsigned long long [33]
+  DevBuf bucket_nodes;   // int [N]
+  DevBuf bucket_cnt;     // int [LMM_NBUCKET + 2]
+  int64_t bucket_off[LMM_NBUCKET + 3] = {0};
+  bool lattice_ok = false;
+  // meta-mesh
+  DevBuf node_hdr;   // int4 [N]
+  DevBuf vert;       // float4 slab
+  DevBuf arc;        // ArcRec slab
+  DevBuf loop_hdr;   // int2 [2S]
+  DevBuf loop;       // LoopRec slab
+  DevBuf hole_hdr;   // int2 slab
+  DevBuf hole_ent;   // HoleEnt slab
+  bool mm_ok = false;
+  // triangulation
+  double ce = 0.0;
+  float th0 = 0.0f;
+  DevBuf band;       // int4 [S] nA, nB, kB, 0
+  DevBuf strut_off;  // int64 [S+1]
+  DevBuf node_hole0; // int [N+1]  (int64 scan kept in tmp)
+  DevBuf node_hole0_64;
+  DevBuf hole_M;     // int [H]
+  DevBuf hole_off;   // int64 [H+1]
+  DevBuf hole_bp;    // float4 [H]
+  DevBuf hole_node;  // int [H]
+  int64_t H = 0, n_tri = 0, n_tri_band = 0;
+  bool tri_ok = false;
+  // scratch
+  DevBuf tmp64;      // int64 scan scratch
+  DevBuf scratch;    // misc
+  DevBuf stage[2];   // device staging for host output
+  void *pinned[2] = {nullptr, nullptr};
+  size_t pinned_bytes = 0;
+  cudaEvent_t stage_ev[2] = {nullptr, nullptr};
+  // timing
+  bool timing = false;
+  double k_ms[LMM_K_NCLASSES] = {0};
+  int64_t k_launch[LMM_K_NCLASSES] = {0};
+  struct EvPair { int cls; cudaEvent_t a, b; };
+  std::vector<EvPair> ev_pending;
+  std::vector<cudaEvent_t> ev_pool;
+  int timer_depth = 0;
+  int64_t n_launch = 0;   // kernels launched by this context
+};
+
+// memory helpers (lmm_api.cu)
+int dev_alloc(DevBuf &b, size_t bytes);
+void dev_free(DevBuf &b);
+
+// timing scope: records events around a launch when ctx->timing
+struct KTimer {
+  lmm_ctx *c;
+  int cls;
+  bool active = false;
+  cudaEvent_t a = nullptr;
+  KTimer(lmm_ctx *c_, int cls_);
+  ~KTimer();
+};
+
+// lattice.cu
+int lattice_build(lmm_ctx *c, const float *xyz_dev, const int64_t *ends_dev, const float *rend_dev);
+int degree_buckets(lmm_ctx *c);
+// metamesh.cu
+int metamesh_run(lmm_ctx *c);
+// scan.cu
+int scan_exclusive_i64(lmm_ctx *c, const int64_t *in, int64_t *out, int64_t n, int64_t *total_host);
+int scan_exclusive_i32_to_i64(lmm_ctx *c, const int *in, int64_t *out, int64_t n, int64_t *total_host);
+// triangulate.cu
+int triangulate_count(lmm_ctx *c);
+int triangulate_emit(lmm_ctx *c, int64_t first, int64_t count, void *out_dev, cudaStream_t st);
+
+#define CUDA_TRY(x)                                   \
+  do {                                                \
+    cudaError_t e__ = (x);                            \
+    if (e__ != cudaSuccess) return LMM_E_CUDA;        \
+  } while (0)

@@ -1,0 +1,742 @@
+// metamesh.cu -- per-node meta-mesh kernel (Sec. 4.1, 4.3.1, Eq. 7-9).
+//
+// One lane group (a warp) owns one lattice node.  Lanes map to the node's struts for
+// the per-side set-up, to (side, side, side) triples for the junction solve, to side
+// pairs for the arc walk (Eq. 7 ellipse + interval tests, Eq. 8-9 read as
+// the half-space tests at interval midpoints) and to struts for loop assembly; warp
+// ballots compact the variable-length results in the deterministic order of
+// DESIGN.md Sec. 4.  Nodes are scheduled through degree buckets (lattice.cu) so the
+// warps of a CTA carry comparable work.
+//
+// COMPILED WITH -fmad=false: every binary32 operation below is rounded as written, so
+// the topology decisions are bit-identical to the specification (and to the CPU
+// oracle's, which evaluates the same operations).
+#include <cooperative_groups.h>
+
+#include "lmm_internal.h"
+
+namespace cg = cooperative_groups;
+
+namespace {
+
+struct MMParams {
+  const float4 *node;
+  const int *csr_off;
+  const int2 *csr_ent;
+  const int2 *ends;
+  const int *node_list;
+  int n_list;
+  int4 *node_hdr;
+  float4 *vert;
+  ArcRec *arc;
+  int2 *loop_hdr;
+  LoopRec *loop;
+  int2 *hole_hdr;
+  HoleEnt *hole_ent;
+};
+
+template <int MAXS, int MAXJ, int MAXV, int MAXA, int MAXLE, int MAXH>
+struct alignas(16) NodeWS {
+  // sides: 0 = nodal sphere, 1..d = incident struts in ascending strut id
+  float wx[MAXS], wy[MAXS], wz[MAXS], e[MAXS];
+  float ux[MAXS], uy[MAXS], uz[MAXS], s[MAXS], c[MAXS], L[MAXS];
+  float asx[MAXS], asy[MAXS], asz[MAXS];
+  float e1x[MAXS], e1y[MAXS], e1z[MAXS];
+  float e2x[MAXS], e2y[MAXS], e2z[MAXS];
+  int sign[MAXS];
+  // junctions
+  float jx[MAXJ], jy[MAXJ], jz[MAXJ];
+  uint32_t jabc[MAXJ];
+  // vertices: clusters then seams
+  float vx[MAXV], vy[MAXV], vz[MAXV];
+  uint32_t vmask[MAXV];
+  ArcRec arcs[MAXA];
+  float atmid[MAXA];
+  int adrop[MAXA];
+  LoopRec le[MAXLE];
+  int lfirst[MAXS], lcount[MAXS];
+  int hoff[MAXH + 1];
+  uint32_t he[MAXA];
+};
+
+template <class WS> struct Node {
+  WS &w;
+  int d;
+  float R;
+  __device__ f3 W(int k) const { return F3(w.wx[k], w.wy[k], w.wz[k]); }
+  __device__ f3 U(int k) const { return F3(w.ux[k], w.uy[k], w.uz[k]); }
+  __device__ f3 AS(int k) const { return F3(w.asx[k], w.asy[k], w.asz[k]); }
+  __device__ f3 E1(int k) const { return F3(w.e1x[k], w.e1y[k], w.e1z[k]); }
+  __device__ f3 E2(int k) const { return F3(w.e2x[k], w.e2y[k], w.e2z[k]); }
+  __device__ f3 V(int q) const { return F3(w.vx[q], w.vy[q], w.vz[q]); }
+  __device__ float h(int k, f3 y) const { return k == 0 ? 0.0f : f_dot(W(k), y) - w.e[k]; }
+
+  // triple junction (oracle junction32)
+  __device__ bool junction(int a, int b, int c, f3 *y, float *tau) const {
+    f3 Wa = W(a), Wb = W(b), Wc = W(c);
+    float Ea = w.e[a], Eb = w.e[b], Ec = w.e[c];
+    if (a == 0) { Wa = F3(0.0f, 0.0f, 0.0f); Ea = 0.0f; }
+    f3 n1 = f_sub(Wa, Wb), n2 = f_sub(Wa, Wc);
+    float q1 = Ea - Eb, q2 = Ea - Ec;
+    f3 m = f_cross(n1, n2);
+    float mm = f_dot(m, m);
+    float nn1 = f_dot(n1, n1), nn2 = f_dot(n2, n2);
+    if (!(mm > (1e-8f * nn1) * nn2)) return false;
+    f3 c1 = f_cross(n2, m), c2 = f_cross(m, n1);
+    f3 y0 = F3((q1 * c1.x + q2 * c2.x) / mm, (q1 * c1.y + q2 * c2.y) / mm, (q1 * c1.z + q2 * c2.z) / mm);
+    float ml = sqrtf(mm);
+    f3 mh = f_div(m, ml);
+    float tau0 = f_dot(Wa, y0) - Ea;
+    float tau1 = f_dot(Wa, mh);
+    float A = 1.0f - tau1 * tau1;
+    if (!(A > 1e-6f)) return false;
+    float Bp = f_dot(y0, mh) - tau0 * tau1;
+    float C = (f_dot(y0, y0) - R * R) - tau0 * tau0;
+    float disc = Bp * Bp - A * C;
+    if (disc < 0.0f) return false;
+    float sq = sqrtf(disc);
+    float l0 = (-Bp - sq) / A, l1 = (-Bp + sq) / A;
+    y[0] = f_add(y0, f_scl(mh, l0));
+    tau[0] = tau0 + l0 * tau1;
+    y[1] = f_add(y0, f_scl(mh, l1));
+    tau[1] = tau0 + l1 * tau1;
+    return true;
+  }
+
+  __device__ bool valid_strut_pt(uint32_t excl, f3 y, float tau, float delta) const {
+    if (tau < -delta) return false;
+    for (int m = 1; m <= d; m++) {
+      if (excl & (1u << m)) continue;
+      if (h(m, y) - tau > delta) return false;
+    }
+    return true;
+  }
+  __device__ bool valid_sphere_pt(uint32_t excl, f3 y, float delta) const {
+    for (int m = 1; m <= d; m++) {
+      if (excl & (1u << m)) continue;
+      if (h(m, y) > -delta) return false;
+    }
+    return true;
+  }
+
+  // PAPER.md Eq. 7: strut a's ellipse in the auxiliary plane P_{a,b}
+  __device__ bool ellipse(int a, int b, f3 *o, f3 *av, f3 *bv) const {
+    f3 N = f_sub(W(a), W(b));
+    float nl = sqrtf(f_dot(N, N));
+    f3 n = f_div(N, nl);
+    float pc = (w.e[a] - w.e[b]) / nl;
+    f3 p = f_scl(n, pc);
+    float s = w.s[a], c = w.c[a];
+    f3 u = U(a);
+    if (!(fabsf(f_dot(n, u)) > fabsf(s) + 1e-3f)) return false;
+    f3 dd = F3(-u.x, -u.y, -u.z);
+    f3 dp = f_cross(dd, n);
+    float dpl2 = f_dot(dp, dp);
+    f3 r_;
+    if (dpl2 > 1e-12f) { dp = f_div(dp, sqrtf(dpl2)); r_ = f_cross(dp, dd); }
+    else r_ = E1(a);
+    f3 g1 = F3(c * dd.x - s * r_.x, c * dd.y - s * r_.y, c * dd.z - s * r_.z);
+    f3 g2 = F3(c * dd.x + s * r_.x, c * dd.y + s * r_.y, c * dd.z + s * r_.z);
+    f3 F1 = F3(R * ((-s) * dd.x - c * r_.x), R * ((-s) * dd.y - c * r_.y), R * ((-s) * dd.z - c * r_.z));
+    f3 F2 = F3(R * ((-s) * dd.x + c * r_.x), R * ((-s) * dd.y + c * r_.y), R * ((-s) * dd.z + c * r_.z));
+    float k1 = f_dot(n, f_sub(p, F1)) / f_dot(n, g1);
+    float k2 = f_dot(n, f_sub(p, F2)) / f_dot(n, g2);
+    f3 E1v = f_add(F1, f_scl(g1, k1)), E2v = f_add(F2, f_scl(g2, k2));
+    *o = f_scl(f_add(E1v, E2v), 0.5f);
+    *av = f_scl(f_sub(E1v, E2v), 0.5f);
+    float ad = f_dot(*av, dd), aa = f_dot(*av, *av);
+    float arg = 1.0f - (ad * ad) / ((c * c) * aa);
+    if (arg < 0.0f) arg = 0.0f;
+    float lam = sqrtf(arg);
+    *bv = f_scl(f_cross(*av, n), lam);
+    if (!(f_dot(*bv, *bv) > 1e-12f * aa)) return false;
+    return true;
+  }
+
+  // end-section (tangency) circle of strut b, parametrised by its strut frame
+  __device__ void circle(int b, f3 *o, f3 *av, f3 *bv) const {
+    float rs = R * w.s[b], rr = R * w.c[b];
+    *o = f_scl(U(b), rs);
+    *av = f_scl(E2(b), rr);
+    *bv = f_scl(E1(b), rr);
+  }
+};
+
+__device__ __forceinline__ float conic_t(f3 o, f3 av, f3 bv, f3 P, float *us, float *uc) {
+  f3 Q = f_sub(P, o);
+  float st = f_dot(Q, av) / f_dot(av, av);
+  float ct = f_dot(Q, bv) / f_dot(bv, bv);
+  float l = sqrtf(st * st + ct * ct);
+  *us = st / l;
+  *uc = ct / l;
+  return atan2p(st, ct);
+}
+
+template <int G> __device__ __forceinline__ int excl_scan(cg::thread_block_tile<G> &g, int v, int *total) {
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < G; o <<= 1) {
+    int y = g.shfl_up(x, o);
+    if ((int)g.thread_rank() >= o) x += y;
+  }
+  *total = g.shfl(x, G - 1);
+  return x - v;
+}
+
+// first lane (lowest rank) whose err != 0, its code; 0 if none
+template <int G> __device__ __forceinline__ int first_err(cg::thread_block_tile<G> &g, int err) {
+  unsigned m = g.ballot(err != 0);
+  if (!m) return 0;
+  return g.shfl(err, __ffs(m) - 1);
+}
+
+__device__ __forceinline__ void unrank3(int t, int n, int *a, int *b, int *c) {
+  int A = 0;
+  for (;;) {
+    int cnt = (n - 1 - A) * (n - 2 - A) / 2;
+    if (t < cnt) break;
+    t -= cnt;
+    A++;
+  }
+  int B = A + 1;
+  for (;;) {
+    int cnt = n - 1 - B;
+    if (t < cnt) break;
+    t -= cnt;
+    B++;
+  }
+  *a = A; *b = B; *c = B + 1 + t;
+}
+
+__device__ __forceinline__ void unrank2(int t, int n, int *a, int *b) {
+  int A = 0;
+  for (;;) {
+    int cnt = n - 1 - A;
+    if (t < cnt) break;
+    t -= cnt;
+    A++;
+  }
+  *a = A; *b = A + 1 + t;
+}
+
+#define MAXQ 16
+#define MAXLOOP 32
+
+template <int G, int MAXS, int MAXJ, int MAXV, int MAXA, int MAXLE, int MAXH>
+__device__ void process_node(cg::thread_block_tile<G> &g, NodeWS<MAXS, MAXJ, MAXV, MAXA, MAXLE, MAXH> &ws,
+                             const MMParams &P, int n) {
+  using WS = NodeWS<MAXS, MAXJ, MAXV, MAXA, MAXLE, MAXH>;
+  const int lane = g.thread_rank();
+  const int off = P.csr_off[n];
+  const int d = P.csr_off[n + 1] - off;
+  const float4 on = P.node[n];
+  Node<WS> nd{ws, d, on.w};
+  const float R = on.w;
+  const float delta = LMM_TOL_REL * R, dc = LMM_CTOL_REL * R;
+  int status = 0;
+
+  // ---- 1. sides -------------------------------------------------------------------
+  if (lane == 0) {
+    ws.wx[0] = ws.wy[0] = ws.wz[0] = ws.e[0] = 0.0f;
+  }
+  int err = 0;
+  for (int k0 = 0; k0 < d; k0 += G) {
+    int idx = k0 + lane;
+    if (idx < d) {
+      int k = idx + 1;
+      int2 ent = P.csr_ent[off + idx];
+      int far = ent.y & 0x7fffffff;
+      int endbit = (unsigned)ent.y >> 31;
+      float4 pf = P.node[far];
+      f3 po = F3(on.x, on.y, on.z), pfar = F3(pf.x, pf.y, pf.z);
+      f3 D = f_sub(pfar, po);
+      float Ln = sqrtf(f_dot(D, D));
+      if (!(Ln > 0.0f)) err = LMM_NODE_STRUT;
+      else {
+        f3 u = f_div(D, Ln);
+        float s = (R - pf.w) / Ln;
+        if (!(fabsf(s) < 0.9f)) err = LMM_NODE_STRUT;
+        else {
+          float c = sqrtf(1.0f - s * s);
+          f3 wv = f_div(u, c);
+          ws.wx[k] = wv.x; ws.wy[k] = wv.y; ws.wz[k] = wv.z;
+          ws.e[k] = (R * s) / c;
+          ws.ux[k] = u.x; ws.uy[k] = u.y; ws.uz[k] = u.z;
+          ws.s[k] = s; ws.c[k] = c; ws.L[k] = Ln;
+          ws.sign[k] = endbit ? -1 : 1;
+          // strut frame from p[i1] - p[i0]
+          f3 Da = endbit ? f_sub(po, pfar) : f_sub(pfar, po);
+          f3 as = f_nrm(Da);
+          float ax = fabsf(as.x), ay = fabsf(as.y), az = fabsf(as.z);
+          f3 ref = (ax <= ay && ax <= az) ? F3(1.0f, 0.0f, 0.0f) : (ay <= az ? F3(0.0f, 1.0f, 0.0f) : F3(0.0f, 0.0f, 1.0f));
+          f3 e1 = f_nrm(f_cross(as, ref));
+          f3 e2 = f_cross(as, e1);
+          ws.asx[k] = as.x; ws.asy[k] = as.y; ws.asz[k] = as.z;
+          ws.e1x[k] = e1.x; ws.e1y[k] = e1.y; ws.e1z[k] = e1.z;
+          ws.e2x[k] = e2.x; ws.e2y[k] = e2.y; ws.e2z[k] = e2.z;
+        }
+      }
+    }
+  }
+  if (g.any(err != 0)) status = LMM_NODE_STRUT;
+  g.sync();
+
+  int nj = 0, nc = 0, nv = 0, na = 0, nle = 0, nh = 0, nhe = 0;
+  const int ns = d + 1;
+
+  // ---- 2. triple junctions, lexicographic (a<b<c), root-minor ---------------------
+  if (status == 0 && d > 0) {
+    const int ntri = ns * (ns - 1) * (ns - 2) / 6;
+    for (int base = 0; base < ntri; base += G) {
+      int t = base + lane;
+      bool v0 = false, v1 = false;
+      int a = 0, b = 0, c = 0;
+      f3 y[2];
+      float tau[2];
+      bool sh0 = false, sh1 = false;
+      if (t < ntri) {
+        unrank3(t, ns, &a, &b, &c);
+        if (nd.junction(a, b, c, y, tau)) {
+          uint32_t excl = (1u << a) | (1u << b) | (1u << c);
+          for (int r = 0; r < 2; r++) {
+            bool ok = a == 0 ? nd.valid_sphere_pt(excl, y[r], delta) : nd.valid_strut_pt(excl, y[r], tau[r], delta);
+            if (!ok) continue;
+            bool sh = false;
+            int ks[3] = {a, b, c};
+            for (int q = 0; q < 3; q++)
+              if (ks[q] > 0 && tau[r] > 0.45f * (ws.L[ks[q]] * ws.c[ks[q]])) sh = true;
+            if (r == 0) { v0 = true; sh0 = sh; } else { v1 = true; sh1 = sh; }
+          }
+        }
+      }
+      unsigned m0 = g.ballot(v0), m1 = g.ballot(v1);
+      unsigned lt = (1u << lane) - 1u;
+      int pos = nj + __popc(m0 & lt) + __popc(m1 & lt);
+      int p0 = pos, p1 = pos + (v0 ? 1 : 0);
+      int e = 0;
+      if (v0) e = p0 >= MAXJ ? LMM_NODE_JCAP : (sh0 ? LMM_NODE_SHORT : 0);
+      if (!e && v1) e = p1 >= MAXJ ? LMM_NODE_JCAP : (sh1 ? LMM_NODE_SHORT : 0);
+      int fe = first_err<G>(g, e);
+      if (fe) { status = fe; break; }
+      uint32_t code = (uint32_t)a | ((uint32_t)b << 8) | ((uint32_t)c << 16);
+      if (v0) {
+        ws.jx[p0] = y[0].x; ws.jy[p0] = y[0].y; ws.jz[p0] = y[0].z;
+        ws.jabc[p0] = code | (fabsf(tau[0]) <= delta ? (1u << 25) : 0u);
+      }
+      if (v1) {
+        ws.jx[p1] = y[1].x; ws.jy[p1] = y[1].y; ws.jz[p1] = y[1].z;
+        ws.jabc[p1] = code | (1u << 24) | (fabsf(tau[1]) <= delta ? (1u << 25) : 0u);
+      }
+      nj += __popc(m0) + __popc(m1);
+    }
+  }
+  g.sync();
+
+  // ---- 3. leader clustering of coincident junctions --------------------------------
+  if (status == 0) {
+    for (int j = 0; j < nj; j++) {
+      float yx = ws.jx[j], yy = ws.jy[j], yz = ws.jz[j];
+      uint32_t code = ws.jabc[j];
+      uint32_t bits = (1u << (code & 0xff)) | (1u << ((code >> 8) & 0xff)) | (1u << ((code >> 16) & 0xff));
+      if (code & (1u << 25)) bits |= 1u;   // strut junction at tangent length ~0: on the sphere
+      int found = -1;
+      for (int q0 = 0; q0 < nc && found < 0; q0 += G) {
+        int q = q0 + lane;
+        bool mt = q < nc && fabsf(yx - ws.vx[q]) <= dc && fabsf(yy - ws.vy[q]) <= dc && fabsf(yz - ws.vz[q]) <= dc;
+        unsigned m = g.ballot(mt);
+        if (m) found = q0 + __ffs(m) - 1;
+      }
+      if (found < 0) {
+        if (nc >= MAXV) { status = LMM_NODE_CCAP; break; }
+        found = nc;
+        if (lane == 0) { ws.vx[found] = yx; ws.vy[found] = yy; ws.vz[found] = yz; ws.vmask[found] = 0u; }
+        nc++;
+      }
+      g.sync();
+      if (lane == 0) ws.vmask[found] |= bits;
+      g.sync();
+    }
+  }
+  nv = nc;
+  g.sync();
+
+  // ---- 4. arcs: every side pair walks its conic through its vertices --------------
+  if (status == 0 && d > 0) {
+    const int npair = ns * (ns - 1) / 2;
+    for (int base = 0; base < npair; base += G) {
+      int p = base + lane;
+      int e = 0, cnt = 0, closed = 0;
+      int a = 0, b = 0;
+      f3 o = F3(0.f, 0.f, 0.f), av = o, bv = o;
+      int vsv[MAXQ], vev[MAXQ];
+      float t0v[MAXQ], dtv[MAXQ], tmv[MAXQ];
+      if (p < npair) {
+        unrank2(p, ns, &a, &b);
+        uint32_t pm = (1u << a) | (1u << b);
+        bool conic_ok = true;
+        if (a == 0) nd.circle(b, &o, &av, &bv);
+        else conic_ok = nd.ellipse(a, b, &o, &av, &bv);
+        if (!conic_ok) {
+          for (int q = 0; q < nc; q++)
+            if ((ws.vmask[q] & pm) == pm) e = LMM_NODE_CONIC;
+        } else {
+          int Q[MAXQ];
+          float tq[MAXQ], us[MAXQ], uc[MAXQ];
+          int nq = 0;
+          for (int q = 0; q < nc && !e; q++)
+            if ((ws.vmask[q] & pm) == pm) {
+              if (nq >= MAXQ) { e = LMM_NODE_QCAP; break; }
+              Q[nq] = q;
+              tq[nq] = conic_t(o, av, bv, nd.V(q), &us[nq], &uc[nq]);
+              nq++;
+            }
+          if (!e) {
+            for (int i = 1; i < nq; i++)
+              for (int j = i; j > 0 && (tq[j] < tq[j - 1] || (tq[j] == tq[j - 1] && Q[j] < Q[j - 1])); j--) {
+                int ti = Q[j]; Q[j] = Q[j - 1]; Q[j - 1] = ti;
+                float tf = tq[j]; tq[j] = tq[j - 1]; tq[j - 1] = tf;
+                tf = us[j]; us[j] = us[j - 1]; us[j - 1] = tf;
+                tf = uc[j]; uc[j] = uc[j - 1]; uc[j - 1] = tf;
+              }
+            int nint = nq == 0 ? 1 : nq;
+            for (int i = 0; i < nint; i++) {
+              float ms, mc, t0, dt;
+              int vs, ve;
+              if (nq == 0) { ms = 0.0f; mc = 1.0f; t0 = 0.0f; dt = LMM_TWO_PI_F; vs = ve = -1; }
+              else if (nq == 1) { ms = -us[0]; mc = -uc[0]; t0 = tq[0]; dt = LMM_TWO_PI_F; vs = ve = Q[0]; }
+              else {
+                int j = (i + 1) % nq;
+                dt = j == 0 ? (tq[0] + LMM_TWO_PI_F) - tq[nq - 1] : tq[j] - tq[i];
+                if (!(dt > 0.0f)) { e = LMM_NODE_CHAIN; break; }
+                float sx = us[i] + us[j], sc = uc[i] + uc[j];
+                float l2 = sx * sx + sc * sc;
+                if (l2 > 1e-6f) {
+                  float l = sqrtf(l2);
+                  ms = sx / l; mc = sc / l;
+                  if (dt > LMM_PI_F) { ms = -ms; mc = -mc; }
+                } else { ms = uc[i]; mc = -us[i]; }
+                t0 = tq[i]; vs = Q[i]; ve = Q[j];
+              }
+              f3 y = F3((o.x + av.x * ms) + bv.x * mc, (o.y + av.y * ms) + bv.y * mc, (o.z + av.z * ms) + bv.z * mc);
+              float tmid = a == 0 ? 0.0f : nd.h(a, y);
+              bool ok = a == 0 ? nd.valid_sphere_pt(pm, y, delta) : nd.valid_strut_pt(pm, y, tmid, delta);
+              if (!ok) continue;
+              vsv[cnt] = vs; vev[cnt] = ve; t0v[cnt] = t0; dtv[cnt] = dt; tmv[cnt] = tmid;
+              if (vs < 0) closed = 1;
+              cnt++;
+            }
+          }
+        }
+      }
+      int tot, ctot;
+      int pos = na + excl_scan<G>(g, e ? 0 : cnt, &tot);
+      int spos = nv + excl_scan<G>(g, e ? 0 : closed, &ctot);
+      if (!e && cnt > 0 && pos + cnt > MAXA) e = LMM_NODE_ACAP;
+      if (!e && closed && spos >= MAXV) e = LMM_NODE_ACAP;
+      int fe = first_err<G>(g, e);
+      if (fe) { status = fe; break; }
+      for (int i = 0; i < cnt; i++) {
+        ArcRec &A = ws.arcs[pos + i];
+        int vs = vsv[i], ve = vev[i];
+        if (vs < 0) {
+          ws.vx[spos] = o.x + bv.x; ws.vy[spos] = o.y + bv.y; ws.vz[spos] = o.z + bv.z;
+          ws.vmask[spos] = (1u << a) | (1u << b);
+          vs = ve = spos;
+        }
+        A.ids = (uint32_t)a | ((uint32_t)b << 8) | ((uint32_t)vs << 16) | ((uint32_t)ve << 24);
+        A.t0 = t0v[i]; A.dt = dtv[i];
+        ws.atmid[pos + i] = tmv[i];
+        A.ox = o.x; A.oy = o.y; A.oz = o.z;
+        A.ax = av.x; A.ay = av.y; A.az = av.z;
+        A.bx = bv.x; A.by = bv.y; A.bz = bv.z;
+      }
+      na += tot;
+      nv += ctot;
+    }
+  }
+  g.sync();
+
+  // ambiguous strut-strut arcs running under a strictly exposed hole lune are dropped
+  // (R10): midpoint tangent length < delta and both end circles join its ends
+  if (status == 0 && na > 0) {
+    for (int i = lane; i < na; i += G) {
+      uint32_t ids = ws.arcs[i].ids;
+      int lo = ids & 0xff, hi = (ids >> 8) & 0xff, vs = (ids >> 16) & 0xff, ve = ids >> 24;
+      int drop = 0;
+      if (lo > 0 && vs != ve && ws.atmid[i] < delta) {
+        int ca = 0, cb = 0;
+        for (int j = 0; j < na; j++) {
+          uint32_t jd = ws.arcs[j].ids;
+          if ((jd & 0xff) != 0) continue;
+          int js = (jd >> 16) & 0xff, je = jd >> 24, jh = (jd >> 8) & 0xff;
+          if (!((js == vs && je == ve) || (js == ve && je == vs))) continue;
+          if (jh == lo) ca = 1;
+          if (jh == hi) cb = 1;
+        }
+        drop = ca && cb;
+      }
+      ws.adrop[i] = drop;
+    }
+    g.sync();
+    int w = 0;
+    for (int base = 0; base < na; base += G) {
+      int i = base + lane;
+      bool keep = i < na && !ws.adrop[i];
+      ArcRec rec;
+      if (keep) rec = ws.arcs[i];
+      unsigned km = g.ballot(keep);
+      g.sync();
+      if (keep) ws.arcs[w + __popc(km & ((1u << lane) - 1u))] = rec;
+      w += __popc(km);
+      g.sync();
+    }
+    na = w;
+  }
+  g.sync();
+
+  // every junction vertex must carry an arc
+  if (status == 0) {
+    int e = 0;
+    for (int q0 = 0; q0 < nc; q0 += G) {
+      int q = q0 + lane;
+      if (q < nc) {
+        bool used = false;
+        for (int i = 0; i < na && !used; i++) {
+          uint32_t ids = ws.arcs[i].ids;
+          used = (int)((ids >> 16) & 0xff) == q || (int)(ids >> 24) == q;
+        }
+        if (!used) e = LMM_NODE_UNREF;
+      }
+    }
+    if (g.any(e != 0)) status = LMM_NODE_UNREF;
+  }
+
+  // ---- 5. arc loops per strut end (ordered by angle around the strut axis) -----------
+  if (status == 0 && d > 0) {
+    for (int k0 = 0; k0 < d; k0 += G) {
+      int k = k0 + lane + 1;
+      int e = 0, cnt = 0;
+      int arcv[MAXLOOP], fwdv[MAXLOOP];
+      float psv[MAXLOOP], dpv[MAXLOOP];
+      if (k <= d) {
+        f3 as = nd.AS(k), e1 = nd.E1(k), e2 = nd.E2(k);
+        for (int i = 0; i < na; i++) {
+          const ArcRec &A = ws.arcs[i];
+          int lo = A.ids & 0xff, hi = (A.ids >> 8) & 0xff;
+          if (lo != k && hi != k) continue;
+          if (cnt >= MAXLOOP) { e = LMM_NODE_ACAP; break; }
+          int avs = (A.ids >> 16) & 0xff, ave = A.ids >> 24;
+          int fwd = f_dot(f_cross(F3(A.ax, A.ay, A.az), F3(A.bx, A.by, A.bz)), as) < 0.0f;
+          int vs = fwd ? avs : ave, ve = fwd ? ave : avs;
+          f3 Ps = nd.V(vs);
+          float ps = atan2p(f_dot(Ps, e2), f_dot(Ps, e1));
+          if (ps < 0.0f) ps += LMM_TWO_PI_F;
+          float dph;
+          if (vs == ve) dph = LMM_TWO_PI_F;
+          else {
+            f3 Pe = nd.V(ve);
+            float pe = atan2p(f_dot(Pe, e2), f_dot(Pe, e1));
+            if (pe < 0.0f) pe += LMM_TWO_PI_F;
+            dph = pe - ps;
+            if (dph <= 0.0f) dph += LMM_TWO_PI_F;
+          }
+          // insertion by (ps, arc index); arcs arrive in index order
+          int j = cnt;
+          while (j > 0 && ps < psv[j - 1]) {
+            arcv[j] = arcv[j - 1]; fwdv[j] = fwdv[j - 1]; psv[j] = psv[j - 1]; dpv[j] = dpv[j - 1];
+            j--;
+          }
+          arcv[j] = i; fwdv[j] = fwd; psv[j] = ps; dpv[j] = dph;
+          cnt++;
+        }
+        if (!e && cnt == 0) e = LMM_NODE_EMPTY;
+        if (!e) {
+          float sum = 0.0f;
+          for (int i = 0; i < cnt; i++) {
+            const ArcRec &X = ws.arcs[arcv[i]];
+            const ArcRec &Y = ws.arcs[arcv[(i + 1) % cnt]];
+            int xe = fwdv[i] ? (X.ids >> 24) : ((X.ids >> 16) & 0xff);
+            int ys = fwdv[(i + 1) % cnt] ? ((Y.ids >> 16) & 0xff) : (Y.ids >> 24);
+            if (xe != ys) { e = LMM_NODE_CHAIN; break; }
+            sum += dpv[i];
+          }
+          if (!e && fabsf(sum - LMM_TWO_PI_F) > 1e-3f) e = LMM_NODE_ANGLE;
+        }
+      }
+      int tot;
+      int pos = nle + excl_scan<G>(g, e ? 0 : cnt, &tot);
+      if (!e && cnt > 0 && pos + cnt > MAXLE) e = LMM_NODE_ACAP;
+      int fe = first_err<G>(g, e);
+      if (fe) { status = fe; break; }
+      if (k <= d) {
+        ws.lfirst[k] = pos;
+        ws.lcount[k] = cnt;
+        float ph = psv[0];
+        for (int i = 0; i < cnt; i++) {
+          if (i > 0) ph = ph + dpv[i - 1];
+          LoopRec &L = ws.le[pos + i];
+          L.arc_fwd = (uint32_t)arcv[i] | ((uint32_t)fwdv[i] << 16);
+          L.phs = ph;
+          L.dph = dpv[i];
+          L.cum = 0;
+        }
+      }
+      nle += tot;
+    }
+  }
+  g.sync();
+
+  // ---- 6. hole contours: cap arcs chained around the exposed sphere (lane 0) --------
+  if (status == 0 && d > 0) {
+    int st = 0;
+    if (lane == 0) {
+      uint64_t used = 0;   // MAXA <= 64 tracked per word below
+      uint64_t usedw[(MAXA + 63) / 64];
+      for (int i = 0; i < (MAXA + 63) / 64; i++) usedw[i] = 0;
+      (void)used;
+      for (int i = 0; i < na && !st; i++) {
+        const ArcRec &Ai = ws.arcs[i];
+        if ((Ai.ids & 0xff) != 0 || ((usedw[i >> 6] >> (i & 63)) & 1)) continue;
+        if (nh >= MAXH) { st = LMM_NODE_ACAP; break; }
+        ws.hoff[nh++] = nhe;
+        int cur = i;
+        int hb0 = (Ai.ids >> 8) & 0xff;
+        int hf0 = ws.sign[hb0] < 0;
+        int start_v = hf0 ? ((Ai.ids >> 16) & 0xff) : (Ai.ids >> 24);
+        for (;;) {
+          usedw[cur >> 6] |= 1ull << (cur & 63);
+          const ArcRec &C = ws.arcs[cur];
+          int hf = ws.sign[(C.ids >> 8) & 0xff] < 0;
+          ws.he[nhe++] = (uint32_t)cur | ((uint32_t)hf << 16);
+          int endv = hf ? (C.ids >> 24) : ((C.ids >> 16) & 0xff);
+          if (endv == start_v) break;
+          int nxt = -1;
+          for (int j = 0; j < na && nxt < 0; j++) {
+            const ArcRec &Aj = ws.arcs[j];
+            if ((Aj.ids & 0xff) != 0 || ((usedw[j >> 6] >> (j & 63)) & 1)) continue;
+            int hj = ws.sign[(Aj.ids >> 8) & 0xff] < 0;
+            if ((hj ? ((Aj.ids >> 16) & 0xff) : (Aj.ids >> 24)) == endv) nxt = j;
+          }
+          if (nxt < 0) { st = LMM_NODE_HOLE; break; }
+          cur = nxt;
+        }
+      }
+      ws.hoff[nh] = nhe;
+    }
+    st = g.shfl(st, 0);
+    nh = g.shfl(nh, 0);
+    nhe = g.shfl(nhe, 0);
+    if (st) status = st;
+  }
+  g.sync();
+
+  // ---- 7. write the node's slabs ----------------------------------------------------
+  if (status == 0 && (nv > slab_cap(d, SLAB_V_K, SLAB_V_K0) || na > slab_cap(d, SLAB_A_K, SLAB_A_K0) ||
+                      nle > slab_cap(d, SLAB_L_K, SLAB_L_K0) || nh > slab_cap(d, SLAB_H_K, SLAB_H_K0) ||
+                      nhe > slab_cap(d, SLAB_HE_K, SLAB_HE_K0)))
+    status = LMM_NODE_ACAP;
+  if (status != 0) { nv = na = nle = nh = nhe = 0; }
+  if (lane == 0)
+    P.node_hdr[n] = make_int4(status | (d << 8), nv | (na << 16), nh | (nle << 16), nhe);
+  const int64_t vb = slab_base(off, n, SLAB_V_K, SLAB_V_K0);
+  const int64_t ab = slab_base(off, n, SLAB_A_K, SLAB_A_K0);
+  const int64_t lb = slab_base(off, n, SLAB_L_K, SLAB_L_K0);
+  const int64_t hb = slab_base(off, n, SLAB_H_K, SLAB_H_K0);
+  const int64_t heb = slab_base(off, n, SLAB_HE_K, SLAB_HE_K0);
+  for (int q = lane; q < nv; q += G) P.vert[vb + q] = make_float4(ws.vx[q], ws.vy[q], ws.vz[q], __uint_as_float(ws.vmask[q]));
+  {
+    const uint32_t *src = reinterpret_cast<const uint32_t *>(ws.arcs);
+    uint32_t *dst = reinterpret_cast<uint32_t *>(P.arc + ab);
+    for (int q = lane; q < na * 12; q += G) dst[q] = src[q];
+  }
+  for (int q = lane; q < nle; q += G) P.loop[lb + q] = ws.le[q];
+  for (int k = lane; k < d; k += G)
+    P.loop_hdr[off + k] = status == 0 ? make_int2(ws.lfirst[k + 1], ws.lcount[k + 1]) : make_int2(0, 0);
+  for (int h = lane; h < nh; h += G) P.hole_hdr[hb + h] = make_int2(ws.hoff[h], ws.hoff[h + 1] - ws.hoff[h]);
+  for (int q = lane; q < nhe; q += G) { HoleEnt he; he.arc_fwd = ws.he[q]; he.cum = 0; P.hole_ent[heb + q] = he; }
+  g.sync();
+}
+
+template <int G, int MAXS, int MAXJ, int MAXV, int MAXA, int MAXLE, int MAXH>
+__global__ void __launch_bounds__(128) metamesh_kernel(MMParams P) {
+  using WS = NodeWS<MAXS, MAXJ, MAXV, MAXA, MAXLE, MAXH>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  auto block = cg::this_thread_block();
+  cg::thread_block_tile<G> g = cg::tiled_partition<G>(block);
+  const int gid_in_block = threadIdx.x / G;
+  WS &ws = reinterpret_cast<WS *>(smem_raw)[gid_in_block];
+  const int groups_per_block = blockDim.x / G;
+  const int gid = blockIdx.x * groups_per_block + gid_in_block;
+  const int ngroups = gridDim.x * groups_per_block;
+  for (int i = gid; i < P.n_list; i += ngroups) process_node<G>(g, ws, P, P.node_list[i]);
+}
+
+// nodes of degree 0 or > LMM_MAXD
+__global__ void trivial_nodes_kernel(const int *csr_off, int N, int4 *node_hdr, int2 *loop_hdr) {
+  int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= N) return;
+  int d = csr_off[n + 1] - csr_off[n];
+  if (d == 0) node_hdr[n] = make_int4(0, 0, 0, 0);
+  else if (d > LMM_MAXD) {
+    node_hdr[n] = make_int4(LMM_NODE_DEGREE | (d << 8), 0, 0, 0);
+    for (int k = 0; k < d; k++) loop_hdr[csr_off[n] + k] = make_int2(0, 0);
+  }
+}
+
+template <int G, int MAXS, int MAXJ, int MAXV, int MAXA, int MAXLE, int MAXH>
+int launch_bucket(lmm_ctx *c, MMParams P) {
+  using WS = NodeWS<MAXS, MAXJ, MAXV, MAXA, MAXLE, MAXH>;
+  if (P.n_list <= 0) return LMM_OK;
+  const int threads = 128;
+  const int groups = threads / G;
+  size_t smem = sizeof(WS) * groups;
+  auto kern = metamesh_kernel<G, MAXS, MAXJ, MAXV, MAXA, MAXLE, MAXH>;
+  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int occ = 0;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem));
+  if (occ < 1) occ = 1;
+  int64_t need = (P.n_list + groups - 1) / groups;
+  int64_t grid = (int64_t)c->n_sm * occ;
+  if (grid > need) grid = need;
+  (c->n_launch++), kern<<<(unsigned)grid, threads, smem, c->stream>>>(P);
+  CUDA_TRY(cudaGetLastError());
+  return LMM_OK;
+}
+
+}  // namespace
+
+int metamesh_run(lmm_ctx *c) {
+  MMParams P;
+  P.node = (const float4 *)c->node.p;
+  P.csr_off = (const int *)c->csr_off.p;
+  P.csr_ent = (const int2 *)c->csr_ent.p;
+  P.ends = (const int2 *)c->ends.p;
+  P.node_hdr = (int4 *)c->node_hdr.p;
+  P.vert = (float4 *)c->vert.p;
+  P.arc = (ArcRec *)c->arc.p;
+  P.loop_hdr = (int2 *)c->loop_hdr.p;
+  P.loop = (LoopRec *)c->loop.p;
+  P.hole_hdr = (int2 *)c->hole_hdr.p;
+  P.hole_ent = (HoleEnt *)c->hole_ent.p;
+  const int *bn = (const int *)c->bucket_nodes.p;
+  int rc;
+  {
+    KTimer t(c, LMM_K_METAMESH);
+    if (c->N > 0) {
+      (c->n_launch++), trivial_nodes_kernel<<<(unsigned)((c->N + 255) / 256), 256, 0, c->stream>>>(
+          (const int *)c->csr_off.p, (int)c->N, (int4 *)c->node_hdr.p, (int2 *)c->loop_hdr.p);
+      CUDA_TRY(cudaGetLastError());
+    }
+    // bucket b occupies bucket_nodes[bucket_off[b] .. bucket_off[b+1])
+    P.node_list = bn + c->bucket_off[0];
+    P.n_list = (int)(c->bucket_off[1] - c->bucket_off[0]);
+    if ((rc = launch_bucket<32, 9, 96, 18, 26, 52, 18>(c, P))) return rc;
+    P.node_list = bn + c->bucket_off[1];
+    P.n_list = (int)(c->bucket_off[2] - c->bucket_off[1]);
+    if ((rc = launch_bucket<32, 17, 192, 34, 50, 100, 34>(c, P))) return rc;
+    P.node_list = bn + c->bucket_off[2];
+    P.n_list = (int)(c->bucket_off[3] - c->bucket_off[2]);
+    if ((rc = launch_bucket<32, 32, 448, 64, 95, 190, 64>(c, P))) return rc;
+  }
+  return LMM_OK;
+}

@@ -1,0 +1,62 @@
+"""CPU-side checks of the boundary: liblmm.so builds for sm_100a, loads, and exports every
+function include/lmm.h declares; the product package never imports the oracle."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "lmm.h")).read()
+    return sorted(set(re.findall(r"LMM_API\s+[\w\s\*]+?\b(lmm_\w+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2405_15197_b200 import build as b
+    return b.build()
+
+
+def test_header_declares_the_problem_statement_calls():
+    names = _declared()
+    for must in ("lmm_create", "lmm_load_lattice", "lmm_build_metamesh", "lmm_triangulate", "lmm_write_triangles",
+                 "lmm_destroy"):
+        assert must in names
+
+
+def test_library_exports_every_declared_symbol(lib):
+    out = subprocess.run(["nm", "-D", "--defined-only", lib], capture_output=True, text=True, check=True).stdout
+    exported = set(re.findall(r"\bT (lmm_\w+)", out))
+    missing = [n for n in _declared() if n not in exported]
+    assert not missing, missing
+    h = ctypes.CDLL(lib)
+    for n in _declared():
+        getattr(h, n)
+
+
+def test_library_is_sm100a_code(lib):
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", lib], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_no_gpu_means_loud_failure(lib):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_2405_15197_b200 import LmmError, lmm_create
+    with pytest.raises(LmmError):
+        lmm_create(0)
+
+
+def test_product_package_does_not_import_oracle():
+    pkg = os.path.join(ROOT, "paper_2405_15197_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert not re.search(r"^\s*(import|from)\s+oracle", txt, re.M), f
+                assert "mm_oracle" not in txt and "liborc" not in txt, f

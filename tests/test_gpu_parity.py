@@ -1,0 +1,172 @@
+"""Parity of the CUDA path (through the C-ABI) with the CPU oracle.
+
+Topology -- vertex/arc/hole counts, tie masks, arc endpoints, loop order, hole contours,
+per-arc parameter ranges and stitch angles (binary32 decision values), subdivision
+counts, band sizes and rotations, triangle offsets -- must be bit-exact.  Geometry: the
+kernel's binary32 against the oracle's binary64 within 1e-4 x the minimum strut radius
+(north star), plus the binary32 rounding of absolute coordinates for triangles.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+GEOM_TOL = 1e-4
+
+
+def _lat(name):
+    return {
+        "single": lambda: synth.single_strut(1.0, 0.1, 0.1),
+        "cone": lambda: synth.single_strut(1.0, 0.1, 0.06),
+        "chain-bent": lambda: synth.chain(5, 1.0, 0.1, 50.0),
+        "star-bcc": lambda: synth.star([[1, 1, 1], [1, 1, -1], [1, -1, 1], [1, -1, -1], [-1, 1, 1], [-1, 1, -1],
+                                        [-1, -1, 1], [-1, -1, -1]], 1.0, 0.1),
+        "cubic3": lambda: synth.cubic(3, 3, 3),
+        "bcc3": lambda: synth.bcc(3, 3, 3),
+        "octet2": lambda: synth.octet(2, 2, 2),
+        "octet2-graded": lambda: synth.graded_radii(synth.octet(2, 2, 2), 0.03, 0.06),
+        "bcc3-jitter": lambda: synth.jitter(synth.bcc(3, 3, 3), 0.05, 1),
+        "cubic4-graded-jitter": lambda: synth.jitter(synth.graded_radii(synth.cubic(4, 4, 4), 0.06, 0.12, 2), 0.04, 2),
+        "voronoi": lambda: synth.voronoi_like(300, seed=3, radius=0.05),
+        # BASELINE.json configs[0]: 10x10x10 BCC, uniform radius, eps = 1e-3 r
+        "bcc10": lambda: synth.bcc(10, 10, 10),
+    }[name]()
+
+
+NAMES = ["single", "cone", "chain-bent", "star-bcc", "cubic3", "bcc3", "octet2", "octet2-graded", "bcc3-jitter",
+         "cubic4-graded-jitter", "voronoi", "bcc10"]
+
+
+@pytest.fixture(scope="module")
+def built():
+    from paper_2405_15197_b200 import build as b
+    b.build()
+    cache = {}
+
+    def get(name):
+        if name not in cache:
+            from paper_2405_15197_b200 import MetaMesher
+            lat = _lat(name)
+            mm = MetaMesher(0).load_lattice(lat).build()
+            orc = oracle.Oracle.from_lattice(lat)
+            orc.metamesh()
+            cache[name] = (lat, mm, orc, mm.buffers())
+        return cache[name]
+    return get
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_metamesh_topology_bit_exact_and_geometry(built, name):
+    from paper_2405_15197_b200 import decode_node
+    lat, mm, orc, bufs = built(name)
+    tol = GEOM_TOL * float(lat.node_r.min())
+    for n in range(lat.n_nodes):
+        g, o = decode_node(bufs, n), orc.node(n)
+        assert (g["status"], g["d"]) == (o["status"], o["d"]), (n, g["status"], o["status"])
+        if o["status"]:
+            continue
+        assert (g["nv"], g["na"], g["nh"]) == (o["nv"], o["na"], o["nh"]), n
+        assert np.array_equal(g["v_mask"], o["v_mask"]), n
+        assert np.array_equal(g["v_pos32"].view(np.uint32), o["v_pos32"].view(np.uint32)), n
+        assert np.array_equal(g["a_int"], o["a_int"]), n
+        assert np.array_equal(g["a_f32"].view(np.uint32), o["a_f32"].view(np.uint32)), n   # t0, dt, conic (binary32)
+        assert np.array_equal(g["loop_off"], o["loop_off"]), n
+        assert np.array_equal(g["l_int"], o["l_int"]), n
+        assert np.array_equal(g["l_f32"].view(np.uint32), o["l_f32"].view(np.uint32)), n
+        assert np.array_equal(g["hole_off"], o["hole_off"]) and np.array_equal(g["h_int"], o["h_int"]), n
+        # geometry: binary32 kernel vs binary64 oracle
+        if g["nv"]:
+            assert np.max(np.abs(g["v_pos32"] - o["v_pos64"])) < tol, n
+        if g["na"]:
+            assert np.max(np.abs(g["a_f32"][:, 2:] - o["a_f64"][:, 2:])) < tol, n
+
+
+def _mesh_edges_ok(tris):
+    V = tris[:, 1:, :].reshape(-1, 3)
+    uniq, inv = np.unique(V, axis=0, return_inverse=True)
+    F = inv.reshape(-1, 3)
+    e = np.sort(np.concatenate([F[:, [0, 1]], F[:, [1, 2]], F[:, [2, 0]]]), axis=1)
+    eu, cnt = np.unique(e, axis=0, return_counts=True)
+    return set(cnt.tolist()), len(uniq) - len(eu) + len(F)
+
+
+@pytest.mark.parametrize("name", NAMES)
+@pytest.mark.parametrize("ce", [1e-2, 1e-3])
+def test_triangulation_parity(built, name, ce):
+    lat, mm, orc, _ = built(name)
+    assert mm.stats()["n_error_nodes"] == 0
+    T = mm.triangulate(ce)
+    To = orc.triangulate(ce)
+    assert T == To
+    tb = mm.tri_buffers()
+    bn, soff = orc.band_info()
+    assert np.array_equal(tb["band"][:, :3].astype(np.int64), bn)
+    assert np.array_equal(tb["strut_off"], soff)
+    base, M, bp = orc.hole_info()
+    assert np.array_equal(tb["hole_M"].astype(np.int64), M)
+    assert np.array_equal(tb["node_hole0"], base)
+    tri = mm.triangles(0, T).astype(np.float64)
+    ref = orc.write_triangles()
+    r = float(lat.node_r.min())
+    tol = GEOM_TOL * r + 4e-7 * np.abs(ref[:, 1:]).max()
+    assert np.max(np.abs(tri[:, 1:] - ref[:, 1:])) < tol
+    # facet normals agree wherever the facet is not tiny
+    # facet normals: error bounded by vertex error / shortest altitude
+    v1, v2, v3 = ref[:, 1], ref[:, 2], ref[:, 3]
+    area2 = np.linalg.norm(np.cross(v2 - v1, v3 - v1), axis=1)
+    longest = np.max(np.stack([np.linalg.norm(v2 - v1, axis=1), np.linalg.norm(v3 - v2, axis=1),
+                               np.linalg.norm(v1 - v3, axis=1)]), axis=0)
+    alt = area2 / np.maximum(longest, 1e-300)
+    verr = np.max(np.abs(tri[:, 1:] - ref[:, 1:]), axis=(1, 2))
+    ok = alt > 0
+    nerr = np.max(np.abs(tri[ok, 0] - ref[ok, 0]), axis=1)
+    assert np.all(nerr <= 4 * verr[ok] / alt[ok] + 1e-5)
+    # the kernel's own output is watertight: welded by exact binary32 coordinates
+    counts, chi = _mesh_edges_ok(mm.triangles(0, T))
+    assert counts == {2}
+    assert chi == 2 - 2 * lat.genus()
+
+
+@pytest.mark.parametrize("ce", [1e-2, 1e-3])
+def test_ranges_and_device_output(built, ce):
+    """Arbitrary [first, first+count) windows equal the full emission; device destination."""
+    import torch
+    lat, mm, orc, _ = built("bcc3-jitter")
+    T = mm.triangulate(ce)
+    full = mm.triangles(0, T)
+    rng = np.random.default_rng(0)
+    for _ in range(20):
+        a = int(rng.integers(0, T))
+        b = int(rng.integers(a, min(T, a + 5000) + 1))
+        assert np.array_equal(mm.triangles(a, b - a).view(np.uint32), full[a:b].view(np.uint32))
+    dev = torch.zeros(T * 50 + 16, dtype=torch.uint8, device="cuda")
+    mm.write(0, T, dev)
+    torch.cuda.synchronize()
+    from paper_2405_15197_b200 import stl_records_to_array
+    got = stl_records_to_array(dev[: T * 50].cpu().numpy())
+    assert np.array_equal(got.view(np.uint32), full.view(np.uint32))
+
+
+def test_remesh_reuses_metamesh(built):
+    """Algorithm 1: a chord-error list re-triangulates one meta-mesh; counts are monotone."""
+    lat, mm, orc, _ = built("octet2-graded")
+    counts = [mm.triangulate(ce) for ce in (1e-4, 1e-3, 1e-2, 5e-2)]
+    assert all(a >= b for a, b in zip(counts, counts[1:]))
+    assert counts[-1] == orc.triangulate(5e-2)
+
+
+def test_csr_offsets_are_the_degree_prefix_sum(built):
+    """PAPER.md Sec. 4.3.2 index region = exclusive prefix sum (device scan), here of the
+    node degrees; incident struts ascending per node."""
+    from paper_2405_15197_b200 import lmm_buffer
+    from paper_2405_15197_b200 import binding as B
+    lat, mm, orc, _ = built("voronoi")
+    off = lmm_buffer(mm.h, B.LMM_BUF_CSR_OFF, np.int32)
+    ent = lmm_buffer(mm.h, B.LMM_BUF_CSR_ENT, np.int32, 2)
+    assert np.array_equal(off.astype(np.int64), np.concatenate([[0], np.cumsum(lat.degrees())]))
+    o_off, o_st = orc.csr()
+    assert np.array_equal(off.astype(np.int64), o_off)
+    assert np.array_equal(ent[:, 0].astype(np.int64), o_st)
