@@ -474,8 +474,18 @@ static int valid_strut_pt(const side32 *S, int d, uint32_t excl, f3 y, float tau
   }
   return 1;
 }
-/* a point of the nodal sphere is exposed only if every other strut is below it by
- * more than delta: ties with the sphere go to the struts (zero-area holes vanish). */
+/* sphere junction (sphere, b, c): no other strut above the sphere by more than delta
+ * (tolerant, like strut junctions: near-coincident junctions then cluster into one
+ * vertex of higher valence). */
+static int valid_sphere_junction(const side32 *S, int d, uint32_t excl, f3 y, float delta) {
+  for (int m = 1; m <= d; m++) {
+    if (excl & (1u << m)) continue;
+    if (h32(S, m, y) > delta) return 0;
+  }
+  return 1;
+}
+/* a point of an end circle is exposed only if every other strut is below it by more
+ * than delta: ties with the sphere go to the struts (zero-area holes vanish). */
 static int valid_sphere_pt(const side32 *S, int d, uint32_t excl, f3 y, float delta) {
   for (int m = 1; m <= d; m++) {
     if (excl & (1u << m)) continue;
@@ -514,7 +524,7 @@ static int node_metamesh(orc_lat *L, int64_t n) {
         if (!junction32(S, R, a, b, c, y, tau)) continue;
         uint32_t excl = (1u << a) | (1u << b) | (1u << c);
         for (int r = 0; r < 2; r++) {
-          int ok = a == 0 ? valid_sphere_pt(S, d, excl, y[r], delta)
+          int ok = a == 0 ? valid_sphere_junction(S, d, excl, y[r], delta)
                           : valid_strut_pt(S, d, excl, y[r], tau[r], delta);
           if (!ok) continue;
           if (nj >= ORC_MAXJ) { free(J); M->status = ORC_E_JCAP; return M->status; }

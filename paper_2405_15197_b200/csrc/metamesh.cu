@@ -111,6 +111,15 @@ template <class WS> struct Node {
     }
     return true;
   }
+  // sphere junction: tolerant (no other strut above the sphere by more than delta)
+  __device__ bool valid_sphere_junction(uint32_t excl, f3 y, float delta) const {
+    for (int m = 1; m <= d; m++) {
+      if (excl & (1u << m)) continue;
+      if (h(m, y) > delta) return false;
+    }
+    return true;
+  }
+  // end-circle (cap) point: strictly exposed
   __device__ bool valid_sphere_pt(uint32_t excl, f3 y, float delta) const {
     for (int m = 1; m <= d; m++) {
       if (excl & (1u << m)) continue;
@@ -299,7 +308,7 @@ __device__ void process_node(cg::thread_block_tile<G> &g, NodeWS<MAXS, MAXJ, MAX
         if (nd.junction(a, b, c, y, tau)) {
           uint32_t excl = (1u << a) | (1u << b) | (1u << c);
           for (int r = 0; r < 2; r++) {
-            bool ok = a == 0 ? nd.valid_sphere_pt(excl, y[r], delta) : nd.valid_strut_pt(excl, y[r], tau[r], delta);
+            bool ok = a == 0 ? nd.valid_sphere_junction(excl, y[r], delta) : nd.valid_strut_pt(excl, y[r], tau[r], delta);
             if (!ok) continue;
             bool sh = false;
             int ks[3] = {a, b, c};
