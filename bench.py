@@ -217,7 +217,6 @@ def main():
     for _ in range(max(args.warmup, 0)):
         T = step()
     torch.cuda.synchronize()
-    st = B.lmm_metamesh_stats(h)
     B.lmm_reset_kernel_times(h)
     B.lmm_timing(h, True)
     l0 = B.lmm_launch_count(h)
@@ -235,6 +234,7 @@ def main():
             dist.barrier()
     B.lmm_timing(h, False)
     launches = B.lmm_launch_count(h) - l0
+    st = B.lmm_metamesh_stats(h)
     ms = ev0.elapsed_time(ev1) / args.steps
     kt = B.lmm_kernel_times(h)
     t = torch.tensor([ms], dtype=torch.float64, device="cuda")

@@ -557,12 +557,23 @@ static int node_metamesh(orc_lat *L, int64_t n) {
   free(J);
   int nv = nc;
 
-  /* 3. arcs: for every pair of sides, walk the conic through its vertices */
+  /* 3. arcs: for every pair of sides, walk the conic through its vertices.  A conic
+   * carrying no vertex can only be one closed arc, which is then the whole loop of its
+   * strut side(s): it is tested only when its strut sides appear in no vertex. */
   arc_t *A = (arc_t *)calloc(ORC_MAXA, sizeof(arc_t));
   int na = 0;
+  uint32_t in_vertex = 0;
+  for (int q = 0; q < nc; q++) in_vertex |= V[q].mask;
   for (int a = 0; a <= d; a++)
     for (int b = a + 1; b <= d; b++) {
       f3 o, av, bv;
+      {
+        uint32_t pm0 = (1u << a) | (1u << b);
+        int has = 0;
+        for (int q = 0; q < nc && !has; q++) has = (V[q].mask & pm0) == pm0;
+        uint32_t strut_bits = a == 0 ? (1u << b) : pm0;
+        if (!has && (in_vertex & strut_bits)) continue;
+      }
       if (a == 0) circle32(S, R, b, &o, &av, &bv);
       else if (!ellipse32(S, R, a, b, &o, &av, &bv)) {
         /* a pair whose plane section is unbounded cannot carry an arc only if no

@@ -133,8 +133,9 @@ int lattice_build(lmm_ctx *c, const float *xyz, const int64_t *ends, const float
   if (S) (c->n_launch++), k_scatter_r<<<(unsigned)((S + T - 1) / T), T, 0, c->stream>>>((const int2 *)c->ends.p, rend, S, (float4 *)c->node.p);
   if (S) (c->n_launch++), k_check_r<<<(unsigned)((S + T - 1) / T), T, 0, c->stream>>>((const int2 *)c->ends.p, rend, S, (const float4 *)c->node.p, bad + 1);
   CUDA_TRY(cudaGetLastError());
-  int hbad[2] = {0, 0};
-  CUDA_TRY(cudaMemcpyAsync(hbad, bad, sizeof(hbad), cudaMemcpyDeviceToHost, c->stream));
+  if (!c->pinned_scalar) CUDA_TRY(cudaMallocHost((void **)&c->pinned_scalar, 64));
+  int *hbad = (int *)(c->pinned_scalar + 4);
+  CUDA_TRY(cudaMemcpyAsync(hbad, bad, 2 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
   if (hbad[0]) return LMM_E_ARG;
   if (hbad[1]) return LMM_E_RADIUS;
@@ -167,17 +168,18 @@ int degree_buckets(lmm_ctx *c) {
     if (grid > c->n_sm * 8) grid = c->n_sm * 8;
     (c->n_launch++), k_deg_hist<<<grid, T, 0, c->stream>>>((const int *)c->csr_off.p, N, (unsigned long long *)c->deg_hist.p);
   }
-  unsigned long long h[33];
-  CUDA_TRY(cudaMemcpyAsync(h, c->deg_hist.p, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+  if (!c->pinned_hist) CUDA_TRY(cudaMallocHost((void **)&c->pinned_hist, 64 * sizeof(unsigned long long)));
+  unsigned long long *h = c->pinned_hist;
+  CUDA_TRY(cudaMemcpyAsync(h, c->deg_hist.p, 33 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
   int64_t cnt[LMM_NBUCKET] = {0, 0, 0};
   for (int d = 1; d <= 31; d++) cnt[d <= 8 ? 0 : (d <= 16 ? 1 : 2)] += (int64_t)h[d];
   c->bucket_off[0] = 0;
   for (int b = 0; b < LMM_NBUCKET; b++) c->bucket_off[b + 1] = c->bucket_off[b] + cnt[b];
-  int base[LMM_NBUCKET];
+  int *base = (int *)(c->pinned_hist + 40);
   for (int b = 0; b < LMM_NBUCKET; b++) base[b] = (int)c->bucket_off[b];
   int *dbase = (int *)c->bucket_cnt.p + 8;
-  CUDA_TRY(cudaMemcpyAsync(dbase, base, sizeof(base), cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(dbase, base, LMM_NBUCKET * sizeof(int), cudaMemcpyHostToDevice, c->stream));
   if (N) (c->n_launch++), k_bucket_fill<<<(unsigned)((N + T - 1) / T), T, 0, c->stream>>>((const int *)c->csr_off.p, N, dbase, (int *)c->bucket_cnt.p, (int *)c->bucket_nodes.p);
   CUDA_TRY(cudaGetLastError());
   return LMM_OK;

@@ -97,7 +97,7 @@ static void free_all(lmm_ctx *c) {
   DevBuf *bufs[] = {&c->node, &c->ends, &c->csr_off, &c->csr_ent, &c->strut_csr, &c->deg_hist, &c->bucket_nodes,
                     &c->bucket_cnt, &c->node_hdr, &c->vert, &c->arc, &c->loop_hdr, &c->loop, &c->hole_hdr,
                     &c->hole_ent, &c->band, &c->strut_off, &c->node_hole0, &c->node_hole0_64, &c->hole_M,
-                    &c->hole_off, &c->hole_bp, &c->hole_node, &c->tmp64, &c->scratch, &c->stage[0], &c->stage[1]};
+                    &c->hole_off, &c->hole_bp, &c->hole_node, &c->mbits, &c->macc, &c->cmap, &c->tmp64, &c->scratch, &c->scan_tmp, &c->stage[0], &c->stage[1]};
   for (DevBuf *b : bufs) dev_free(*b);
 }
 
@@ -112,6 +112,8 @@ LMM_API void lmm_destroy(lmm_ctx *c) {
   }
   resolve_timers(c);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+  if (c->pinned_scalar) cudaFreeHost(c->pinned_scalar);
+  if (c->pinned_hist) cudaFreeHost(c->pinned_hist);
   delete c;
 }
 

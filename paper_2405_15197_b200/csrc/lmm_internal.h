@@ -50,11 +50,17 @@ struct lmm_ctx {
   DevBuf hole_off;   // int64 [H+1]
   DevBuf hole_bp;    // float4 [H]
   DevBuf hole_node;  // int [H]
+  DevBuf mbits;      // uint32 merge bits (1 per band triangle)
+  DevBuf macc;       // int per merge word
+  DevBuf cmap;       // int per emit chunk
   int64_t H = 0, n_tri = 0, n_tri_band = 0;
   bool tri_ok = false;
   // scratch
   DevBuf tmp64;      // int64 scan scratch
   DevBuf scratch;    // misc
+  DevBuf scan_tmp;   // scan tile sums (all recursion levels)
+  int64_t *pinned_scalar = nullptr;   // pinned host words for scan totals / flags
+  unsigned long long *pinned_hist = nullptr;   // pinned degree histogram + bucket bases
   DevBuf stage[2];   // device staging for host output
   void *pinned[2] = {nullptr, nullptr};
   size_t pinned_bytes = 0;

@@ -12,6 +12,7 @@
 // the topology decisions are bit-identical to the specification (and to the CPU
 // oracle's, which evaluates the same operations).
 #include <cooperative_groups.h>
+#include <cooperative_groups/reduce.h>
 
 #include "lmm_internal.h"
 
@@ -53,6 +54,13 @@ struct alignas(16) NodeWS {
   ArcRec arcs[MAXA];
   float atmid[MAXA];
   int adrop[MAXA];
+  // arc walk: incidences (cluster ids) counting-sorted by side pair
+  int pcnt[MAXS * (MAXS - 1) / 2], pofs[MAXS * (MAXS - 1) / 2], pfill[MAXS * (MAXS - 1) / 2];
+  int plist[MAXS * (MAXS - 1) / 2];
+  int inc[4 * MAXV];
+  // loop entries of every (arc, side): phi start, span, forward flag
+  float eps[2 * MAXA], edp[2 * MAXA];
+  uint8_t efw[2 * MAXA];
   LoopRec le[MAXLE];
   int lfirst[MAXS], lcount[MAXS];
   int hoff[MAXH + 1];
@@ -230,6 +238,12 @@ __device__ __forceinline__ void unrank2(int t, int n, int *a, int *b) {
 
 #define MAXQ 16
 #define MAXLOOP 32
+#define MAXINC (4 * MAXV)
+
+__device__ __forceinline__ int rank2(int a, int b, int n) {
+  // lexicographic index of pair (a < b) among the pairs of {0..n-1}
+  return a * (2 * n - a - 1) / 2 + (b - a - 1);
+}
 
 template <int G, int MAXS, int MAXJ, int MAXV, int MAXA, int MAXLE, int MAXH>
 __device__ void process_node(cg::thread_block_tile<G> &g, NodeWS<MAXS, MAXJ, MAXV, MAXA, MAXLE, MAXH> &ws,
@@ -369,44 +383,103 @@ __device__ void process_node(cg::thread_block_tile<G> &g, NodeWS<MAXS, MAXJ, MAX
   nv = nc;
   g.sync();
 
-  // ---- 4. arcs: every side pair walks its conic through its vertices --------------
+  // ---- 4. arcs: conics walked through their vertices, incidence-driven --------------
+  // Clusters enumerate the side pairs of their tie sets (counting sort by pair), the
+  // pairs with vertices -- plus pairs of sides that appear in no vertex (only these can
+  // carry a closed arc) -- are compacted in lexicographic order and walked densely.
   if (status == 0 && d > 0) {
     const int npair = ns * (ns - 1) / 2;
+    uint32_t um = 0;
+    for (int q = lane; q < nc; q += G) um |= ws.vmask[q];
+    um = cg::reduce(g, um, cg::bit_or<uint32_t>());
+    for (int p = lane; p < npair; p += G) { ws.pcnt[p] = 0; ws.pfill[p] = 0; }
+    g.sync();
+    for (int q = lane; q < nc; q += G) {
+      uint32_t m = ws.vmask[q];
+      for (uint32_t ma = m; ma; ma &= ma - 1) {
+        int a = __ffs(ma) - 1;
+        for (uint32_t mb = ma & (ma - 1); mb; mb &= mb - 1) {
+          int b = __ffs(mb) - 1;
+          atomicAdd(&ws.pcnt[rank2(a, b, ns)], 1);
+        }
+      }
+    }
+    g.sync();
+    int ninc = 0;
     for (int base = 0; base < npair; base += G) {
       int p = base + lane;
-      int e = 0, cnt = 0, closed = 0;
-      int a = 0, b = 0;
-      f3 o = F3(0.f, 0.f, 0.f), av = o, bv = o;
-      int vsv[MAXQ], vev[MAXQ];
-      float t0v[MAXQ], dtv[MAXQ], tmv[MAXQ];
-      if (p < npair) {
-        unrank2(p, ns, &a, &b);
-        uint32_t pm = (1u << a) | (1u << b);
-        bool conic_ok = true;
-        if (a == 0) nd.circle(b, &o, &av, &bv);
-        else conic_ok = nd.ellipse(a, b, &o, &av, &bv);
-        if (!conic_ok) {
-          for (int q = 0; q < nc; q++)
-            if ((ws.vmask[q] & pm) == pm) e = LMM_NODE_CONIC;
-        } else {
-          int Q[MAXQ];
-          float tq[MAXQ], us[MAXQ], uc[MAXQ];
-          int nq = 0;
-          for (int q = 0; q < nc && !e; q++)
-            if ((ws.vmask[q] & pm) == pm) {
-              if (nq >= MAXQ) { e = LMM_NODE_QCAP; break; }
-              Q[nq] = q;
-              tq[nq] = conic_t(o, av, bv, nd.V(q), &us[nq], &uc[nq]);
-              nq++;
-            }
-          if (!e) {
-            for (int i = 1; i < nq; i++)
-              for (int j = i; j > 0 && (tq[j] < tq[j - 1] || (tq[j] == tq[j - 1] && Q[j] < Q[j - 1])); j--) {
-                int ti = Q[j]; Q[j] = Q[j - 1]; Q[j - 1] = ti;
-                float tf = tq[j]; tq[j] = tq[j - 1]; tq[j - 1] = tf;
-                tf = us[j]; us[j] = us[j - 1]; us[j - 1] = tf;
-                tf = uc[j]; uc[j] = uc[j - 1]; uc[j - 1] = tf;
+      int v = p < npair ? ws.pcnt[p] : 0;
+      int tot;
+      int ex = excl_scan<G>(g, v, &tot);
+      if (p < npair) ws.pofs[p] = ninc + ex;
+      ninc += tot;
+    }
+    if (ninc > MAXINC) status = LMM_NODE_QCAP;
+    g.sync();
+    if (status == 0) {
+      for (int q = lane; q < nc; q += G) {
+        uint32_t m = ws.vmask[q];
+        for (uint32_t ma = m; ma; ma &= ma - 1) {
+          int a = __ffs(ma) - 1;
+          for (uint32_t mb = ma & (ma - 1); mb; mb &= mb - 1) {
+            int b = __ffs(mb) - 1;
+            int pr = rank2(a, b, ns);
+            ws.inc[ws.pofs[pr] + atomicAdd(&ws.pfill[pr], 1)] = q;
+          }
+        }
+      }
+      // active pairs, lexicographic order
+      int nact = 0;
+      for (int base = 0; base < npair; base += G) {
+        int p = base + lane;
+        bool act = false;
+        if (p < npair) {
+          if (ws.pcnt[p] > 0) act = true;
+          else {
+            int a, b;
+            unrank2(p, ns, &a, &b);
+            uint32_t strut_bits = a == 0 ? (1u << b) : ((1u << a) | (1u << b));
+            act = (um & strut_bits) == 0;
+          }
+        }
+        unsigned am = g.ballot(act);
+        if (act) ws.plist[nact + __popc(am & ((1u << lane) - 1u))] = p;
+        nact += __popc(am);
+      }
+      g.sync();
+      for (int base = 0; base < nact; base += G) {
+        int k = base + lane;
+        int e = 0, cnt = 0, closed = 0;
+        int a = 0, b = 0;
+        f3 o = F3(0.f, 0.f, 0.f), av = o, bv = o;
+        int vsv[MAXQ], vev[MAXQ];
+        float t0v[MAXQ], dtv[MAXQ], tmv[MAXQ];
+        if (k < nact) {
+          const int p = ws.plist[k];
+          unrank2(p, ns, &a, &b);
+          uint32_t pm = (1u << a) | (1u << b);
+          const int nq = ws.pcnt[p];
+          bool conic_ok = true;
+          if (a == 0) nd.circle(b, &o, &av, &bv);
+          else conic_ok = nd.ellipse(a, b, &o, &av, &bv);
+          if (!conic_ok) {
+            if (nq > 0) e = LMM_NODE_CONIC;
+          } else if (nq > MAXQ) {
+            e = LMM_NODE_QCAP;
+          } else {
+            int Q[MAXQ];
+            float tq[MAXQ], us[MAXQ], uc[MAXQ];
+            for (int i = 0; i < nq; i++) {
+              int q = ws.inc[ws.pofs[p] + i];
+              float su, sc;
+              float t = conic_t(o, av, bv, nd.V(q), &su, &sc);
+              int j = i;   // insertion by (t, cluster index): order-independent
+              while (j > 0 && (t < tq[j - 1] || (t == tq[j - 1] && q < Q[j - 1]))) {
+                Q[j] = Q[j - 1]; tq[j] = tq[j - 1]; us[j] = us[j - 1]; uc[j] = uc[j - 1];
+                j--;
               }
+              Q[j] = q; tq[j] = t; us[j] = su; uc[j] = sc;
+            }
             int nint = nq == 0 ? 1 : nq;
             for (int i = 0; i < nint; i++) {
               float ms, mc, t0, dt;
@@ -436,31 +509,31 @@ __device__ void process_node(cg::thread_block_tile<G> &g, NodeWS<MAXS, MAXJ, MAX
             }
           }
         }
-      }
-      int tot, ctot;
-      int pos = na + excl_scan<G>(g, e ? 0 : cnt, &tot);
-      int spos = nv + excl_scan<G>(g, e ? 0 : closed, &ctot);
-      if (!e && cnt > 0 && pos + cnt > MAXA) e = LMM_NODE_ACAP;
-      if (!e && closed && spos >= MAXV) e = LMM_NODE_ACAP;
-      int fe = first_err<G>(g, e);
-      if (fe) { status = fe; break; }
-      for (int i = 0; i < cnt; i++) {
-        ArcRec &A = ws.arcs[pos + i];
-        int vs = vsv[i], ve = vev[i];
-        if (vs < 0) {
-          ws.vx[spos] = o.x + bv.x; ws.vy[spos] = o.y + bv.y; ws.vz[spos] = o.z + bv.z;
-          ws.vmask[spos] = (1u << a) | (1u << b);
-          vs = ve = spos;
+        int tot, ctot;
+        int pos = na + excl_scan<G>(g, e ? 0 : cnt, &tot);
+        int spos = nv + excl_scan<G>(g, e ? 0 : closed, &ctot);
+        if (!e && cnt > 0 && pos + cnt > MAXA) e = LMM_NODE_ACAP;
+        if (!e && closed && spos >= MAXV) e = LMM_NODE_ACAP;
+        int fe = first_err<G>(g, e);
+        if (fe) { status = fe; break; }
+        for (int i = 0; i < cnt; i++) {
+          ArcRec &A = ws.arcs[pos + i];
+          int vs = vsv[i], ve = vev[i];
+          if (vs < 0) {
+            ws.vx[spos] = o.x + bv.x; ws.vy[spos] = o.y + bv.y; ws.vz[spos] = o.z + bv.z;
+            ws.vmask[spos] = (1u << a) | (1u << b);
+            vs = ve = spos;
+          }
+          A.ids = (uint32_t)a | ((uint32_t)b << 8) | ((uint32_t)vs << 16) | ((uint32_t)ve << 24);
+          A.t0 = t0v[i]; A.dt = dtv[i];
+          ws.atmid[pos + i] = tmv[i];
+          A.ox = o.x; A.oy = o.y; A.oz = o.z;
+          A.ax = av.x; A.ay = av.y; A.az = av.z;
+          A.bx = bv.x; A.by = bv.y; A.bz = bv.z;
         }
-        A.ids = (uint32_t)a | ((uint32_t)b << 8) | ((uint32_t)vs << 16) | ((uint32_t)ve << 24);
-        A.t0 = t0v[i]; A.dt = dtv[i];
-        ws.atmid[pos + i] = tmv[i];
-        A.ox = o.x; A.oy = o.y; A.oz = o.z;
-        A.ax = av.x; A.ay = av.y; A.az = av.z;
-        A.bx = bv.x; A.by = bv.y; A.bz = bv.z;
+        na += tot;
+        nv += ctot;
       }
-      na += tot;
-      nv += ctot;
     }
   }
   g.sync();
@@ -522,52 +595,63 @@ __device__ void process_node(cg::thread_block_tile<G> &g, NodeWS<MAXS, MAXJ, MAX
 
   // ---- 5. arc loops per strut end (ordered by angle around the strut axis) -----------
   if (status == 0 && d > 0) {
+    // 5a: loop-entry data of every (arc, strut side), lanes over arcs
+    for (int i = lane; i < na; i += G) {
+      const ArcRec &A = ws.arcs[i];
+      const int lo = A.ids & 0xff, hi = (A.ids >> 8) & 0xff;
+      const int avs = (A.ids >> 16) & 0xff, ave = A.ids >> 24;
+      for (int x = 0; x < 2; x++) {
+        int k = x ? hi : lo;
+        if (k == 0) continue;
+        f3 as = nd.AS(k), e1 = nd.E1(k), e2 = nd.E2(k);
+        int fwd = f_dot(f_cross(F3(A.ax, A.ay, A.az), F3(A.bx, A.by, A.bz)), as) < 0.0f;
+        int vs = fwd ? avs : ave, ve = fwd ? ave : avs;
+        f3 Ps = nd.V(vs);
+        float ps = atan2p(f_dot(Ps, e2), f_dot(Ps, e1));
+        if (ps < 0.0f) ps += LMM_TWO_PI_F;
+        float dph;
+        if (vs == ve) dph = LMM_TWO_PI_F;
+        else {
+          f3 Pe = nd.V(ve);
+          float pe = atan2p(f_dot(Pe, e2), f_dot(Pe, e1));
+          if (pe < 0.0f) pe += LMM_TWO_PI_F;
+          dph = pe - ps;
+          if (dph <= 0.0f) dph += LMM_TWO_PI_F;
+        }
+        ws.eps[2 * i + x] = ps;
+        ws.edp[2 * i + x] = dph;
+        ws.efw[2 * i + x] = (uint8_t)fwd;
+      }
+    }
+    g.sync();
+    // 5b: per strut side: gather, order by (phi, arc index), check the chain
     for (int k0 = 0; k0 < d; k0 += G) {
       int k = k0 + lane + 1;
       int e = 0, cnt = 0;
-      int arcv[MAXLOOP], fwdv[MAXLOOP];
-      float psv[MAXLOOP], dpv[MAXLOOP];
+      int slot[MAXLOOP];
       if (k <= d) {
-        f3 as = nd.AS(k), e1 = nd.E1(k), e2 = nd.E2(k);
         for (int i = 0; i < na; i++) {
-          const ArcRec &A = ws.arcs[i];
-          int lo = A.ids & 0xff, hi = (A.ids >> 8) & 0xff;
+          uint32_t ids = ws.arcs[i].ids;
+          int lo = ids & 0xff, hi = (ids >> 8) & 0xff;
           if (lo != k && hi != k) continue;
           if (cnt >= MAXLOOP) { e = LMM_NODE_ACAP; break; }
-          int avs = (A.ids >> 16) & 0xff, ave = A.ids >> 24;
-          int fwd = f_dot(f_cross(F3(A.ax, A.ay, A.az), F3(A.bx, A.by, A.bz)), as) < 0.0f;
-          int vs = fwd ? avs : ave, ve = fwd ? ave : avs;
-          f3 Ps = nd.V(vs);
-          float ps = atan2p(f_dot(Ps, e2), f_dot(Ps, e1));
-          if (ps < 0.0f) ps += LMM_TWO_PI_F;
-          float dph;
-          if (vs == ve) dph = LMM_TWO_PI_F;
-          else {
-            f3 Pe = nd.V(ve);
-            float pe = atan2p(f_dot(Pe, e2), f_dot(Pe, e1));
-            if (pe < 0.0f) pe += LMM_TWO_PI_F;
-            dph = pe - ps;
-            if (dph <= 0.0f) dph += LMM_TWO_PI_F;
-          }
-          // insertion by (ps, arc index); arcs arrive in index order
-          int j = cnt;
-          while (j > 0 && ps < psv[j - 1]) {
-            arcv[j] = arcv[j - 1]; fwdv[j] = fwdv[j - 1]; psv[j] = psv[j - 1]; dpv[j] = dpv[j - 1];
-            j--;
-          }
-          arcv[j] = i; fwdv[j] = fwd; psv[j] = ps; dpv[j] = dph;
+          int sl = 2 * i + (hi == k ? 1 : 0);
+          float ps = ws.eps[sl];
+          int j = cnt;   // arcs arrive in index order: stable insertion by phi
+          while (j > 0 && ps < ws.eps[slot[j - 1]]) { slot[j] = slot[j - 1]; j--; }
+          slot[j] = sl;
           cnt++;
         }
         if (!e && cnt == 0) e = LMM_NODE_EMPTY;
         if (!e) {
           float sum = 0.0f;
           for (int i = 0; i < cnt; i++) {
-            const ArcRec &X = ws.arcs[arcv[i]];
-            const ArcRec &Y = ws.arcs[arcv[(i + 1) % cnt]];
-            int xe = fwdv[i] ? (X.ids >> 24) : ((X.ids >> 16) & 0xff);
-            int ys = fwdv[(i + 1) % cnt] ? ((Y.ids >> 16) & 0xff) : (Y.ids >> 24);
+            int sx = slot[i], sy = slot[(i + 1) % cnt];
+            const uint32_t X = ws.arcs[sx >> 1].ids, Y = ws.arcs[sy >> 1].ids;
+            int xe = ws.efw[sx] ? (X >> 24) : ((X >> 16) & 0xff);
+            int ys = ws.efw[sy] ? ((Y >> 16) & 0xff) : (Y >> 24);
             if (xe != ys) { e = LMM_NODE_CHAIN; break; }
-            sum += dpv[i];
+            sum += ws.edp[sx];
           }
           if (!e && fabsf(sum - LMM_TWO_PI_F) > 1e-3f) e = LMM_NODE_ANGLE;
         }
@@ -580,13 +664,13 @@ __device__ void process_node(cg::thread_block_tile<G> &g, NodeWS<MAXS, MAXJ, MAX
       if (k <= d) {
         ws.lfirst[k] = pos;
         ws.lcount[k] = cnt;
-        float ph = psv[0];
+        float ph = cnt ? ws.eps[slot[0]] : 0.0f;
         for (int i = 0; i < cnt; i++) {
-          if (i > 0) ph = ph + dpv[i - 1];
+          if (i > 0) ph = ph + ws.edp[slot[i - 1]];
           LoopRec &L = ws.le[pos + i];
-          L.arc_fwd = (uint32_t)arcv[i] | ((uint32_t)fwdv[i] << 16);
+          L.arc_fwd = (uint32_t)(slot[i] >> 1) | ((uint32_t)ws.efw[slot[i]] << 16);
           L.phs = ph;
-          L.dph = dpv[i];
+          L.dph = ws.edp[slot[i]];
           L.cum = 0;
         }
       }

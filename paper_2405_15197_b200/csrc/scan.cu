@@ -66,26 +66,46 @@ template <class T> __global__ void k_tile_scan(const T *in, int64_t n, const int
   }
 }
 
-template <class T> int scan_impl(lmm_ctx *c, const T *in, int64_t *out, int64_t n, int64_t *total_host) {
+// scratch for the tile sums of every recursion level, grown once (no per-call
+// allocation: stream-ordered allocation inside a timed step stalls the host)
+static size_t scan_scratch_elems(int64_t n) {
+  size_t tot = 0;
+  int64_t m = n;
+  while (true) {
+    int64_t nt = (m + 1 + SCAN_TILE - 1) / SCAN_TILE;
+    if (nt <= 1) break;
+    tot += 2 * (size_t)nt + 2;
+    m = nt;
+  }
+  return tot + 2;
+}
+
+template <class T> int scan_impl(lmm_ctx *c, const T *in, int64_t *out, int64_t n, int64_t *scratch) {
   // out has n+1 entries; out[n] = total
   int64_t ntile = (n + 1 + SCAN_TILE - 1) / SCAN_TILE;
   if (ntile <= 1) {
     (c->n_launch++), k_tile_scan<T><<<1, SCAN_T, 0, c->stream>>>(in, n, nullptr, out);
   } else {
-    int64_t *sums = nullptr, *soff = nullptr;
-    CUDA_TRY(cudaMallocAsync((void **)&sums, sizeof(int64_t) * (2 * ntile + 2), c->stream));
-    soff = sums + ntile + 1;
+    int64_t *sums = scratch, *soff = scratch + ntile + 1;
     (c->n_launch++), k_tile_sums<T><<<(unsigned)ntile, SCAN_T, 0, c->stream>>>(in, n, sums);
     CUDA_TRY(cudaGetLastError());
-    int rc = scan_impl<int64_t>(c, sums, soff, ntile, nullptr);
+    int rc = scan_impl<int64_t>(c, sums, soff, ntile, scratch + 2 * ntile + 2);
     if (rc) return rc;
     (c->n_launch++), k_tile_scan<T><<<(unsigned)ntile, SCAN_T, 0, c->stream>>>(in, n, soff, out);
-    CUDA_TRY(cudaFreeAsync(sums, c->stream));
   }
   CUDA_TRY(cudaGetLastError());
+  return LMM_OK;
+}
+
+template <class T> int scan_top(lmm_ctx *c, const T *in, int64_t *out, int64_t n, int64_t *total_host) {
+  int rc;
+  if ((rc = dev_alloc(c->scan_tmp, sizeof(int64_t) * scan_scratch_elems(n)))) return rc;
+  if (!c->pinned_scalar) CUDA_TRY(cudaMallocHost((void **)&c->pinned_scalar, 64));
+  if ((rc = scan_impl<T>(c, in, out, n, (int64_t *)c->scan_tmp.p))) return rc;
   if (total_host) {
-    CUDA_TRY(cudaMemcpyAsync(total_host, out + n, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaMemcpyAsync(c->pinned_scalar, out + n, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
+    *total_host = c->pinned_scalar[0];
   }
   return LMM_OK;
 }
@@ -94,10 +114,10 @@ template <class T> int scan_impl(lmm_ctx *c, const T *in, int64_t *out, int64_t 
 
 int scan_exclusive_i64(lmm_ctx *c, const int64_t *in, int64_t *out, int64_t n, int64_t *total_host) {
   KTimer t(c, LMM_K_SCAN);
-  return scan_impl<int64_t>(c, in, out, n, total_host);
+  return scan_top<int64_t>(c, in, out, n, total_host);
 }
 
 int scan_exclusive_i32_to_i64(lmm_ctx *c, const int *in, int64_t *out, int64_t n, int64_t *total_host) {
   KTimer t(c, LMM_K_SCAN);
-  return scan_impl<int>(c, in, out, n, total_host);
+  return scan_top<int>(c, in, out, n, total_host);
 }

@@ -117,9 +117,10 @@ def decode_node(bufs: dict, n: int) -> dict:
         v_mask=v[:, 3].copy().view(np.uint32), v_pos32=v[:, :3].copy(),
         a_int=a_int, a_f32=a[:, 1:12].copy().view(np.float32),
         loop_off=loop_off,
-        l_int=np.stack([le[:, 0] & 0xFFFF, le[:, 0] >> 16], 1).astype(np.int32),
+        l_int=np.stack([le[:, 0] & 0xFFFF, (le[:, 0] >> 16) & 1], 1).astype(np.int32),
+        l_N=(le[:, 0] >> 17).astype(np.int32),
         l_f32=le[:, 1:3].copy().view(np.float32),
         l_cum=le[:, 3].astype(np.int32),
         hole_off=hole_off,
-        h_int=np.stack([he[:, 0] & 0xFFFF, he[:, 0] >> 16], 1).astype(np.int32),
+        h_int=np.stack([he[:, 0] & 0xFFFF, (he[:, 0] >> 16) & 1], 1).astype(np.int32),
     )
