@@ -319,9 +319,10 @@ static int junction32(const side32 *S, float R, int a, int b, int c, f3 *y, floa
   float nn1 = f_dot(n1, n1), nn2 = f_dot(n2, n2);
   if (!(mm > (1e-8f * nn1) * nn2)) return 0;
   f3 c1 = f_cross(n2, m), c2 = f_cross(m, n1);
-  f3 y0 = F3((q1 * c1.x + q2 * c2.x) / mm, (q1 * c1.y + q2 * c2.y) / mm, (q1 * c1.z + q2 * c2.z) / mm);
-  float ml = sqrtf(mm);
-  f3 mh = f_div(m, ml);
+  float imm = 1.0f / mm;
+  f3 y0 = F3((q1 * c1.x + q2 * c2.x) * imm, (q1 * c1.y + q2 * c2.y) * imm, (q1 * c1.z + q2 * c2.z) * imm);
+  float iml = 1.0f / sqrtf(mm);
+  f3 mh = f_scl(m, iml);
   float tau0 = f_dot(Wa, y0) - Ea;
   float tau1 = f_dot(Wa, mh);
   float A = 1.0f - tau1 * tau1;
@@ -331,7 +332,8 @@ static int junction32(const side32 *S, float R, int a, int b, int c, f3 *y, floa
   float disc = Bp * Bp - A * C;
   if (disc < 0.0f) return 0;
   float sq = sqrtf(disc);
-  float lam[2] = {(-Bp - sq) / A, (-Bp + sq) / A};
+  float iA = 1.0f / A;
+  float lam[2] = {(-Bp - sq) * iA, (-Bp + sq) * iA};
   for (int r = 0; r < 2; r++) {
     y[r] = f_add(y0, f_scl(mh, lam[r]));
     tau[r] = tau0 + lam[r] * tau1;
@@ -370,9 +372,9 @@ static void junction64(const side64 *S, double R, int a, int b, int c, int root,
 static int ellipse32(const side32 *S, float R, int a, int b, f3 *o, f3 *av, f3 *bv) {
   const side32 *A = &S[a];
   f3 N = f_sub(A->w, S[b].w);
-  float nl = sqrtf(f_dot(N, N));
-  f3 n = f_div(N, nl);
-  float pc = (A->e - S[b].e) / nl;
+  float inl = 1.0f / sqrtf(f_dot(N, N));
+  f3 n = f_scl(N, inl);
+  float pc = (A->e - S[b].e) * inl;
   f3 p = f_scl(n, pc);
   float s = A->s, c = A->c;
   if (!(fabsf(f_dot(n, A->u)) > fabsf(s) + 1e-3f)) return 0;
@@ -380,7 +382,7 @@ static int ellipse32(const side32 *S, float R, int a, int b, f3 *o, f3 *av, f3 *
   f3 dp = f_cross(d, n);
   float dpl2 = f_dot(dp, dp);
   f3 r_;
-  if (dpl2 > 1e-12f) { dp = f_div(dp, sqrtf(dpl2)); r_ = f_cross(dp, d); }
+  if (dpl2 > 1e-12f) { dp = f_scl(dp, 1.0f / sqrtf(dpl2)); r_ = f_cross(dp, d); }
   else r_ = A->e1;
   f3 g1 = F3(c * d.x - s * r_.x, c * d.y - s * r_.y, c * d.z - s * r_.z);
   f3 g2 = F3(c * d.x + s * r_.x, c * d.y + s * r_.y, c * d.z + s * r_.z);
@@ -414,7 +416,7 @@ static void ellipse64(const side64 *S, const side32 *S32, double R, int a, int b
   /* degenerate-branch choice follows the binary32 decision */
   f3 d32 = F3(-S32[a].u.x, -S32[a].u.y, -S32[a].u.z);
   f3 N32 = f_sub(S32[a].w, S32[b].w);
-  f3 n32 = f_div(N32, sqrtf(f_dot(N32, N32)));
+  f3 n32 = f_scl(N32, 1.0f / sqrtf(f_dot(N32, N32)));
   f3 dp32 = f_cross(d32, n32);
   if (f_dot(dp32, dp32) > 1e-12f) { dp = d_div(dp, sqrt(dpl2)); r_ = d_cross(dp, d); }
   else r_ = A->e1;
@@ -452,8 +454,8 @@ static float conic_t32(f3 o, f3 av, f3 bv, f3 P, float *us, float *uc) {
   f3 Q = f_sub(P, o);
   float st = f_dot(Q, av) / f_dot(av, av);
   float ct = f_dot(Q, bv) / f_dot(bv, bv);
-  float l = sqrtf(st * st + ct * ct);
-  *us = st / l; *uc = ct / l;
+  float il = 1.0f / sqrtf(st * st + ct * ct);
+  *us = st * il; *uc = ct * il;
   return orc_atan2p(st, ct);
 }
 static double conic_t64(d3 o, d3 av, d3 bv, d3 P) {
@@ -536,24 +538,38 @@ static int node_metamesh(orc_lat *L, int64_t n) {
         }
       }
 
-  /* 2. leader clustering (coincident junctions = one vertex of higher valence) */
+  /* 2. clustering: connected components of the graph "junctions within delta_c (max-norm)";
+   *    a component is one vertex (of higher valence when several junctions coincide),
+   *    positioned at and ordered by its lowest-index junction. */
   vert_t *V = (vert_t *)calloc(ORC_MAXC + ORC_MAXA, sizeof(vert_t));
+  int *lab = (int *)malloc(sizeof(int) * (size_t)(nj + 1));
+  for (int j = 0; j < nj; j++) lab[j] = j;
+  for (int changed = 1; changed;) {
+    changed = 0;
+    for (int j = 0; j < nj; j++)
+      for (int k = 0; k < nj; k++)
+        if (lab[k] < lab[j] && fabsf(J[j].y.x - J[k].y.x) <= dc && fabsf(J[j].y.y - J[k].y.y) <= dc &&
+            fabsf(J[j].y.z - J[k].y.z) <= dc) { lab[j] = lab[k]; changed = 1; }
+  }
   int nc = 0;
+  int *cid = (int *)malloc(sizeof(int) * (size_t)(nj + 1));
+  for (int j = 0; j < nj; j++) {
+    if (lab[j] == j) {
+      if (nc >= ORC_MAXC) { free(J); free(V); free(lab); free(cid); M->status = ORC_E_CCAP; return M->status; }
+      cid[j] = nc;
+      V[nc].kind = 0; V[nc].ja = J[j].a; V[nc].jb = J[j].b; V[nc].jc = J[j].c; V[nc].jr = J[j].r;
+      V[nc].y = J[j].y; V[nc].mask = 0; V[nc].seam_arc = -1;
+      nc++;
+    }
+  }
   for (int j = 0; j < nj; j++) {
     uint32_t bits = (1u << J[j].a) | (1u << J[j].b) | (1u << J[j].c);
     /* a strut junction at tangent length ~0 lies on the nodal sphere: it ties with side 0 */
     if (fabsf(J[j].tau) <= delta) bits |= 1u;
-    int q;
-    for (q = 0; q < nc; q++)
-      if (fabsf(J[j].y.x - V[q].y.x) <= dc && fabsf(J[j].y.y - V[q].y.y) <= dc && fabsf(J[j].y.z - V[q].y.z) <= dc) break;
-    if (q == nc) {
-      if (nc >= ORC_MAXC) { free(J); free(V); M->status = ORC_E_CCAP; return M->status; }
-      V[q].kind = 0; V[q].ja = J[j].a; V[q].jb = J[j].b; V[q].jc = J[j].c; V[q].jr = J[j].r;
-      V[q].y = J[j].y; V[q].mask = 0; V[q].seam_arc = -1;
-      nc++;
-    }
-    V[q].mask |= bits;
+    V[cid[lab[j]]].mask |= bits;
   }
+  free(lab);
+  free(cid);
   free(J);
   int nv = nc;
 

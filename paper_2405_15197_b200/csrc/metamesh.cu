@@ -18,6 +18,13 @@
 
 namespace cg = cooperative_groups;
 
+#ifdef LMM_PHASE_TIMING
+__device__ unsigned long long g_phase_cycles[8];
+extern "C" LMM_API int lmm_debug_phase_cycles(unsigned long long *out) {
+  return cudaMemcpyFromSymbol(out, g_phase_cycles, sizeof(g_phase_cycles)) == cudaSuccess ? 0 : 2;
+}
+#endif
+
 namespace {
 
 struct MMParams {
@@ -48,6 +55,7 @@ struct alignas(16) NodeWS {
   // junctions
   float jx[MAXJ], jy[MAXJ], jz[MAXJ];
   uint32_t jabc[MAXJ];
+  int jlab[MAXJ], jcid[MAXJ];
   // vertices: clusters then seams
   float vx[MAXV], vy[MAXV], vz[MAXV];
   uint32_t vmask[MAXV];
@@ -91,9 +99,10 @@ template <class WS> struct Node {
     float nn1 = f_dot(n1, n1), nn2 = f_dot(n2, n2);
     if (!(mm > (1e-8f * nn1) * nn2)) return false;
     f3 c1 = f_cross(n2, m), c2 = f_cross(m, n1);
-    f3 y0 = F3((q1 * c1.x + q2 * c2.x) / mm, (q1 * c1.y + q2 * c2.y) / mm, (q1 * c1.z + q2 * c2.z) / mm);
-    float ml = sqrtf(mm);
-    f3 mh = f_div(m, ml);
+    float imm = 1.0f / mm;
+    f3 y0 = F3((q1 * c1.x + q2 * c2.x) * imm, (q1 * c1.y + q2 * c2.y) * imm, (q1 * c1.z + q2 * c2.z) * imm);
+    float iml = 1.0f / sqrtf(mm);
+    f3 mh = f_scl(m, iml);
     float tau0 = f_dot(Wa, y0) - Ea;
     float tau1 = f_dot(Wa, mh);
     float A = 1.0f - tau1 * tau1;
@@ -103,7 +112,8 @@ template <class WS> struct Node {
     float disc = Bp * Bp - A * C;
     if (disc < 0.0f) return false;
     float sq = sqrtf(disc);
-    float l0 = (-Bp - sq) / A, l1 = (-Bp + sq) / A;
+    float iA = 1.0f / A;
+    float l0 = (-Bp - sq) * iA, l1 = (-Bp + sq) * iA;
     y[0] = f_add(y0, f_scl(mh, l0));
     tau[0] = tau0 + l0 * tau1;
     y[1] = f_add(y0, f_scl(mh, l1));
@@ -111,21 +121,20 @@ template <class WS> struct Node {
     return true;
   }
 
+  // branch-free over the sides (same boolean as the early-exit form)
   __device__ bool valid_strut_pt(uint32_t excl, f3 y, float tau, float delta) const {
-    if (tau < -delta) return false;
+    bool ok = !(tau < -delta);
     for (int m = 1; m <= d; m++) {
-      if (excl & (1u << m)) continue;
-      if (h(m, y) - tau > delta) return false;
+      bool viol = h(m, y) - tau > delta;
+      ok = ok && (((excl >> m) & 1u) || !viol);
     }
-    return true;
+    return ok;
   }
   // sphere junction: tolerant (no other strut above the sphere by more than delta)
   __device__ bool valid_sphere_junction(uint32_t excl, f3 y, float delta) const {
-    for (int m = 1; m <= d; m++) {
-      if (excl & (1u << m)) continue;
-      if (h(m, y) > delta) return false;
-    }
-    return true;
+    bool ok = true;
+    for (int m = 1; m <= d; m++) ok = ok && (((excl >> m) & 1u) || !(h(m, y) > delta));
+    return ok;
   }
   // end-circle (cap) point: strictly exposed
   __device__ bool valid_sphere_pt(uint32_t excl, f3 y, float delta) const {
@@ -139,9 +148,9 @@ template <class WS> struct Node {
   // PAPER.md Eq. 7: strut a's ellipse in the auxiliary plane P_{a,b}
   __device__ bool ellipse(int a, int b, f3 *o, f3 *av, f3 *bv) const {
     f3 N = f_sub(W(a), W(b));
-    float nl = sqrtf(f_dot(N, N));
-    f3 n = f_div(N, nl);
-    float pc = (w.e[a] - w.e[b]) / nl;
+    float inl = 1.0f / sqrtf(f_dot(N, N));
+    f3 n = f_scl(N, inl);
+    float pc = (w.e[a] - w.e[b]) * inl;
     f3 p = f_scl(n, pc);
     float s = w.s[a], c = w.c[a];
     f3 u = U(a);
@@ -150,7 +159,7 @@ template <class WS> struct Node {
     f3 dp = f_cross(dd, n);
     float dpl2 = f_dot(dp, dp);
     f3 r_;
-    if (dpl2 > 1e-12f) { dp = f_div(dp, sqrtf(dpl2)); r_ = f_cross(dp, dd); }
+    if (dpl2 > 1e-12f) { dp = f_scl(dp, 1.0f / sqrtf(dpl2)); r_ = f_cross(dp, dd); }
     else r_ = E1(a);
     f3 g1 = F3(c * dd.x - s * r_.x, c * dd.y - s * r_.y, c * dd.z - s * r_.z);
     f3 g2 = F3(c * dd.x + s * r_.x, c * dd.y + s * r_.y, c * dd.z + s * r_.z);
@@ -183,9 +192,9 @@ __device__ __forceinline__ float conic_t(f3 o, f3 av, f3 bv, f3 P, float *us, fl
   f3 Q = f_sub(P, o);
   float st = f_dot(Q, av) / f_dot(av, av);
   float ct = f_dot(Q, bv) / f_dot(bv, bv);
-  float l = sqrtf(st * st + ct * ct);
-  *us = st / l;
-  *uc = ct / l;
+  float il = 1.0f / sqrtf(st * st + ct * ct);
+  *us = st * il;
+  *uc = ct * il;
   return atan2p(st, ct);
 }
 
@@ -258,6 +267,17 @@ __device__ void process_node(cg::thread_block_tile<G> &g, NodeWS<MAXS, MAXJ, MAX
   const float delta = LMM_TOL_REL * R, dc = LMM_CTOL_REL * R;
   int status = 0;
 
+#ifdef LMM_PHASE_TIMING
+  long long ph_t = clock64();
+#define PHASE_MARK(k)                                                    \
+  do {                                                                   \
+    long long ph_n = clock64();                                          \
+    if (lane == 0) atomicAdd(&g_phase_cycles[(k) - 1], (unsigned long long)(ph_n - ph_t)); \
+    ph_t = ph_n;                                                         \
+  } while (0)
+#else
+#define PHASE_MARK(k) do { } while (0)
+#endif
   // ---- 1. sides -------------------------------------------------------------------
   if (lane == 0) {
     ws.wx[0] = ws.wy[0] = ws.wz[0] = ws.e[0] = 0.0f;
@@ -307,6 +327,7 @@ __device__ void process_node(cg::thread_block_tile<G> &g, NodeWS<MAXS, MAXJ, MAX
   int nj = 0, nc = 0, nv = 0, na = 0, nle = 0, nh = 0, nhe = 0;
   const int ns = d + 1;
 
+  PHASE_MARK(1);
   // ---- 2. triple junctions, lexicographic (a<b<c), root-minor ---------------------
   if (status == 0 && d > 0) {
     const int ntri = ns * (ns - 1) * (ns - 2) / 6;
@@ -355,34 +376,53 @@ __device__ void process_node(cg::thread_block_tile<G> &g, NodeWS<MAXS, MAXJ, MAX
   }
   g.sync();
 
-  // ---- 3. leader clustering of coincident junctions --------------------------------
-  if (status == 0) {
-    for (int j = 0; j < nj; j++) {
-      float yx = ws.jx[j], yy = ws.jy[j], yz = ws.jz[j];
-      uint32_t code = ws.jabc[j];
-      uint32_t bits = (1u << (code & 0xff)) | (1u << ((code >> 8) & 0xff)) | (1u << ((code >> 16) & 0xff));
-      if (code & (1u << 25)) bits |= 1u;   // strut junction at tangent length ~0: on the sphere
-      int found = -1;
-      for (int q0 = 0; q0 < nc && found < 0; q0 += G) {
-        int q = q0 + lane;
-        bool mt = q < nc && fabsf(yx - ws.vx[q]) <= dc && fabsf(yy - ws.vy[q]) <= dc && fabsf(yz - ws.vz[q]) <= dc;
-        unsigned m = g.ballot(mt);
-        if (m) found = q0 + __ffs(m) - 1;
-      }
-      if (found < 0) {
-        if (nc >= MAXV) { status = LMM_NODE_CCAP; break; }
-        found = nc;
-        if (lane == 0) { ws.vx[found] = yx; ws.vy[found] = yy; ws.vz[found] = yz; ws.vmask[found] = 0u; }
-        nc++;
+  PHASE_MARK(2);
+  // ---- 3. clustering: connected components of "junctions within delta_c" -----------
+  // (label propagation to the lowest junction index; a component is one vertex)
+  if (status == 0 && nj > 0) {
+    for (int j = lane; j < nj; j += G) ws.jlab[j] = j;
+    g.sync();
+    for (;;) {
+      bool changed = false;
+      for (int j = lane; j < nj; j += G) {
+        float yx = ws.jx[j], yy = ws.jy[j], yz = ws.jz[j];
+        int lj = ws.jlab[j];
+        for (int k = 0; k < nj; k++) {
+          int lk = ws.jlab[k];
+          if (lk < lj && fabsf(yx - ws.jx[k]) <= dc && fabsf(yy - ws.jy[k]) <= dc && fabsf(yz - ws.jz[k]) <= dc) lj = lk;
+        }
+        if (lj != ws.jlab[j]) { ws.jlab[j] = lj; changed = true; }
       }
       g.sync();
-      if (lane == 0) ws.vmask[found] |= bits;
-      g.sync();
+      if (!g.any(changed)) break;
+    }
+    // component roots in index order -> vertex ids
+    for (int base = 0; base < nj; base += G) {
+      int j = base + lane;
+      bool root = j < nj && ws.jlab[j] == j;
+      unsigned rm = g.ballot(root);
+      int id = nc + __popc(rm & ((1u << lane) - 1u));
+      if (root && id < MAXV) {
+        ws.jcid[j] = id;
+        ws.vx[id] = ws.jx[j]; ws.vy[id] = ws.jy[j]; ws.vz[id] = ws.jz[j]; ws.vmask[id] = 0u;
+      }
+      nc += __popc(rm);
+    }
+    if (nc > MAXV) status = LMM_NODE_CCAP;
+    g.sync();
+    if (status == 0) {
+      for (int j = lane; j < nj; j += G) {
+        uint32_t code = ws.jabc[j];
+        uint32_t bits = (1u << (code & 0xff)) | (1u << ((code >> 8) & 0xff)) | (1u << ((code >> 16) & 0xff));
+        if (code & (1u << 25)) bits |= 1u;   // strut junction at tangent length ~0: on the sphere
+        atomicOr(&ws.vmask[ws.jcid[ws.jlab[j]]], bits);
+      }
     }
   }
   nv = nc;
   g.sync();
 
+  PHASE_MARK(3);
   // ---- 4. arcs: conics walked through their vertices, incidence-driven --------------
   // Clusters enumerate the side pairs of their tie sets (counting sort by pair), the
   // pairs with vertices -- plus pairs of sides that appear in no vertex (only these can
@@ -538,6 +578,7 @@ __device__ void process_node(cg::thread_block_tile<G> &g, NodeWS<MAXS, MAXJ, MAX
   }
   g.sync();
 
+  PHASE_MARK(4);
   // ambiguous strut-strut arcs running under a strictly exposed hole lune are dropped
   // (R10): midpoint tangent length < delta and both end circles join its ends
   if (status == 0 && na > 0) {
@@ -593,6 +634,7 @@ __device__ void process_node(cg::thread_block_tile<G> &g, NodeWS<MAXS, MAXJ, MAX
     if (g.any(e != 0)) status = LMM_NODE_UNREF;
   }
 
+  PHASE_MARK(5);
   // ---- 5. arc loops per strut end (ordered by angle around the strut axis) -----------
   if (status == 0 && d > 0) {
     // 5a: loop-entry data of every (arc, strut side), lanes over arcs
@@ -679,6 +721,7 @@ __device__ void process_node(cg::thread_block_tile<G> &g, NodeWS<MAXS, MAXJ, MAX
   }
   g.sync();
 
+  PHASE_MARK(6);
   // ---- 6. hole contours: cap arcs chained around the exposed sphere (lane 0) --------
   if (status == 0 && d > 0) {
     int st = 0;
@@ -723,6 +766,7 @@ __device__ void process_node(cg::thread_block_tile<G> &g, NodeWS<MAXS, MAXJ, MAX
   }
   g.sync();
 
+  PHASE_MARK(7);
   // ---- 7. write the node's slabs ----------------------------------------------------
   if (status == 0 && (nv > slab_cap(d, SLAB_V_K, SLAB_V_K0) || na > slab_cap(d, SLAB_A_K, SLAB_A_K0) ||
                       nle > slab_cap(d, SLAB_L_K, SLAB_L_K0) || nh > slab_cap(d, SLAB_H_K, SLAB_H_K0) ||
@@ -747,6 +791,7 @@ __device__ void process_node(cg::thread_block_tile<G> &g, NodeWS<MAXS, MAXJ, MAX
     P.loop_hdr[off + k] = status == 0 ? make_int2(ws.lfirst[k + 1], ws.lcount[k + 1]) : make_int2(0, 0);
   for (int h = lane; h < nh; h += G) P.hole_hdr[hb + h] = make_int2(ws.hoff[h], ws.hoff[h + 1] - ws.hoff[h]);
   for (int q = lane; q < nhe; q += G) { HoleEnt he; he.arc_fwd = ws.he[q]; he.cum = 0; P.hole_ent[heb + q] = he; }
+  PHASE_MARK(8);
   g.sync();
 }
 

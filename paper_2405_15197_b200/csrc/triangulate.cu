@@ -23,9 +23,7 @@ namespace {
 
 constexpr int TPC = 1024;       // triangles per emit chunk (51 200 B of records)
 constexpr int EMIT_T = 256;     // threads per emit CTA
-constexpr int EMIT_R = TPC / EMIT_T;
 constexpr int REC = 50;
-constexpr int MAXSB = 64;       // band offsets cached per chunk
 
 struct TriParams {
   const float4 *node;
@@ -244,8 +242,10 @@ __global__ void k_hole_count(TriParams P) {
     }
     // Eq. 13 fan centre: barycentre of the contour vertices, direction regularised by
     // the contour's outward (Newell) normal (reading R7)
+    // sums taken relative to the first contour point p0 (the Newell sum is translation
+    // invariant for a closed contour; this keeps small holes well conditioned in binary32)
     float bx = 0.f, by = 0.f, bz = 0.f, nx = 0.f, ny = 0.f, nz = 0.f;
-    f3 first = F3(0.f, 0.f, 0.f), prev = first;
+    f3 p0 = F3(0.f, 0.f, 0.f), prev = p0;
     bool have = false;
     for (int i = 0; i < H.y; i++) {
       uint32_t af = he[H.x + i].arc_fwd;
@@ -254,21 +254,17 @@ __global__ void k_hole_count(TriParams P) {
       int N = le_N(af);
       for (int j = 0; j < N; j++) {
         f3 p = arc_point(A, vs, N, fwd ? j : N - j);
-        bx += p.x; by += p.y; bz += p.z;
-        if (have) {
-          f3 cr = f_cross(prev, p);
-          nx += cr.x; ny += cr.y; nz += cr.z;
-        } else { first = p; have = true; }
-        prev = p;
+        if (!have) { p0 = p; have = true; prev = F3(0.f, 0.f, 0.f); continue; }
+        f3 q = f_sub(p, p0);
+        bx += q.x; by += q.y; bz += q.z;
+        f3 cr = f_cross(prev, q);
+        nx += cr.x; ny += cr.y; nz += cr.z;
+        prev = q;
       }
-    }
-    {
-      f3 cr = f_cross(prev, first);
-      nx += cr.x; ny += cr.y; nz += cr.z;
     }
     float inv = 1.0f / (float)M;
     float nl = rsqrtf(nx * nx + ny * ny + nz * nz);
-    float dx = bx * inv + R * nx * nl, dy = by * inv + R * ny * nl, dz = bz * inv + R * nz * nl;
+    float dx = (p0.x + bx * inv) + R * nx * nl, dy = (p0.y + by * inv) + R * ny * nl, dz = (p0.z + bz * inv) + R * nz * nl;
     float dl = R * rsqrtf(dx * dx + dy * dy + dz * dz);
     P.hole_M[g] = M;
     P.hole_bp[g] = make_float4(dx * dl, dy * dl, dz * dl, 0.0f);
@@ -316,28 +312,58 @@ __device__ __forceinline__ void put_rec(unsigned char *dst, f3 a, f3 b, f3 c) {
   }
 }
 
-// point cursor over a ring (node-local arcs -> absolute positions)
-struct PtCursor {
-  const LoopRec *le;
+// Warp-per-band emission.  Warps grid-stride over the strut bands (then the hole fans)
+// that intersect [first, first+count).  Per band the warp caches both rings' loop
+// entries and arc records in shared memory and walks the band in windows of WIN merge
+// steps: the ring points a window touches are computed once, in parallel, into shared
+// memory.  Triangles then go in groups of 64 whose output offset is 16-byte aligned:
+// lane l assembles records 2l and 2l+1 (100 bytes = 25 aligned words), its ring positions
+// following from ballot prefix-popcounts of the merge bits; the group leaves the per-warp
+// staging buffer as 16-byte vector stores.  The <= 7 triangles before a band's first
+// aligned position go straight to global memory.  No block-level barriers.
+constexpr int EW = EMIT_T / 32;   // warps per CTA
+constexpr int WIN = 128;          // merge steps per window
+constexpr int GRP = 64;           // triangles per aligned group (3200 B)
+constexpr int MAXRE = 32;         // ring entries per ring (>= MAXLOOP of the meta-mesh)
+constexpr int MAXRA = 16;         // arc records cached per ring
+
+struct __align__(16) WarpRing {
+  ArcRec arc[2][MAXRA];
+  int cum[2][MAXRE];
+  int nf[2][MAXRE];     // N | fwd << 16
+  int ax[2][MAXRE];     // arc index in the node's arc slab
+  float px[2][WIN + 2], py[2][WIN + 2], pz[2][WIN + 2];
+  uint4 stage[GRP * REC / 16];
+};
+
+struct RingRef {
   const ArcRec *arcs;
   const float4 *vs;
-  int cnt, e, cum, N, fwd;
-  ArcRec A;
   float ox, oy, oz;
-  __device__ void load(int ee) {
-    e = ee;
-    LoopRec L = le[e];
-    cum = L.cum; N = le_N(L.arc_fwd); fwd = le_fwd(L.arc_fwd);
-    A = load_arc(arcs + le_arc(L.arc_fwd));
-  }
-  __device__ f3 point(int idx) {
-    if (idx < cum) load(0);
-    while (idx >= cum + N && e + 1 < cnt) load(e + 1);
-    int j = idx - cum;
-    f3 p = arc_point(A, vs, N, fwd ? j : N - j);
-    return F3(ox + p.x, oy + p.y, oz + p.z);
-  }
+  int cnt;
 };
+
+__device__ __forceinline__ ArcRec lds_arc(const ArcRec *p) {
+  const float4 *q = reinterpret_cast<const float4 *>(p);
+  float4 x = q[0], y = q[1], z = q[2];
+  ArcRec a;
+  a.ids = __float_as_uint(x.x); a.t0 = x.y; a.dt = x.z; a.ox = x.w;
+  a.oy = y.x; a.oz = y.y; a.ax = y.z; a.ay = y.w;
+  a.az = z.x; a.bx = z.y; a.by = z.z; a.bz = z.w;
+  return a;
+}
+
+__device__ __forceinline__ f3 ring_point(const WarpRing &w, int r, const RingRef &R, int idx) {
+  int e = 0;
+#pragma unroll 4
+  for (int k = 1; k < R.cnt; k++) e += (w.cum[r][k] <= idx) ? 1 : 0;
+  int nf = w.nf[r][e];
+  int N = nf & 0xffff, fwd = nf >> 16;
+  int j = idx - w.cum[r][e];
+  const ArcRec A = e < MAXRA ? lds_arc(&w.arc[r][e]) : load_arc(R.arcs + w.ax[r][e]);
+  f3 p = arc_point(A, R.vs, N, fwd ? j : N - j);
+  return F3(R.ox + p.x, R.oy + p.y, R.oz + p.z);
+}
 
 // A-advances of band [base, ...) before triangle t
 __device__ __forceinline__ int merge_rank(const TriParams &P, int64_t base, int64_t t) {
@@ -352,75 +378,207 @@ __device__ __forceinline__ int merge_rank(const TriParams &P, int64_t base, int6
   return __ldg(&P.macc[w]) + __popc(below);
 }
 
-__device__ void emit_band_run(const TriParams &P, int64_t s, int64_t t, int64_t t1, unsigned char *stage, int64_t sbase) {
-  const int2 e = P.ends[s];
-  const int2 ce = P.strut_csr[s];
+__device__ __forceinline__ void tri_words(f3 a, f3 b, f3 c, uint32_t *f) {
+  f3 u = f_sub(b, a), v = f_sub(c, a);
+  float nx = u.y * v.z - u.z * v.y, ny = u.z * v.x - u.x * v.z, nz = u.x * v.y - u.y * v.x;
+  float l2 = nx * nx + ny * ny + nz * nz;
+  float il = l2 > 0.0f ? rsqrtf(l2) : 0.0f;
+  f[0] = __float_as_uint(nx * il); f[1] = __float_as_uint(ny * il); f[2] = __float_as_uint(nz * il);
+  f[3] = __float_as_uint(a.x); f[4] = __float_as_uint(a.y); f[5] = __float_as_uint(a.z);
+  f[6] = __float_as_uint(b.x); f[7] = __float_as_uint(b.y); f[8] = __float_as_uint(b.z);
+  f[9] = __float_as_uint(c.x); f[10] = __float_as_uint(c.y); f[11] = __float_as_uint(c.z);
+}
+
+// two consecutive 50-byte records as 25 aligned words
+__device__ __forceinline__ void put_pair(uint32_t *d, const uint32_t *f, const uint32_t *g) {
+#pragma unroll
+  for (int i = 0; i < 12; i++) d[i] = f[i];
+  d[12] = g[0] << 16;   // attribute 0 | low half of g0
+#pragma unroll
+  for (int i = 0; i < 11; i++) d[13 + i] = __funnelshift_r(g[i], g[i + 1], 16);
+  d[24] = g[11] >> 16;   // high half of g11 | attribute 0
+}
+
+// one record through 2-byte stores (unaligned head triangles)
+__device__ __forceinline__ void put_rec16(unsigned char *dst, const uint32_t *f) {
+  uint16_t *d = reinterpret_cast<uint16_t *>(dst);
+#pragma unroll
+  for (int i = 0; i < 12; i++) { d[2 * i] = (uint16_t)(f[i] & 0xffffu); d[2 * i + 1] = (uint16_t)(f[i] >> 16); }
+  d[24] = 0;
+}
+
+// staged group [0, bytes) -> global dst (16-byte aligned): vectors then 2-byte tail
+__device__ __forceinline__ void flush_group(WarpRing &w, int bytes, unsigned char *dst, int lane) {
+  __syncwarp();
+  const int nv = bytes >> 4;
+  uint4 *d = reinterpret_cast<uint4 *>(dst);
+  for (int k = lane; k < nv; k += 32) d[k] = w.stage[k];
+  const int tb = bytes - (nv << 4);
+  if (lane < (tb >> 1)) {
+    const uint16_t *s16 = reinterpret_cast<const uint16_t *>(w.stage + nv);
+    reinterpret_cast<uint16_t *>(dst + (nv << 4))[lane] = s16[lane];
+  }
+  __syncwarp();
+}
+
+__device__ __forceinline__ void load_ring(WarpRing &w, int r, const LoopRec *le, int cnt, const ArcRec *arcs, int lane) {
+  if (lane < cnt) {
+    LoopRec L = le[lane];
+    w.cum[r][lane] = L.cum;
+    w.nf[r][lane] = le_N(L.arc_fwd) | (le_fwd(L.arc_fwd) << 16);
+    w.ax[r][lane] = le_arc(L.arc_fwd);
+  }
+  __syncwarp();
+  const int nq = (cnt < MAXRA ? cnt : MAXRA) * 3;
+  float4 *dst = reinterpret_cast<float4 *>(w.arc[r]);
+  for (int k = lane; k < nq; k += 32) dst[k] = __ldg(reinterpret_cast<const float4 *>(arcs + w.ax[r][k / 3]) + (k % 3));
+}
+
+__device__ void emit_band(const TriParams &P, WarpRing &w, int s, int64_t first, int64_t last,
+                          unsigned char *out, int lane) {
+  const int64_t base = P.strut_off[s];
   const int4 bd = P.band[s];
   const int nA = bd.x, nB = bd.y, kB = bd.z;
-  const int64_t base = P.strut_off[s];
+  const int64_t ta = base > first ? base : first;
+  const int64_t tb = base + nA + nB < last ? base + nA + nB : last;
+  if (ta >= tb) return;
+  const int2 e = P.ends[s];
+  const int2 ce = P.strut_csr[s];
   const int2 LA = P.loop_hdr[ce.x], LB = P.loop_hdr[ce.y];
   const float4 oa = P.node[e.x], ob = P.node[e.y];
-  PtCursor A, B;
-  A.le = P.loop + lbase(P.csr_off, e.x) + LA.x; A.arcs = P.arc + abase(P.csr_off, e.x);
-  A.vs = P.vert + vbase(P.csr_off, e.x); A.cnt = LA.y; A.ox = oa.x; A.oy = oa.y; A.oz = oa.z;
-  B.le = P.loop + lbase(P.csr_off, e.y) + LB.x; B.arcs = P.arc + abase(P.csr_off, e.y);
-  B.vs = P.vert + vbase(P.csr_off, e.y); B.cnt = LB.y; B.ox = ob.x; B.oy = ob.y; B.oz = ob.z;
-  A.load(0);
-  B.load(0);
-  int i = merge_rank(P, base, t);
-  int j = (int)(t - base) - i;
-  f3 pa = A.point(i % nA);
-  int jb = (j + kB) % nB;
-  f3 pb = B.point(jb);
-  for (; t < t1; t++) {
-    bool advA = (__ldg(&P.mbits[t >> 5]) >> (t & 31)) & 1u;
-    unsigned char *dst = stage + (t - sbase) * REC;
-    if (advA) {
-      i++;
-      f3 pa1 = A.point(i == nA ? 0 : i);
-      put_rec(dst, pa, pa1, pb);
-      pa = pa1;
-    } else {
-      j++;
-      int jb1 = jb + 1 == nB ? 0 : jb + 1;
-      f3 pb1 = B.point(jb1);
-      put_rec(dst, pa, pb1, pb);
-      pb = pb1;
-      jb = jb1;
+  RingRef RA, RB;
+  RA.arcs = P.arc + abase(P.csr_off, e.x); RA.vs = P.vert + vbase(P.csr_off, e.x);
+  RA.ox = oa.x; RA.oy = oa.y; RA.oz = oa.z; RA.cnt = LA.y;
+  RB.arcs = P.arc + abase(P.csr_off, e.y); RB.vs = P.vert + vbase(P.csr_off, e.y);
+  RB.ox = ob.x; RB.oy = ob.y; RB.oz = ob.z; RB.cnt = LB.y;
+  load_ring(w, 0, P.loop + lbase(P.csr_off, e.x) + LA.x, LA.y, RA.arcs, lane);
+  load_ring(w, 1, P.loop + lbase(P.csr_off, e.y) + LB.x, LB.y, RB.arcs, lane);
+  __syncwarp();
+  const int qb = (int)(ta - base), qe = (int)(tb - base);
+  const unsigned lt = (1u << lane) - 1u;
+  for (int q0 = qb; q0 < qe; q0 += WIN) {
+    const int q1 = q0 + WIN < qe ? q0 + WIN : qe;
+    int i0 = 0, i1 = 0;
+    if (lane == 0) i0 = merge_rank(P, base, base + q0);
+    if (lane == 1) i1 = (q1 == nA + nB) ? nA : merge_rank(P, base, base + q1);
+    i0 = __shfl_sync(0xffffffffu, i0, 0);
+    i1 = __shfl_sync(0xffffffffu, i1, 1);
+    const int j0 = q0 - i0, j1 = q1 - i1;
+    const int na = i1 - i0 + 1, nb = j1 - j0 + 1;
+    for (int k = lane; k < na + nb; k += 32) {
+      f3 p;
+      int r, kk;
+      if (k < na) { int idx = i0 + k; p = ring_point(w, 0, RA, idx >= nA ? idx - nA : idx); r = 0; kk = k; }
+      else { kk = k - na; int idx = j0 + kk + kB; idx = idx >= nB ? idx - nB : idx; idx = idx >= nB ? idx - nB : idx;
+             p = ring_point(w, 1, RB, idx); r = 1; }
+      w.px[r][kk] = p.x; w.py[r][kk] = p.y; w.pz[r][kk] = p.z;
     }
+    __syncwarp();
+    int irun = i0;
+    int qq = q0;
+    // the record of step q is the triangle (A_i, A_i+1, B_j) or (A_i, B_j+1, B_j)
+    auto tri = [&](int q, int i, bool advA, uint32_t *f) {
+      const int ia = i - i0, jb = (q - i) - j0;
+      f3 pa = F3(w.px[0][ia], w.py[0][ia], w.pz[0][ia]);
+      f3 pb = F3(w.px[1][jb], w.py[1][jb], w.pz[1][jb]);
+      if (advA) tri_words(pa, F3(w.px[0][ia + 1], w.py[0][ia + 1], w.pz[0][ia + 1]), pb, f);
+      else tri_words(pa, F3(w.px[1][jb + 1], w.py[1][jb + 1], w.pz[1][jb + 1]), pb, f);
+    };
+    // unaligned head (< 8 triangles): one record per lane, 2-byte stores
+    {
+      const int mis = (int)((base + qq - first) & 7);
+      if (mis) {
+        const int hl = (8 - mis) < (q1 - qq) ? (8 - mis) : (q1 - qq);
+        const int q = qq + lane;
+        const bool valid = lane < hl;
+        const int64_t t = base + q;
+        const bool advA = valid && ((__ldg(&P.mbits[t >> 5]) >> (t & 31)) & 1u);
+        const unsigned m = __ballot_sync(0xffffffffu, advA);
+        if (valid) {
+          uint32_t f[12];
+          tri(q, irun + __popc(m & lt), advA, f);
+          put_rec16(out + (t - first) * REC, f);
+        }
+        irun += __popc(m);
+        qq += hl;
+      }
+    }
+    // aligned groups of 64: lane l takes steps qq+2l, qq+2l+1
+    for (; qq < q1; qq += GRP) {
+      const int gl = q1 - qq < GRP ? q1 - qq : GRP;
+      const int qa = qq + 2 * lane, qb2 = qa + 1;
+      const bool va = qa < qq + gl, vb = qb2 < qq + gl;
+      const int64_t ta2 = base + qa;
+      const uint32_t wa = __ldg(&P.mbits[ta2 >> 5]);
+      const bool aa = va && ((wa >> (ta2 & 31)) & 1u);
+      const bool ab = vb && ((__ldg(&P.mbits[(ta2 + 1) >> 5]) >> ((ta2 + 1) & 31)) & 1u);
+      const unsigned ma = __ballot_sync(0xffffffffu, aa), mb = __ballot_sync(0xffffffffu, ab);
+      const int ia = irun + __popc(ma & lt) + __popc(mb & lt);
+      irun += __popc(ma) + __popc(mb);
+      if (va) {
+        uint32_t f[12], g[12];
+        tri(qa, ia, aa, f);
+        if (vb) tri(qb2, ia + (aa ? 1 : 0), ab, g);
+        else {
+#pragma unroll
+          for (int i = 0; i < 12; i++) g[i] = 0;
+        }
+        put_pair(reinterpret_cast<uint32_t *>(w.stage) + 25 * lane, f, g);
+      }
+      flush_group(w, gl * REC, out + (base + qq - first) * REC, lane);
+    }
+    __syncwarp();
   }
 }
 
-__device__ void emit_hole_run(const TriParams &P, int64_t g, int64_t t, int64_t t1, unsigned char *stage, int64_t sbase) {
+__device__ void emit_hole(const TriParams &P, WarpRing &w, int g, int64_t first, int64_t last,
+                          unsigned char *out, int lane) {
+  const int64_t hb = P.n_tri_band + P.hole_off[g];
+  const int M = P.hole_M[g];
+  const int64_t ta = hb > first ? hb : first;
+  const int64_t tb = hb + M < last ? hb + M : last;
+  if (ta >= tb) return;
   const int n = P.hole_node[g];
   const int64_t g0 = P.node_hole0[n];
   const int2 H = P.hole_hdr[hbase(P.csr_off, n) + (g - g0)];
   const float4 on = P.node[n];
   const float4 bp4 = P.hole_bp[g];
   const f3 bp = F3(on.x + bp4.x, on.y + bp4.y, on.z + bp4.z);
-  const int M = P.hole_M[g];
-  const int64_t hb = P.n_tri_band + P.hole_off[g];
-  // hole entries have the loop-entry layout's first two words (arc_fwd, cum)
+  RingRef RH;
+  RH.arcs = P.arc + abase(P.csr_off, n); RH.vs = P.vert + vbase(P.csr_off, n);
+  RH.ox = on.x; RH.oy = on.y; RH.oz = on.z; RH.cnt = H.y;
+  // hole entries: (arc_fwd, cum) as in loop entries
   const HoleEnt *he = P.hole_ent + hebase(P.csr_off, n) + H.x;
-  const ArcRec *arcs = P.arc + abase(P.csr_off, n);
-  const float4 *vs = P.vert + vbase(P.csr_off, n);
-  int m = (int)(t - hb);
-  int e = 0;
-  auto point = [&](int idx) -> f3 {
-    if (idx < he[e].cum) e = 0;
-    while (e + 1 < H.y && idx >= he[e + 1].cum) e++;
-    uint32_t af = he[e].arc_fwd;
-    ArcRec A = load_arc(arcs + le_arc(af));
-    int N = le_N(af), j = idx - he[e].cum;
-    f3 p = arc_point(A, vs, N, le_fwd(af) ? j : N - j);
-    return F3(on.x + p.x, on.y + p.y, on.z + p.z);
-  };
-  f3 p = point(m);
-  for (; t < t1; t++) {
-    m++;
-    f3 p1 = point(m == M ? 0 : m);
-    put_rec(stage + (t - sbase) * REC, bp, p, p1);
-    p = p1;
+  if (lane < H.y) {
+    HoleEnt E = he[lane];
+    w.cum[0][lane] = E.cum; w.nf[0][lane] = le_N(E.arc_fwd) | (le_fwd(E.arc_fwd) << 16); w.ax[0][lane] = le_arc(E.arc_fwd);
+  }
+  __syncwarp();
+  {
+    const int nq = (H.y < MAXRA ? H.y : MAXRA) * 3;
+    float4 *dst = reinterpret_cast<float4 *>(w.arc[0]);
+    for (int k = lane; k < nq; k += 32) dst[k] = __ldg(reinterpret_cast<const float4 *>(RH.arcs + w.ax[0][k / 3]) + (k % 3));
+  }
+  __syncwarp();
+  const int mb = (int)(ta - hb), me = (int)(tb - hb);
+  for (int m0 = mb; m0 < me; m0 += WIN) {
+    const int m1 = m0 + WIN < me ? m0 + WIN : me;
+    for (int k = lane; k <= m1 - m0; k += 32) {
+      int idx = m0 + k;
+      f3 p = ring_point(w, 0, RH, idx >= M ? idx - M : idx);
+      w.px[0][k] = p.x; w.py[0][k] = p.y; w.pz[0][k] = p.z;
+    }
+    __syncwarp();
+    for (int mm = m0; mm < m1; mm += 32) {
+      const int m = mm + lane;
+      if (m < m1) {
+        int k = m - m0;
+        uint32_t f[12];
+        tri_words(bp, F3(w.px[0][k], w.py[0][k], w.pz[0][k]), F3(w.px[0][k + 1], w.py[0][k + 1], w.pz[0][k + 1]), f);
+        put_rec16(out + (hb + m - first) * REC, f);
+      }
+    }
+    __syncwarp();
   }
 }
 
@@ -432,80 +590,18 @@ __device__ __forceinline__ int64_t upper_bound64(const int64_t *a, int64_t lo, i
   return lo;
 }
 
-__global__ void __launch_bounds__(EMIT_T) k_emit(TriParams P, int64_t first, int64_t count, unsigned char *out) {
-  extern __shared__ __align__(128) unsigned char stage[];
-  __shared__ int64_t soff[MAXSB + 1];
-  __shared__ int sb0, nsb;
+// units: bands [s0, s1) then holes [g0, g1) intersecting [first, last)
+__global__ void __launch_bounds__(EMIT_T) k_emit(TriParams P, int64_t first, int64_t count, unsigned char *out,
+                                                 int64_t s0, int64_t s1, int64_t g0, int64_t g1) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  WarpRing &w = reinterpret_cast<WarpRing *>(smem)[warp];
   const int64_t last = first + count;
-  const int64_t c0 = first / TPC, c1 = (last + TPC - 1) / TPC;
-  const bool congruent = ((first % 8) == 0);   // record offsets then stay 16-byte congruent
-  for (int64_t c = c0 + blockIdx.x; c < c1; c += gridDim.x) {
-    const int64_t cs = c * TPC;
-    const int64_t lo = cs > first ? cs : first;
-    const int64_t hi = cs + TPC < last ? cs + TPC : last;
-    // band offsets of this chunk into shared memory
-    if (threadIdx.x == 0) {
-      int b0 = lo < P.n_tri_band ? P.cmap[c] : -1;
-      sb0 = b0;
-      int cnt = 0;
-      if (b0 >= 0) {
-        int64_t lim = P.S - b0;
-        cnt = (int)(lim < MAXSB ? lim : MAXSB);
-      }
-      nsb = cnt;
-    }
-    __syncthreads();
-    if (sb0 >= 0)
-      for (int k = threadIdx.x; k <= nsb; k += EMIT_T) soff[k] = P.strut_off[sb0 + k];
-    __syncthreads();
-    int64_t t = lo + (int64_t)threadIdx.x * EMIT_R;
-    const int64_t tend = t + EMIT_R < hi ? t + EMIT_R : hi;
-    while (t < tend) {
-      if (t < P.n_tri_band) {
-        int64_t s;
-        if (sb0 >= 0 && t < soff[nsb]) {
-          int a = 0, b = nsb;   // last k with soff[k] <= t
-          while (b - a > 1) { int m = (a + b) >> 1; if (soff[m] <= t) a = m; else b = m; }
-          s = sb0 + a;
-        } else {
-          s = upper_bound64(P.strut_off, 0, P.S + 1, t) - 1;
-        }
-        int64_t bend = P.strut_off[s + 1];
-        int64_t t1 = tend < bend ? tend : bend;
-        emit_band_run(P, s, t, t1, stage, cs);
-        t = t1;
-      } else {
-        int64_t tl = t - P.n_tri_band;
-        int64_t g = cs >= P.n_tri_band ? P.cmap[c] : 0;   // hole holding the chunk's first triangle
-        g = upper_bound64(P.hole_off, g, P.H + 1, tl) - 1;
-        int64_t hend = P.n_tri_band + P.hole_off[g + 1];
-        int64_t t1 = tend < hend ? tend : hend;
-        emit_hole_run(P, g, t, t1, stage, cs);
-        t = t1;
-      }
-    }
-    // chunk -> global: TMA bulk store of the 16-byte-aligned body, plain stores around it
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    __syncthreads();
-    const int64_t sb = (lo - cs) * REC, se = (hi - cs) * REC;   // staging byte range
-    unsigned char *gdst = out + (lo - first) * REC - sb;          // gdst[sb..se) <- stage[sb..se)
-    int64_t bb = sb, be = sb;
-    if (congruent) {
-      bb = (sb + 15) & ~(int64_t)15;
-      be = se & ~(int64_t)15;
-      if (be < bb) be = bb;
-    }
-    if (threadIdx.x == 0 && be > bb) {
-      uint32_t saddr = (uint32_t)__cvta_generic_to_shared(stage + bb);
-      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst + bb), "r"(saddr),
-                   "r"((uint32_t)(be - bb))
-                   : "memory");
-      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-    }
-    for (int64_t b = sb + threadIdx.x; b < bb; b += EMIT_T) gdst[b] = stage[b];
-    for (int64_t b = (be > bb ? be : bb) + threadIdx.x; b < se; b += EMIT_T) gdst[b] = stage[b];
-    if (threadIdx.x == 0 && be > bb) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-    __syncthreads();
+  const int64_t gw = (int64_t)blockIdx.x * EW + warp, nw = (int64_t)gridDim.x * EW;
+  const int64_t nb = s1 - s0, nh = g1 - g0;
+  for (int64_t u = gw; u < nb + nh; u += nw) {
+    if (u < nb) emit_band(P, w, (int)(s0 + u), first, last, out, lane);
+    else emit_hole(P, w, (int)(g0 + u - nb), first, last, out, lane);
   }
 }
 
@@ -597,7 +693,7 @@ int triangulate_count(lmm_ctx *c) {
 int triangulate_emit(lmm_ctx *c, int64_t first, int64_t count, void *out_dev, cudaStream_t st) {
   if (count <= 0) return LMM_OK;
   TriParams P = make_params(c);
-  const size_t smem = (size_t)TPC * REC;
+  const size_t smem = sizeof(WarpRing) * EW;
   static bool attr_set = false;
   static int occ = 1;
   if (!attr_set) {
@@ -606,11 +702,35 @@ int triangulate_emit(lmm_ctx *c, int64_t first, int64_t count, void *out_dev, cu
     if (occ < 1) occ = 1;
     attr_set = true;
   }
-  int64_t nch = (first + count + TPC - 1) / TPC - first / TPC;
+  // bands and holes intersecting [first, last): the chunk map at the chunk holding
+  // `first` bounds the first unit, the one of the chunk after `last - 1` the last unit
+  const int64_t last = first + count;
+  const int64_t nch = (c->n_tri + TPC - 1) / TPC;
+  int64_t s0 = c->S, s1 = c->S, g0 = c->H, g1 = c->H;
+  if (!c->pinned_scalar) CUDA_TRY(cudaMallocHost((void **)&c->pinned_scalar, 64));
+  int *hm = (int *)(c->pinned_scalar + 2);
+  const int64_t ca = first / TPC, cn = (last - 1) / TPC + 1;
+  CUDA_TRY(cudaMemcpyAsync(hm, (int *)c->cmap.p + ca, sizeof(int), cudaMemcpyDeviceToHost, st));
+  if (cn < nch) CUDA_TRY(cudaMemcpyAsync(hm + 1, (int *)c->cmap.p + cn, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  const int64_t cna = cn * TPC;
+  if (first < c->n_tri_band) {
+    s0 = hm[0];
+    s1 = (cn < nch && cna < c->n_tri_band) ? (int64_t)hm[1] + 1 : c->S;
+  }
+  if (last > c->n_tri_band) {
+    g0 = (ca * TPC >= c->n_tri_band) ? hm[0] : 0;
+    g1 = (cn < nch && cna >= c->n_tri_band) ? (int64_t)hm[1] + 1 : c->H;
+  }
+  if (s1 < s0) s1 = s0;
+  if (g1 < g0) g1 = g0;
+  int64_t units = (s1 - s0) + (g1 - g0);
   int64_t grid = (int64_t)c->n_sm * occ;
-  if (grid > nch) grid = nch;
+  int64_t need = (units + EW - 1) / EW;
+  if (grid > need) grid = need;
+  if (grid < 1) grid = 1;
   KTimer t(c, LMM_K_EMIT);
-  (c->n_launch++), k_emit<<<(unsigned)grid, EMIT_T, smem, st>>>(P, first, count, (unsigned char *)out_dev);
+  (c->n_launch++), k_emit<<<(unsigned)grid, EMIT_T, smem, st>>>(P, first, count, (unsigned char *)out_dev, s0, s1, g0, g1);
   CUDA_TRY(cudaGetLastError());
   return LMM_OK;
 }
