@@ -22,7 +22,7 @@
 namespace {
 
 constexpr int TPC = 1024;       // triangles per emit chunk (51 200 B of records)
-constexpr int EMIT_T = 256;     // threads per emit CTA
+constexpr int EMIT_T = 128;     // threads per emit CTA
 constexpr int REC = 50;
 
 struct TriParams {
@@ -322,10 +322,10 @@ __device__ __forceinline__ void put_rec(unsigned char *dst, f3 a, f3 b, f3 c) {
 // staging buffer as 16-byte vector stores.  The <= 7 triangles before a band's first
 // aligned position go straight to global memory.  No block-level barriers.
 constexpr int EW = EMIT_T / 32;   // warps per CTA
-constexpr int WIN = 128;          // merge steps per window
+constexpr int WIN = 80;           // merge steps per window
 constexpr int GRP = 64;           // triangles per aligned group (3200 B)
 constexpr int MAXRE = 32;         // ring entries per ring (>= MAXLOOP of the meta-mesh)
-constexpr int MAXRA = 16;         // arc records cached per ring
+constexpr int MAXRA = 12;         // arc records cached per ring
 
 struct __align__(16) WarpRing {
   ArcRec arc[2][MAXRA];
@@ -407,16 +407,23 @@ __device__ __forceinline__ void put_rec16(unsigned char *dst, const uint32_t *f)
   d[24] = 0;
 }
 
-// staged group [0, bytes) -> global dst (16-byte aligned): vectors then 2-byte tail
-__device__ __forceinline__ void flush_group(WarpRing &w, int bytes, unsigned char *dst, int lane) {
+// staged group bytes [b0, b1) -> dst + [b0, b1), dst 16-byte aligned: 2-byte head up to the
+// first 16-byte boundary, 16-byte vectors, 2-byte tail (b0, b1 even)
+__device__ __forceinline__ void flush_group(WarpRing &w, int b0, int b1, unsigned char *dst, int lane) {
   __syncwarp();
-  const int nv = bytes >> 4;
-  uint4 *d = reinterpret_cast<uint4 *>(dst);
-  for (int k = lane; k < nv; k += 32) d[k] = w.stage[k];
-  const int tb = bytes - (nv << 4);
-  if (lane < (tb >> 1)) {
-    const uint16_t *s16 = reinterpret_cast<const uint16_t *>(w.stage + nv);
-    reinterpret_cast<uint16_t *>(dst + (nv << 4))[lane] = s16[lane];
+  const int v0 = (b0 + 15) >> 4, v1 = b1 >> 4;
+  const uint16_t *s16 = reinterpret_cast<const uint16_t *>(w.stage);
+  uint16_t *d16 = reinterpret_cast<uint16_t *>(dst);
+  if (v0 <= v1) {
+    const int h = (v0 << 3) - (b0 >> 1);          // head half-words
+    if (lane < h) d16[(b0 >> 1) + lane] = s16[(b0 >> 1) + lane];
+    uint4 *d = reinterpret_cast<uint4 *>(dst);
+    for (int k = v0 + lane; k < v1; k += 32) d[k] = w.stage[k];
+    const int t0 = v1 << 3, tn = (b1 >> 1) - t0;  // tail half-words
+    if (lane < tn) d16[t0 + lane] = s16[t0 + lane];
+  } else {                                          // range inside one 16-byte unit
+    const int n = (b1 - b0) >> 1;
+    if (lane < n) d16[(b0 >> 1) + lane] = s16[(b0 >> 1) + lane];
   }
   __syncwarp();
 }
@@ -456,8 +463,9 @@ __device__ void emit_band(const TriParams &P, WarpRing &w, int s, int64_t first,
   __syncwarp();
   const int qb = (int)(ta - base), qe = (int)(tb - base);
   const unsigned lt = (1u << lane) - 1u;
-  for (int q0 = qb; q0 < qe; q0 += WIN) {
-    const int q1 = q0 + WIN < qe ? q0 + WIN : qe;
+  for (int q0 = qb, q1; q0 < qe; q0 = q1) {
+    q1 = q0 - (int)((base + q0 - first) & 7) + WIN;   // windows end on the 8-triangle grid
+    q1 = q1 < qe ? q1 : qe;
     int i0 = 0, i1 = 0;
     if (lane == 0) i0 = merge_rank(P, base, base + q0);
     if (lane == 1) i1 = (q1 == nA + nB) ? nA : merge_rank(P, base, base + q1);
@@ -466,11 +474,16 @@ __device__ void emit_band(const TriParams &P, WarpRing &w, int s, int64_t first,
     const int j0 = q0 - i0, j1 = q1 - i1;
     const int na = i1 - i0 + 1, nb = j1 - j0 + 1;
     for (int k = lane; k < na + nb; k += 32) {
-      f3 p;
-      int r, kk;
-      if (k < na) { int idx = i0 + k; p = ring_point(w, 0, RA, idx >= nA ? idx - nA : idx); r = 0; kk = k; }
-      else { kk = k - na; int idx = j0 + kk + kB; idx = idx >= nB ? idx - nB : idx; idx = idx >= nB ? idx - nB : idx;
-             p = ring_point(w, 1, RB, idx); r = 1; }
+      const int r = k < na ? 0 : 1;                     // ring selected without branching
+      const int kk = r ? k - na : k;
+      const int n = r ? nB : nA;
+      int idx = r ? j0 + kk + kB : i0 + kk;
+      idx = idx >= n ? idx - n : idx;
+      idx = idx >= n ? idx - n : idx;
+      RingRef RR;
+      RR.arcs = r ? RB.arcs : RA.arcs; RR.vs = r ? RB.vs : RA.vs; RR.cnt = r ? RB.cnt : RA.cnt;
+      RR.ox = r ? RB.ox : RA.ox; RR.oy = r ? RB.oy : RA.oy; RR.oz = r ? RB.oz : RA.oz;
+      f3 p = ring_point(w, r, RR, idx);
       w.px[r][kk] = p.x; w.py[r][kk] = p.y; w.pz[r][kk] = p.z;
     }
     __syncwarp();
@@ -484,40 +497,27 @@ __device__ void emit_band(const TriParams &P, WarpRing &w, int s, int64_t first,
       if (advA) tri_words(pa, F3(w.px[0][ia + 1], w.py[0][ia + 1], w.pz[0][ia + 1]), pb, f);
       else tri_words(pa, F3(w.px[1][jb + 1], w.py[1][jb + 1], w.pz[1][jb + 1]), pb, f);
     };
-    // unaligned head (< 8 triangles): one record per lane, 2-byte stores
-    {
-      const int mis = (int)((base + qq - first) & 7);
-      if (mis) {
-        const int hl = (8 - mis) < (q1 - qq) ? (8 - mis) : (q1 - qq);
-        const int q = qq + lane;
-        const bool valid = lane < hl;
-        const int64_t t = base + q;
-        const bool advA = valid && ((__ldg(&P.mbits[t >> 5]) >> (t & 31)) & 1u);
-        const unsigned m = __ballot_sync(0xffffffffu, advA);
-        if (valid) {
-          uint32_t f[12];
-          tri(q, irun + __popc(m & lt), advA, f);
-          put_rec16(out + (t - first) * REC, f);
-        }
-        irun += __popc(m);
-        qq += hl;
-      }
-    }
-    // aligned groups of 64: lane l takes steps qq+2l, qq+2l+1
-    for (; qq < q1; qq += GRP) {
-      const int gl = q1 - qq < GRP ? q1 - qq : GRP;
-      const int qa = qq + 2 * lane, qb2 = qa + 1;
-      const bool va = qa < qq + gl, vb = qb2 < qq + gl;
+    // groups on the 8-triangle output grid (16-byte aligned records); a band's first group
+    // may start mid-grid: its lanes below the start stay idle and the flush begins with a
+    // partial 16-byte unit.  Lane l takes steps g+2l and g+2l+1.
+    for (int gq = q0 - (int)((base + q0 - first) & 7); gq < q1; gq += GRP) {
+      const int qa = gq + 2 * lane, qb2 = qa + 1;
+      const int lo_q = gq > q0 ? gq : q0;
+      const int hi_q = gq + GRP < q1 ? gq + GRP : q1;
+      const bool va = qa >= lo_q && qa < hi_q, vb = qb2 >= lo_q && qb2 < hi_q;
       const int64_t ta2 = base + qa;
-      const uint32_t wa = __ldg(&P.mbits[ta2 >> 5]);
-      const bool aa = va && ((wa >> (ta2 & 31)) & 1u);
+      const bool aa = va && ((__ldg(&P.mbits[ta2 >> 5]) >> (ta2 & 31)) & 1u);
       const bool ab = vb && ((__ldg(&P.mbits[(ta2 + 1) >> 5]) >> ((ta2 + 1) & 31)) & 1u);
       const unsigned ma = __ballot_sync(0xffffffffu, aa), mb = __ballot_sync(0xffffffffu, ab);
       const int ia = irun + __popc(ma & lt) + __popc(mb & lt);
       irun += __popc(ma) + __popc(mb);
-      if (va) {
+      if (va || vb) {
         uint32_t f[12], g[12];
-        tri(qa, ia, aa, f);
+        if (va) tri(qa, ia, aa, f);
+        else {
+#pragma unroll
+          for (int i = 0; i < 12; i++) f[i] = 0;
+        }
         if (vb) tri(qb2, ia + (aa ? 1 : 0), ab, g);
         else {
 #pragma unroll
@@ -525,7 +525,7 @@ __device__ void emit_band(const TriParams &P, WarpRing &w, int s, int64_t first,
         }
         put_pair(reinterpret_cast<uint32_t *>(w.stage) + 25 * lane, f, g);
       }
-      flush_group(w, gl * REC, out + (base + qq - first) * REC, lane);
+      flush_group(w, (lo_q - gq) * REC, (hi_q - gq) * REC, out + (base + gq - first) * REC, lane);
     }
     __syncwarp();
   }
@@ -591,7 +591,7 @@ __device__ __forceinline__ int64_t upper_bound64(const int64_t *a, int64_t lo, i
 }
 
 // units: bands [s0, s1) then holes [g0, g1) intersecting [first, last)
-__global__ void __launch_bounds__(EMIT_T) k_emit(TriParams P, int64_t first, int64_t count, unsigned char *out,
+__global__ void __launch_bounds__(EMIT_T, 8) k_emit(TriParams P, int64_t first, int64_t count, unsigned char *out,
                                                  int64_t s0, int64_t s1, int64_t g0, int64_t g1) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
