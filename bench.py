@@ -34,24 +34,26 @@ STL = 50
 EMIT_CHUNK = 1 << 28
 
 
-def make_config(name: str, rank: int = 0):
-    """Synthetic workload of BASELINE.json's configs (block `rank` of a weak-scaling stack)."""
-    if name == "octet100":
-        lat = synth.graded_radii(synth.octet(100, 100, 100), 0.03, 0.06, axis=0)
-        desc = "octet-truss 100x100x100 cells, conical struts (node radii graded 0.03-0.06 along x, pitch 1)"
+def make_config(name: str, rank: int = 0, world: int = 1):
+    """Synthetic workload of BASELINE.json's configs.  Weak scaling: the global lattice is
+    `world` blocks stacked along z; rank r gets its slab plus a 2-layer halo and the emit
+    masks of the nodes / struts it owns (paper_2405_15197_b200.partition)."""
+    from paper_2405_15197_b200 import partition as P
+    if name in ("octet100", "octet40"):
+        n = 100 if name == "octet100" else 40
+        k_top = 2 * n * world
+        k_lo, k_hi = P.window(rank, world, k_top) if world > 1 else (0, k_top)
+        lat = synth.octet_window(n, n, n * world, k_lo, k_hi, radius=0.03, r_max=0.06)
+        masks = P.emit_masks(lat.ijk[:, 2], lat.ends, rank, world, k_top) if world > 1 else (None, None)
+        desc = (f"octet-truss {n}x{n}x{n} cells per GPU (global {n}x{n}x{n * world}), conical struts "
+                f"(node radii graded 0.03-0.06 along x, pitch 1)")
     elif name == "bcc10":
         lat = synth.bcc(10, 10, 10)
+        masks = (None, None)
         desc = "BCC 10x10x10 cells, uniform strut radius 0.05 (pitch 1)"
-    elif name == "octet40":
-        lat = synth.graded_radii(synth.octet(40, 40, 40), 0.03, 0.06, axis=0)
-        desc = "octet-truss 40x40x40 cells, graded radii 0.03-0.06"
     else:
         raise SystemExit(f"unknown config {name}")
-    if rank:
-        xyz = lat.xyz.astype(np.float64)
-        xyz[:, 2] += rank * (xyz[:, 2].max() - xyz[:, 2].min() + 1.0)
-        lat = synth.Lattice(xyz.astype(np.float32), lat.ends, lat.node_r, lat.name)
-    return lat, desc
+    return lat, masks, desc
 
 
 class ClockSampler:
@@ -192,12 +194,22 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # LMM_BENCH_ONE_GPU=1: every rank on cuda:0 with a gloo group (tests the multi-rank path
+    # on a single device; timings are then not scaling numbers)
+    one_gpu = os.environ.get("LMM_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)
+    coll_dev = "cpu" if one_gpu else "cuda"
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    lat, desc = make_config(args.config, rank)
+    lat, (node_mask, strut_mask), desc = make_config(args.config, rank, world)
     S, N = lat.n_struts, lat.n_nodes
+    S_own = int(strut_mask.sum()) if strut_mask is not None else S
     xyz_h = torch.from_numpy(np.ascontiguousarray(lat.xyz)).pin_memory()
     ends_h = torch.from_numpy(np.ascontiguousarray(lat.ends)).pin_memory()
     rend_h = torch.from_numpy(np.ascontiguousarray(lat.r_end)).pin_memory()
@@ -206,10 +218,24 @@ def main():
     h = B.lmm_create(local, stream.cuda_stream)
     out = torch.empty(EMIT_CHUNK * STL, dtype=torch.uint8, device="cuda")
 
+    nmask_d = torch.from_numpy(node_mask).cuda() if node_mask is not None else None
+    smask_d = torch.from_numpy(strut_mask).cuda() if strut_mask is not None else None
+    cnt = torch.zeros(1, dtype=torch.int64, device=coll_dev)
+    cnts = torch.zeros(world, dtype=torch.int64, device=coll_dev)
+    offsets = {"base": 0, "total": 0}
+
     def step():
         B.lmm_load_lattice(h, xyz_d, ends_d, rend_d)
+        if world > 1:
+            B.lmm_set_emit_mask(h, nmask_d, smask_d)
         B.lmm_build_metamesh(h)
         T = B.lmm_triangulate(h, args.ce)
+        if world > 1:   # global output offsets: all-gather of the per-rank triangle counts
+            cnt.fill_(T)
+            parts = list(cnts.split(1))
+            dist.all_gather(parts, cnt)
+            c = [int(x) for x in torch.cat(parts).tolist()]
+            offsets["base"], offsets["total"] = sum(c[:rank]), sum(c)
         for f in range(0, T, EMIT_CHUNK):
             B.lmm_write_triangles(h, f, min(EMIT_CHUNK, T - f), out)
         return T
@@ -237,8 +263,8 @@ def main():
     st = B.lmm_metamesh_stats(h)
     ms = ev0.elapsed_time(ev1) / args.steps
     kt = B.lmm_kernel_times(h)
-    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-    tot = torch.tensor([float(S), float(T)], dtype=torch.float64, device="cuda")
+    t = torch.tensor([ms], dtype=torch.float64, device=coll_dev)
+    tot = torch.tensor([float(S_own), float(T)], dtype=torch.float64, device=coll_dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.all_reduce(tot, op=dist.ReduceOp.SUM)
@@ -254,6 +280,8 @@ def main():
 
         def e2e_step():
             B.lmm_load_lattice(h2, xyz_h, ends_h, rend_h)
+            if world > 1:
+                B.lmm_set_emit_mask(h2, node_mask, strut_mask)
             B.lmm_build_metamesh(h2)
             T2 = B.lmm_triangulate(h2, args.ce)
             for f in range(0, T2, chunk):
@@ -268,7 +296,7 @@ def main():
             T2 = e2e_step()
         torch.cuda.synchronize()
         e2e_ms = (time.perf_counter() - t0) * 1e3 / args.e2e_steps
-        te = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
+        te = torch.tensor([e2e_ms], dtype=torch.float64, device=coll_dev)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e_ms = float(te.item())
@@ -310,11 +338,12 @@ def main():
         "vs_baseline": None,
         "dtype": "f32",
         "data": "synthetic",
-        "config": {"workload": desc, "chord_error": args.ce, "n_struts": S, "n_nodes": N,
+        "config": {"workload": desc, "chord_error": args.ce, "n_struts": int(S_all), "n_struts_local": S,
+                   "n_nodes_local": N, "global_output_offset_rank0": offsets["base"],
                    "triangles_per_step": int(T), "parallelism": f"dp{world} (one spatial block per GPU)",
                    "l2": "output chunks of 13.4 GB >> 126 MB L2 (no flush needed)",
                    "error_nodes": st["n_error_nodes"]},
-        "metamesh_struts_per_s": S * args.steps / (mm_ms / 1e3) if mm_ms else None,
+        "metamesh_struts_per_s": S_own * args.steps / (mm_ms / 1e3) if mm_ms else None,
         "triangles_per_s": T_all / (ms_max / 1e3),
         "triangulate_triangles_per_s": T * args.steps / (tri_ms / 1e3) if tri_ms else None,
         "kernel_ms_per_step": {k: v[0] / args.steps for k, v in kt.items()},

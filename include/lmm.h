@@ -99,6 +99,15 @@ LMM_API int lmm_build_metamesh(lmm_ctx *ctx);
 /* Totals and histograms of the current meta-mesh (synchronises). */
 LMM_API int lmm_metamesh_stats(lmm_ctx *ctx, lmm_stats *out);
 
+/* Restrict emission to a subset (spatial partitioning across GPUs): only struts with
+ * strut_mask[s] != 0 contribute their band and only nodes with node_mask[n] != 0 their
+ * hole fans (counts become 0 otherwise; the meta-mesh of every node is still built, so
+ * halo nodes give the bands of boundary struts their far-end loops).
+ *   node_mask  : uint8 [n_nodes] or NULL (= all), strut_mask : uint8 [n_struts] or NULL (= all)
+ *   where      : LMM_HOST or LMM_DEVICE for both arrays.
+ * Cleared by lmm_load_lattice; takes effect at the next lmm_triangulate. */
+LMM_API int lmm_set_emit_mask(lmm_ctx *ctx, const uint8_t *node_mask, const uint8_t *strut_mask, int where);
+
 /* Count pass for chord error CE (fraction of the radius, 0 < CE <= 1): per-arc
  * subdivision counts N (Eq. 11), band and hole triangle counts, device prefix scan of
  * the output offsets.  *n_triangles receives the total (synchronises).  Reuses the

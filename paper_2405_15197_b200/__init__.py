@@ -5,11 +5,11 @@ include/lmm.h); this package is its thin binding plus the meta-mesh decoder used
 tests and the benchmark.  See DESIGN.md.
 """
 from .binding import (LmmError, LMM_DEVICE, LMM_HOST, lmm_build_metamesh, lmm_buffer, lmm_create, lmm_destroy,
-                      lmm_kernel_times, lmm_load_lattice, lmm_metamesh_stats, lmm_reset_kernel_times, lmm_sync,
+                      lmm_kernel_times, lmm_load_lattice, lmm_metamesh_stats, lmm_reset_kernel_times, lmm_set_emit_mask, lmm_sync,
                       lmm_timing, lmm_triangulate, lmm_write_triangles, load_library, stl_records_to_array)
 from .metamesh import MetaMesher, decode_node
 
 __all__ = ["LmmError", "LMM_DEVICE", "LMM_HOST", "MetaMesher", "decode_node", "lmm_build_metamesh", "lmm_buffer",
            "lmm_create", "lmm_destroy", "lmm_kernel_times", "lmm_load_lattice", "lmm_metamesh_stats",
-           "lmm_reset_kernel_times", "lmm_sync", "lmm_timing", "lmm_triangulate", "lmm_write_triangles",
+           "lmm_reset_kernel_times", "lmm_set_emit_mask", "lmm_sync", "lmm_timing", "lmm_triangulate", "lmm_write_triangles",
            "load_library", "stl_records_to_array"]

@@ -53,6 +53,7 @@ def load_library():
     lib.lmm_build_metamesh.argtypes = [P]
     lib.lmm_metamesh_stats.argtypes = [P, C.POINTER(_Stats)]
     lib.lmm_triangulate.argtypes = [P, C.c_double, C.POINTER(i64)]
+    lib.lmm_set_emit_mask.argtypes = [P, P, P, i32]
     lib.lmm_write_triangles.argtypes = [P, i64, i64, P, i32]
     lib.lmm_sync.argtypes = [P]
     lib.lmm_buffer_size.argtypes = [P, i32, C.POINTER(i64)]
@@ -66,7 +67,7 @@ def load_library():
     lib.lmm_version.restype = C.c_char_p
     for name in ("lmm_create", "lmm_load_lattice", "lmm_build_metamesh", "lmm_metamesh_stats", "lmm_triangulate",
                  "lmm_write_triangles", "lmm_sync", "lmm_buffer_size", "lmm_copy_buffer", "lmm_timing",
-                 "lmm_kernel_times", "lmm_reset_kernel_times", "lmm_launch_count"):
+                 "lmm_kernel_times", "lmm_reset_kernel_times", "lmm_launch_count", "lmm_set_emit_mask"):
         getattr(lib, name).restype = i32
     _lib = lib
     return lib
@@ -117,6 +118,14 @@ def lmm_metamesh_stats(h) -> dict:
     out["err_hist"] = list(st.err_hist)
     out["degree_hist"] = list(st.degree_hist)
     return out
+
+
+def lmm_set_emit_mask(h, node_mask=None, strut_mask=None):
+    """uint8 masks (numpy host or torch device arrays), None = all."""
+    pn, wn = _ptr(node_mask) if node_mask is not None else (None, None)
+    ps, ws = _ptr(strut_mask) if strut_mask is not None else (None, None)
+    where = wn if wn is not None else (ws if ws is not None else LMM_HOST)
+    _check(load_library().lmm_set_emit_mask(h, pn, ps, where))
 
 
 def lmm_triangulate(h, chord_error: float) -> int:

@@ -97,7 +97,7 @@ static void free_all(lmm_ctx *c) {
   DevBuf *bufs[] = {&c->node, &c->ends, &c->csr_off, &c->csr_ent, &c->strut_csr, &c->deg_hist, &c->bucket_nodes,
                     &c->bucket_cnt, &c->node_hdr, &c->vert, &c->arc, &c->loop_hdr, &c->loop, &c->hole_hdr,
                     &c->hole_ent, &c->band, &c->strut_off, &c->node_hole0, &c->node_hole0_64, &c->hole_M,
-                    &c->hole_off, &c->hole_bp, &c->hole_node, &c->mbits, &c->macc, &c->cmap, &c->tmp64, &c->scratch, &c->scan_tmp, &c->stage[0], &c->stage[1]};
+                    &c->hole_off, &c->hole_bp, &c->hole_node, &c->node_mask, &c->strut_mask, &c->mbits, &c->macc, &c->cmap, &c->tmp64, &c->scratch, &c->scan_tmp, &c->stage[0], &c->stage[1]};
   for (DevBuf *b : bufs) dev_free(*b);
 }
 
@@ -147,6 +147,7 @@ LMM_API int lmm_load_lattice(lmm_ctx *c, const float *xyz, int64_t n_nodes, cons
     if (n_nodes) CUDA_TRY(cudaMemcpyAsync((void *)dx, xyz, bx, cudaMemcpyHostToDevice, c->stream));
     if (n_struts) CUDA_TRY(cudaMemcpyAsync((void *)dr, r_end, br, cudaMemcpyHostToDevice, c->stream));
   }
+  c->has_node_mask = c->has_strut_mask = false;
   int rc = lattice_build(c, dx, de, dr);
   if (tmp) cudaFreeAsync(tmp, c->stream);
   if (rc) return rc;
@@ -200,6 +201,27 @@ LMM_API int lmm_metamesh_stats(lmm_ctx *c, lmm_stats *out) {
   }
   out->n_elliptical_arcs = out->n_arcs - out->n_circular_arcs;
   free(hdr);
+  return LMM_OK;
+}
+
+LMM_API int lmm_set_emit_mask(lmm_ctx *c, const uint8_t *node_mask, const uint8_t *strut_mask, int where) {
+  if (!c || (where != LMM_HOST && where != LMM_DEVICE)) return LMM_E_ARG;
+  if (!c->lattice_ok) return LMM_E_STATE;
+  CUDA_TRY(cudaSetDevice(c->device));
+  const cudaMemcpyKind kind = where == LMM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+  int rc;
+  c->has_node_mask = node_mask != nullptr;
+  c->has_strut_mask = strut_mask != nullptr;
+  if (node_mask && c->N) {
+    if ((rc = dev_alloc(c->node_mask, (size_t)c->N))) return rc;
+    CUDA_TRY(cudaMemcpyAsync(c->node_mask.p, node_mask, (size_t)c->N, kind, c->stream));
+  }
+  if (strut_mask && c->S) {
+    if ((rc = dev_alloc(c->strut_mask, (size_t)c->S))) return rc;
+    CUDA_TRY(cudaMemcpyAsync(c->strut_mask.p, strut_mask, (size_t)c->S, kind, c->stream));
+  }
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  c->tri_ok = false;
   return LMM_OK;
 }
 

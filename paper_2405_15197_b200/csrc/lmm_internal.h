@@ -50,6 +50,9 @@ struct lmm_ctx {
   DevBuf hole_off;   // int64 [H+1]
   DevBuf hole_bp;    // float4 [H]
   DevBuf hole_node;  // int [H]
+  DevBuf node_mask;  // uint8 [N] hole emission mask (empty = all)
+  DevBuf strut_mask; // uint8 [S] band emission mask (empty = all)
+  bool has_node_mask = false, has_strut_mask = false;
   DevBuf mbits;      // uint32 merge bits (1 per band triangle)
   DevBuf macc;       // int per merge word
   DevBuf cmap;       // int per emit chunk

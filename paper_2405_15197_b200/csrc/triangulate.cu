@@ -52,6 +52,8 @@ struct TriParams {
   uint32_t *mbits;          // merge bits, bit t = triangle t advances ring A
   int *macc;                // [word] A-advances of the band before the word's first bit
   int *cmap;                // [chunk] first band (band region) / hole (hole region)
+  const uint8_t *node_mask; // [N] or null
+  const uint8_t *strut_mask;// [S] or null
   int64_t n_chunks;
 };
 
@@ -114,7 +116,8 @@ __global__ void k_band_count(TriParams P) {
   int2 ce = P.strut_csr[s];
   int4 hA = P.node_hdr[e.x], hB = P.node_hdr[e.y];
   int nA = 0, nB = 0, kB = 0;
-  if ((hA.x & 0xff) == 0 && (hB.x & 0xff) == 0) {
+  const bool emit = !P.strut_mask || P.strut_mask[s];
+  if (emit && (hA.x & 0xff) == 0 && (hB.x & 0xff) == 0) {
     int2 LA = P.loop_hdr[ce.x], LB = P.loop_hdr[ce.y];
     LoopRec *la = P.loop + lbase(P.csr_off, e.x) + LA.x;
     LoopRec *lb = P.loop + lbase(P.csr_off, e.y) + LB.x;
@@ -212,11 +215,11 @@ __global__ void k_band_merge(TriParams P) {
   }
 }
 
-__global__ void k_node_nholes(const int4 *hdr, int64_t N, int *nh) {
+__global__ void k_node_nholes(const int4 *hdr, int64_t N, const uint8_t *mask, int *nh) {
   int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (n >= N) return;
   int4 h = hdr[n];
-  nh[n] = (h.x & 0xff) == 0 ? (h.z & 0xffff) : 0;
+  nh[n] = ((h.x & 0xff) == 0 && (!mask || mask[n])) ? (h.z & 0xffff) : 0;
 }
 
 __global__ void k_hole_count(TriParams P) {
@@ -635,6 +638,8 @@ TriParams make_params(lmm_ctx *c) {
   P.mbits = (uint32_t *)c->mbits.p;
   P.macc = (int *)c->macc.p;
   P.cmap = (int *)c->cmap.p;
+  P.node_mask = c->has_node_mask ? (const uint8_t *)c->node_mask.p : nullptr;
+  P.strut_mask = c->has_strut_mask ? (const uint8_t *)c->strut_mask.p : nullptr;
   P.n_chunks = (c->n_tri + TPC - 1) / TPC;
   return P;
 }
@@ -654,7 +659,7 @@ int triangulate_count(lmm_ctx *c) {
   {
     KTimer t(c, LMM_K_COUNT);
     if (S) (c->n_launch++), k_band_count<<<(unsigned)((S + T - 1) / T), T, 0, c->stream>>>(P);
-    if (N) (c->n_launch++), k_node_nholes<<<(unsigned)((N + T - 1) / T), T, 0, c->stream>>>((const int4 *)c->node_hdr.p, N, (int *)c->node_hole0.p);
+    if (N) (c->n_launch++), k_node_nholes<<<(unsigned)((N + T - 1) / T), T, 0, c->stream>>>((const int4 *)c->node_hdr.p, N, c->has_node_mask ? (const uint8_t *)c->node_mask.p : nullptr, (int *)c->node_hole0.p);
     CUDA_TRY(cudaGetLastError());
   }
   if ((rc = scan_exclusive_i64(c, (const int64_t *)c->tmp64.p, (int64_t *)c->strut_off.p, S, &c->n_tri_band))) return rc;

@@ -41,6 +41,10 @@ class MetaMesher:
     def stats(self) -> dict:
         return B.lmm_metamesh_stats(self.h)
 
+    def set_emit_mask(self, node_mask=None, strut_mask=None):
+        B.lmm_set_emit_mask(self.h, node_mask, strut_mask)
+        return self
+
     def triangulate(self, chord_error: float) -> int:
         return B.lmm_triangulate(self.h, chord_error)
 

@@ -22,6 +22,8 @@ class Lattice:
     ends: np.ndarray     # int64   [S, 2]
     node_r: np.ndarray   # float32 [N]
     name: str = "lattice"
+    ijk: np.ndarray | None = None   # int64 [N, 3] integer lattice coordinates (windowed generators)
+    gid: np.ndarray | None = None   # int64 [N] global node ids (windowed generators), ascending
 
     @property
     def n_nodes(self) -> int:
@@ -137,6 +139,39 @@ def octet(nx: int, ny: int, nz: int, pitch: float = 1.0, radius: float = 0.04) -
         ends.append(np.stack([np.nonzero(m)[0], lut[q[m, 0], q[m, 1], q[m, 2]]], 1))
     xyz = g.astype(np.float64) * (0.5 * pitch)
     return _finish(xyz, np.concatenate(ends), _radii(len(g), radius), f"octet{nx}x{ny}x{nz}")
+
+
+def octet_window(nx: int, ny: int, nz: int, k_lo: int, k_hi: int, pitch: float = 1.0,
+                 radius: float = 0.04, r_max: float | None = None) -> Lattice:
+    """The part of the octet truss of nx*ny*nz cells whose FCC points have half-pitch z index
+    k in [k_lo, k_hi] (clipped to [0, 2nz]), with the struts among them.  Nodes are listed in
+    ascending global id gid = (i*(2ny+1) + j)*(2nz+1) + k and struts in ascending (gid, gid),
+    so any two windows order the struts of a shared node identically.  With r_max given, node
+    radii are graded radius..r_max along x (as graded_radii on the full lattice)."""
+    k_lo, k_hi = max(0, k_lo), min(2 * nz, k_hi)
+    I, J, K = np.meshgrid(np.arange(2 * nx + 1), np.arange(2 * ny + 1), np.arange(k_lo, k_hi + 1), indexing="ij")
+    g = np.stack([I, J, K], -1).reshape(-1, 3)
+    g = g[(g.sum(1) % 2) == 0]
+    lut = -np.ones((2 * nx + 1, 2 * ny + 1, k_hi - k_lo + 1), dtype=np.int64)
+    lut[g[:, 0], g[:, 1], g[:, 2] - k_lo] = np.arange(len(g))
+    offs = np.array([(1, 1, 0), (1, -1, 0), (1, 0, 1), (1, 0, -1), (0, 1, 1), (0, 1, -1)])
+    ends = []
+    lim_lo = np.array([0, 0, k_lo])
+    lim_hi = np.array([2 * nx, 2 * ny, k_hi])
+    for o in offs:
+        q = g + o
+        m = np.all((q >= lim_lo) & (q <= lim_hi), axis=1)
+        ends.append(np.stack([np.nonzero(m)[0], lut[q[m, 0], q[m, 1], q[m, 2] - k_lo]], 1))
+    xyz = g.astype(np.float64) * (0.5 * pitch)
+    if r_max is None:
+        r = np.full(len(g), radius)
+    else:
+        x = g[:, 0].astype(np.float64) / (2 * nx)
+        r = radius + (r_max - radius) * x
+    lat = _finish(xyz, np.concatenate(ends), r, f"octetwin{nx}x{ny}x{nz}[{k_lo}:{k_hi}]")
+    lat.ijk = g.astype(np.int64)
+    lat.gid = (g[:, 0].astype(np.int64) * (2 * ny + 1) + g[:, 1]) * (2 * nz + 1) + g[:, 2]
+    return lat
 
 
 def star(directions, lengths=1.0, radius: float = 0.1, far_radii=None) -> Lattice:
