@@ -69,6 +69,8 @@ struct alignas(16) NodeWS {
   // loop entries of every (arc, side): phi start, span, forward flag
   float eps[2 * MAXA], edp[2 * MAXA];
   uint8_t efw[2 * MAXA];
+  int lcnt[MAXS], lpos[MAXS], lfill[MAXS];
+  int lslot[2 * MAXA];
   LoopRec le[MAXLE];
   int lfirst[MAXS], lcount[MAXS];
   int hoff[MAXH + 1];
@@ -378,22 +380,33 @@ __device__ void process_node(cg::thread_block_tile<G> &g, NodeWS<MAXS, MAXJ, MAX
 
   PHASE_MARK(2);
   // ---- 3. clustering: connected components of "junctions within delta_c" -----------
-  // (label propagation to the lowest junction index; a component is one vertex)
+  // (label = lowest junction index of the component; junction coordinates travel by warp
+  //  shuffles, so the O(nj^2) proximity tests touch no shared memory)
   if (status == 0 && nj > 0) {
     for (int j = lane; j < nj; j += G) ws.jlab[j] = j;
     g.sync();
     for (;;) {
       bool changed = false;
-      for (int j = lane; j < nj; j += G) {
-        float yx = ws.jx[j], yy = ws.jy[j], yz = ws.jz[j];
-        int lj = ws.jlab[j];
-        for (int k = 0; k < nj; k++) {
-          int lk = ws.jlab[k];
-          if (lk < lj && fabsf(yx - ws.jx[k]) <= dc && fabsf(yy - ws.jy[k]) <= dc && fabsf(yz - ws.jz[k]) <= dc) lj = lk;
+      for (int cj = 0; cj < nj; cj += G) {
+        const int j = cj + lane;
+        const bool vj = j < nj;
+        const float yx = vj ? ws.jx[j] : 0.f, yy = vj ? ws.jy[j] : 0.f, yz = vj ? ws.jz[j] : 0.f;
+        int lj = vj ? ws.jlab[j] : 0x7fffffff;
+        for (int ck = 0; ck < nj; ck += G) {
+          const int k = ck + lane;
+          const float kx = k < nj ? ws.jx[k] : 0.f, ky = k < nj ? ws.jy[k] : 0.f, kz = k < nj ? ws.jz[k] : 0.f;
+          const int lk0 = k < nj ? ws.jlab[k] : 0x7fffffff;
+          const int kn = nj - ck < G ? nj - ck : G;
+          for (int t = 0; t < kn; t++) {
+            const float x = g.shfl(kx, t), y = g.shfl(ky, t), z = g.shfl(kz, t);
+            const int lk = g.shfl(lk0, t);
+            if (lk < lj && fabsf(yx - x) <= dc && fabsf(yy - y) <= dc && fabsf(yz - z) <= dc) lj = lk;
+          }
         }
-        if (lj != ws.jlab[j]) { ws.jlab[j] = lj; changed = true; }
+        g.sync();
+        if (vj && lj != ws.jlab[j]) { ws.jlab[j] = lj; changed = true; }
+        g.sync();
       }
-      g.sync();
       if (!g.any(changed)) break;
     }
     // component roots in index order -> vertex ids
@@ -666,24 +679,54 @@ __device__ void process_node(cg::thread_block_tile<G> &g, NodeWS<MAXS, MAXJ, MAX
       }
     }
     g.sync();
-    // 5b: per strut side: gather, order by (phi, arc index), check the chain
+    // 5b: counting sort of the (arc, side) entries by strut side (shared atomics), then each
+    // strut orders its few entries by (phi, arc index) and checks the chain
+    for (int k = lane; k <= d; k += G) { ws.lcnt[k] = 0; ws.lfill[k] = 0; }
+    g.sync();
+    for (int i = lane; i < na; i += G) {
+      uint32_t ids = ws.arcs[i].ids;
+      int lo = ids & 0xff, hi = (ids >> 8) & 0xff;
+      if (lo) atomicAdd(&ws.lcnt[lo], 1);
+      atomicAdd(&ws.lcnt[hi], 1);
+    }
+    g.sync();
+    {
+      int run = 0;
+      for (int k0 = 0; k0 <= d; k0 += G) {
+        int k = k0 + lane;
+        int v = k <= d ? ws.lcnt[k] : 0, tot;
+        int ex = excl_scan<G>(g, v, &tot);
+        if (k <= d) ws.lpos[k] = run + ex;
+        run += tot;
+      }
+    }
+    g.sync();
+    for (int i = lane; i < na; i += G) {
+      uint32_t ids = ws.arcs[i].ids;
+      int lo = ids & 0xff, hi = (ids >> 8) & 0xff;
+      if (lo) ws.lslot[ws.lpos[lo] + atomicAdd(&ws.lfill[lo], 1)] = 2 * i;
+      ws.lslot[ws.lpos[hi] + atomicAdd(&ws.lfill[hi], 1)] = 2 * i + 1;
+    }
+    g.sync();
     for (int k0 = 0; k0 < d; k0 += G) {
       int k = k0 + lane + 1;
       int e = 0, cnt = 0;
       int slot[MAXLOOP];
       if (k <= d) {
-        for (int i = 0; i < na; i++) {
-          uint32_t ids = ws.arcs[i].ids;
-          int lo = ids & 0xff, hi = (ids >> 8) & 0xff;
-          if (lo != k && hi != k) continue;
-          if (cnt >= MAXLOOP) { e = LMM_NODE_ACAP; break; }
-          int sl = 2 * i + (hi == k ? 1 : 0);
-          float ps = ws.eps[sl];
-          int j = cnt;   // arcs arrive in index order: stable insertion by phi
-          while (j > 0 && ps < ws.eps[slot[j - 1]]) { slot[j] = slot[j - 1]; j--; }
-          slot[j] = sl;
-          cnt++;
-        }
+        const int n = ws.lcnt[k], p0 = ws.lpos[k];
+        if (n > MAXLOOP) e = LMM_NODE_ACAP;
+        else
+          for (int t = 0; t < n; t++) {
+            int sl = ws.lslot[p0 + t];
+            float ps = ws.eps[sl];
+            int j = cnt;   // insertion by (phi, arc index)
+            while (j > 0 && (ps < ws.eps[slot[j - 1]] || (ps == ws.eps[slot[j - 1]] && sl < slot[j - 1]))) {
+              slot[j] = slot[j - 1];
+              j--;
+            }
+            slot[j] = sl;
+            cnt++;
+          }
         if (!e && cnt == 0) e = LMM_NODE_EMPTY;
         if (!e) {
           float sum = 0.0f;

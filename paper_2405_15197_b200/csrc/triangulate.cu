@@ -143,10 +143,11 @@ __global__ void k_band_count(TriParams P) {
       float best = 0.0f;
       int idx = 0;
       for (int i = 0; i < LB.y; i++) {
-        float phs = lb[i].phs, dph = lb[i].dph;
-        int N = le_N(lb[i].arc_fwd);
+        const float phs = lb[i].phs;
+        const int N = le_N(lb[i].arc_fwd);
+        const float step = __fdiv_rn(lb[i].dph, (float)N);   // key_at's step, hoisted (same bits)
         for (int j = 0; j < N; j++, idx++) {
-          float r = wrap_rel(key_at(phs, dph, N, j), a0);
+          float r = wrap_rel(__fadd_rn(phs, __fmul_rn((float)j, step)), a0);
           if (idx == 0 || r < best) { best = r; kB = idx; }
         }
       }
@@ -160,16 +161,17 @@ __global__ void k_band_count(TriParams P) {
 struct KeyCursor {
   const LoopRec *le;
   int cnt, e, cum, N;
-  float phs, dph;
+  float phs, step;
   __device__ void load(int ee) {
     e = ee;
     LoopRec L = le[e];
-    cum = L.cum; N = le_N(L.arc_fwd); phs = L.phs; dph = L.dph;
+    cum = L.cum; N = le_N(L.arc_fwd); phs = L.phs;
+    step = __fdiv_rn(L.dph, (float)N);   // key_at's step, hoisted (same bits)
   }
   __device__ float key(int idx) {
     if (idx < cum) load(0);
     while (idx >= cum + N && e + 1 < cnt) load(e + 1);
-    return key_at(phs, dph, N, idx - cum);
+    return __fadd_rn(phs, __fmul_rn((float)(idx - cum), step));
   }
 };
 
