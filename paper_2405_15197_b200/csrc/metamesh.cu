@@ -45,8 +45,9 @@ struct MMParams {
 
 template <int MAXS, int MAXJ, int MAXV, int MAXA, int MAXLE, int MAXH>
 struct alignas(16) NodeWS {
-  // sides: 0 = nodal sphere, 1..d = incident struts in ascending strut id
-  float wx[MAXS], wy[MAXS], wz[MAXS], e[MAXS];
+  // sides: 0 = nodal sphere, 1..d = incident struts in ascending strut id;
+  // w4[k] = (w_k, e_k) of h_k(y) = w_k . y - e_k, one 16-byte load per side test
+  float4 w4[MAXS];
   float ux[MAXS], uy[MAXS], uz[MAXS], s[MAXS], c[MAXS], L[MAXS];
   float asx[MAXS], asy[MAXS], asz[MAXS];
   float e1x[MAXS], e1y[MAXS], e1z[MAXS];
@@ -81,18 +82,24 @@ template <class WS> struct Node {
   WS &w;
   int d;
   float R;
-  __device__ f3 W(int k) const { return F3(w.wx[k], w.wy[k], w.wz[k]); }
+  __device__ f3 W(int k) const { const float4 q = w.w4[k]; return F3(q.x, q.y, q.z); }
+  __device__ float E(int k) const { return w.w4[k].w; }
   __device__ f3 U(int k) const { return F3(w.ux[k], w.uy[k], w.uz[k]); }
   __device__ f3 AS(int k) const { return F3(w.asx[k], w.asy[k], w.asz[k]); }
   __device__ f3 E1(int k) const { return F3(w.e1x[k], w.e1y[k], w.e1z[k]); }
   __device__ f3 E2(int k) const { return F3(w.e2x[k], w.e2y[k], w.e2z[k]); }
   __device__ f3 V(int q) const { return F3(w.vx[q], w.vy[q], w.vz[q]); }
-  __device__ float h(int k, f3 y) const { return k == 0 ? 0.0f : f_dot(W(k), y) - w.e[k]; }
+  __device__ float h(int k, f3 y) const { return k == 0 ? 0.0f : hs(k, y); }
+  // strut side k >= 1: (w.x y.x + w.y y.y) + w.z y.z - e, as f_dot
+  __device__ float hs(int k, f3 y) const {
+    const float4 q = w.w4[k];
+    return ((q.x * y.x + q.y * y.y) + q.z * y.z) - q.w;
+  }
 
   // triple junction (oracle junction32)
   __device__ bool junction(int a, int b, int c, f3 *y, float *tau) const {
     f3 Wa = W(a), Wb = W(b), Wc = W(c);
-    float Ea = w.e[a], Eb = w.e[b], Ec = w.e[c];
+    float Ea = E(a), Eb = E(b), Ec = E(c);
     if (a == 0) { Wa = F3(0.0f, 0.0f, 0.0f); Ea = 0.0f; }
     f3 n1 = f_sub(Wa, Wb), n2 = f_sub(Wa, Wc);
     float q1 = Ea - Eb, q2 = Ea - Ec;
@@ -127,24 +134,33 @@ template <class WS> struct Node {
   __device__ bool valid_strut_pt(uint32_t excl, f3 y, float tau, float delta) const {
     bool ok = !(tau < -delta);
     for (int m = 1; m <= d; m++) {
-      bool viol = h(m, y) - tau > delta;
+      bool viol = hs(m, y) - tau > delta;
       ok = ok && (((excl >> m) & 1u) || !viol);
     }
     return ok;
   }
-  // sphere junction: tolerant (no other strut above the sphere by more than delta)
-  __device__ bool valid_sphere_junction(uint32_t excl, f3 y, float delta) const {
-    bool ok = true;
-    for (int m = 1; m <= d; m++) ok = ok && (((excl >> m) & 1u) || !(h(m, y) > delta));
-    return ok;
+  // both roots of a triple junction in one pass over the sides: strut junctions
+  // (valid_strut_pt) or, for a sphere triple (tau taken as 0; h - 0 == h exactly), the
+  // tolerant sphere-junction test "no other strut above the sphere by more than delta"
+  __device__ void valid_junction_pair(bool sphere, uint32_t excl, f3 y0, float t0, f3 y1, float t1, float delta,
+                                      bool *ok0, bool *ok1) const {
+    bool k0 = *ok0 && (sphere || !(t0 < -delta)), k1 = *ok1 && (sphere || !(t1 < -delta));
+    if (sphere) { t0 = 0.0f; t1 = 0.0f; }
+    for (int m = 1; m <= d; m++) {
+      const float4 q = w.w4[m];
+      const bool ex = (excl >> m) & 1u;
+      const float h0 = ((q.x * y0.x + q.y * y0.y) + q.z * y0.z) - q.w;
+      const float h1 = ((q.x * y1.x + q.y * y1.y) + q.z * y1.z) - q.w;
+      k0 = k0 && (ex || !(h0 - t0 > delta));
+      k1 = k1 && (ex || !(h1 - t1 > delta));
+    }
+    *ok0 = k0; *ok1 = k1;
   }
   // end-circle (cap) point: strictly exposed
   __device__ bool valid_sphere_pt(uint32_t excl, f3 y, float delta) const {
-    for (int m = 1; m <= d; m++) {
-      if (excl & (1u << m)) continue;
-      if (h(m, y) > -delta) return false;
-    }
-    return true;
+    bool ok = true;
+    for (int m = 1; m <= d; m++) ok = ok && (((excl >> m) & 1u) || !(hs(m, y) > -delta));
+    return ok;
   }
 
   // PAPER.md Eq. 7: strut a's ellipse in the auxiliary plane P_{a,b}
@@ -152,7 +168,7 @@ template <class WS> struct Node {
     f3 N = f_sub(W(a), W(b));
     float inl = 1.0f / sqrtf(f_dot(N, N));
     f3 n = f_scl(N, inl);
-    float pc = (w.e[a] - w.e[b]) * inl;
+    float pc = (E(a) - E(b)) * inl;
     f3 p = f_scl(n, pc);
     float s = w.s[a], c = w.c[a];
     f3 u = U(a);
@@ -282,7 +298,7 @@ __device__ void process_node(cg::thread_block_tile<G> &g, NodeWS<MAXS, MAXJ, MAX
 #endif
   // ---- 1. sides -------------------------------------------------------------------
   if (lane == 0) {
-    ws.wx[0] = ws.wy[0] = ws.wz[0] = ws.e[0] = 0.0f;
+    ws.w4[0] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
   }
   int err = 0;
   for (int k0 = 0; k0 < d; k0 += G) {
@@ -304,8 +320,7 @@ __device__ void process_node(cg::thread_block_tile<G> &g, NodeWS<MAXS, MAXJ, MAX
         else {
           float c = sqrtf(1.0f - s * s);
           f3 wv = f_div(u, c);
-          ws.wx[k] = wv.x; ws.wy[k] = wv.y; ws.wz[k] = wv.z;
-          ws.e[k] = (R * s) / c;
+          ws.w4[k] = make_float4(wv.x, wv.y, wv.z, (R * s) / c);
           ws.ux[k] = u.x; ws.uy[k] = u.y; ws.uz[k] = u.z;
           ws.s[k] = s; ws.c[k] = c; ws.L[k] = Ln;
           ws.sign[k] = endbit ? -1 : 1;
@@ -343,16 +358,18 @@ __device__ void process_node(cg::thread_block_tile<G> &g, NodeWS<MAXS, MAXJ, MAX
       if (t < ntri) {
         unrank3(t, ns, &a, &b, &c);
         if (nd.junction(a, b, c, y, tau)) {
-          uint32_t excl = (1u << a) | (1u << b) | (1u << c);
-          for (int r = 0; r < 2; r++) {
-            bool ok = a == 0 ? nd.valid_sphere_junction(excl, y[r], delta) : nd.valid_strut_pt(excl, y[r], tau[r], delta);
-            if (!ok) continue;
-            bool sh = false;
-            int ks[3] = {a, b, c};
-            for (int q = 0; q < 3; q++)
-              if (ks[q] > 0 && tau[r] > 0.45f * (ws.L[ks[q]] * ws.c[ks[q]])) sh = true;
-            if (r == 0) { v0 = true; sh0 = sh; } else { v1 = true; sh1 = sh; }
+          const uint32_t excl = (1u << a) | (1u << b) | (1u << c);
+          v0 = v1 = true;
+          nd.valid_junction_pair(a == 0, excl, y[0], tau[0], y[1], tau[1], delta, &v0, &v1);
+          const int ks[3] = {a, b, c};
+          for (int q = 0; q < 3; q++) {
+            if (ks[q] > 0) {
+              const float lim = 0.45f * (ws.L[ks[q]] * ws.c[ks[q]]);
+              if (tau[0] > lim) sh0 = true;
+              if (tau[1] > lim) sh1 = true;
+            }
           }
+          sh0 = sh0 && v0; sh1 = sh1 && v1;
         }
       }
       unsigned m0 = g.ballot(v0), m1 = g.ballot(v1);

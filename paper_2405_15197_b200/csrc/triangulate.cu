@@ -109,6 +109,30 @@ __device__ __forceinline__ ArcRec load_arc(const ArcRec *p) {
 // ---------------------------------------------------------------------------------
 // count pass
 // ---------------------------------------------------------------------------------
+// Eq. 11 N of every arc of one ring and the running point offsets; returns the ring's
+// point count.  Loads are issued four entries at a time ahead of the dependent stores.
+__device__ __forceinline__ int ring_counts(LoopRec *__restrict__ le, int cnt, const ArcRec *__restrict__ arc, float th0) {
+  int n = 0;
+  for (int i0 = 0; i0 < cnt; i0 += 4) {
+    uint32_t af[4];
+    float dt[4];
+#pragma unroll
+    for (int k = 0; k < 4; k++) af[k] = i0 + k < cnt ? (le[i0 + k].arc_fwd & 0x1ffffu) : 0u;
+#pragma unroll
+    for (int k = 0; k < 4; k++) dt[k] = i0 + k < cnt ? __ldg(&arc[le_arc(af[k])].dt) : 0.0f;
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      if (i0 + k < cnt) {
+        int N = arc_N(dt[k], th0);
+        le[i0 + k].arc_fwd = af[k] | ((uint32_t)N << 17);
+        le[i0 + k].cum = n;
+        n += N;
+      }
+    }
+  }
+  return n;
+}
+
 __global__ void k_band_count(TriParams P) {
   int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (s >= P.S) return;
@@ -123,35 +147,9 @@ __global__ void k_band_count(TriParams P) {
     LoopRec *lb = P.loop + lbase(P.csr_off, e.y) + LB.x;
     const ArcRec *aa = P.arc + abase(P.csr_off, e.x);
     const ArcRec *ab = P.arc + abase(P.csr_off, e.y);
-    for (int i = 0; i < LA.y; i++) {
-      uint32_t af = la[i].arc_fwd & 0x1ffffu;
-      int N = arc_N(aa[le_arc(af)].dt, P.th0);
-      la[i].arc_fwd = af | ((uint32_t)N << 17);
-      la[i].cum = nA;
-      nA += N;
-    }
-    for (int i = 0; i < LB.y; i++) {
-      uint32_t af = lb[i].arc_fwd & 0x1ffffu;
-      int N = arc_N(ab[le_arc(af)].dt, P.th0);
-      lb[i].arc_fwd = af | ((uint32_t)N << 17);
-      lb[i].cum = nB;
-      nB += N;
-    }
-    if (nA > 0 && nB > 0) {
-      // rotation of ring B: first point minimising its angle relative to A's start
-      float a0 = la[0].phs;
-      float best = 0.0f;
-      int idx = 0;
-      for (int i = 0; i < LB.y; i++) {
-        const float phs = lb[i].phs;
-        const int N = le_N(lb[i].arc_fwd);
-        const float step = __fdiv_rn(lb[i].dph, (float)N);   // key_at's step, hoisted (same bits)
-        for (int j = 0; j < N; j++, idx++) {
-          float r = wrap_rel(__fadd_rn(phs, __fmul_rn((float)j, step)), a0);
-          if (idx == 0 || r < best) { best = r; kB = idx; }
-        }
-      }
-    } else { nA = nB = 0; }
+    nA = ring_counts(la, LA.y, aa, P.th0);
+    nB = ring_counts(lb, LB.y, ab, P.th0);
+    if (!(nA > 0 && nB > 0)) nA = nB = 0;   // the band rotation kB is found by k_band_merge
   }
   P.band[s] = make_int4(nA, nB, kB, 0);
   P.band_cnt[s] = (int64_t)nA + nB;
@@ -180,7 +178,7 @@ __global__ void k_band_merge(TriParams P) {
   int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (s >= P.S) return;
   int4 bd = P.band[s];
-  const int nA = bd.x, nB = bd.y, kB = bd.z;
+  const int nA = bd.x, nB = bd.y;
   if (nA + nB == 0) return;
   int2 e = P.ends[s];
   int2 ce = P.strut_csr[s];
@@ -189,6 +187,16 @@ __global__ void k_band_merge(TriParams P) {
   A.le = P.loop + lbase(P.csr_off, e.x) + LA.x; A.cnt = LA.y; A.load(0);
   B.le = P.loop + lbase(P.csr_off, e.y) + LB.x; B.cnt = LB.y; B.load(0);
   const float a0 = A.phs;
+  // rotation of ring B: its first point with the smallest angle relative to A's start
+  int kB = 0;
+  {
+    float best = 0.0f;
+    for (int j = 0; j < nB; j++) {
+      float r = wrap_rel(B.key(j), a0);
+      if (j == 0 || r < best) { best = r; kB = j; }
+    }
+    P.band[s].z = kB;
+  }
   const float b0 = wrap_rel(B.key(kB), a0);
   const int64_t base = P.strut_off[s];
   const int64_t end = base + nA + nB;
@@ -318,16 +326,18 @@ __device__ __forceinline__ void put_rec(unsigned char *dst, f3 a, f3 b, f3 c) {
 }
 
 // Warp-per-band emission.  Warps grid-stride over the strut bands (then the hole fans)
-// that intersect [first, first+count).  Per band the warp caches both rings' loop
-// entries and arc records in shared memory and walks the band in windows of WIN merge
-// steps: the ring points a window touches are computed once, in parallel, into shared
-// memory.  Triangles then go in groups of 64 whose output offset is 16-byte aligned:
-// lane l assembles records 2l and 2l+1 (100 bytes = 25 aligned words), its ring positions
+// that intersect [first, first+count).  Per band the warp caches both rings' loop entries
+// and arc records in shared memory and computes every ring point once, in parallel (the
+// entry of a point comes from a ballot/redux count of the entry starts below it).  Bands
+// whose two rings exceed PMAX points are walked in windows of WIN merge steps instead.
+// Triangles then go in groups of 64 whose output offset is 16-byte aligned: lane l
+// assembles records 2l and 2l+1 (100 bytes = 25 aligned words), its ring positions
 // following from ballot prefix-popcounts of the merge bits; the group leaves the per-warp
-// staging buffer as 16-byte vector stores.  The <= 7 triangles before a band's first
-// aligned position go straight to global memory.  No block-level barriers.
+// staging buffer as 16-byte vector stores.  The next band's header loads are issued while
+// the current band is being emitted.  No block-level barriers.
 constexpr int EW = EMIT_T / 32;   // warps per CTA
-constexpr int WIN = 80;           // merge steps per window
+constexpr int PMAX = 160;         // ring points cached per band (both rings)
+constexpr int WIN = PMAX - 2;     // merge steps per window of a band with more points
 constexpr int GRP = 64;           // triangles per aligned group (3200 B)
 constexpr int MAXRE = 32;         // ring entries per ring (>= MAXLOOP of the meta-mesh)
 constexpr int MAXRA = 12;         // arc records cached per ring
@@ -337,7 +347,8 @@ struct __align__(16) WarpRing {
   int cum[2][MAXRE];
   int nf[2][MAXRE];     // N | fwd << 16
   int ax[2][MAXRE];     // arc index in the node's arc slab
-  float px[2][WIN + 2], py[2][WIN + 2], pz[2][WIN + 2];
+  float stp[2][MAXRE];  // parameter step dt / N
+  float px[PMAX], py[PMAX], pz[PMAX];
   uint4 stage[GRP * REC / 16];
 };
 
@@ -358,16 +369,34 @@ __device__ __forceinline__ ArcRec lds_arc(const ArcRec *p) {
   return a;
 }
 
+// Eq. 12 point idx of ring r, whose loop entry is e; endpoints are the shared vertices
+__device__ __forceinline__ f3 ring_point_e(const WarpRing &w, int r, const RingRef &R, int e, int idx) {
+  const int nf = w.nf[r][e];
+  const int N = nf & 0xffff, fwd = nf >> 16;
+  const int j = idx - w.cum[r][e];
+  const int jj = fwd ? j : N - j;
+  f3 p;
+  if (jj == 0 || jj == N) {
+    const uint32_t ids = e < MAXRA ? w.arc[r][e].ids : __ldg(&R.arcs[w.ax[r][e]].ids);
+    const int v = jj == 0 ? (ids >> 16) & 0xff : (ids >> 24);
+    const float4 q = __ldg(&R.vs[v]);
+    p = F3(q.x, q.y, q.z);
+  } else {
+    const ArcRec A = e < MAXRA ? lds_arc(&w.arc[r][e]) : load_arc(R.arcs + w.ax[r][e]);
+    float t = A.t0 + (float)jj * w.stp[r][e];
+    t = t - LMM_TWO_PI_F * rintf(t * (1.0f / LMM_TWO_PI_F));
+    float sn, cs;
+    __sincosf(t, &sn, &cs);
+    p = F3(fmaf(A.ax, sn, fmaf(A.bx, cs, A.ox)), fmaf(A.ay, sn, fmaf(A.by, cs, A.oy)), fmaf(A.az, sn, fmaf(A.bz, cs, A.oz)));
+  }
+  return F3(R.ox + p.x, R.oy + p.y, R.oz + p.z);
+}
+
+// point idx of ring r, its entry found by a scan of the entry starts (windowed bands, holes)
 __device__ __forceinline__ f3 ring_point(const WarpRing &w, int r, const RingRef &R, int idx) {
   int e = 0;
-#pragma unroll 4
   for (int k = 1; k < R.cnt; k++) e += (w.cum[r][k] <= idx) ? 1 : 0;
-  int nf = w.nf[r][e];
-  int N = nf & 0xffff, fwd = nf >> 16;
-  int j = idx - w.cum[r][e];
-  const ArcRec A = e < MAXRA ? lds_arc(&w.arc[r][e]) : load_arc(R.arcs + w.ax[r][e]);
-  f3 p = arc_point(A, R.vs, N, fwd ? j : N - j);
-  return F3(R.ox + p.x, R.oy + p.y, R.oz + p.z);
+  return ring_point_e(w, r, R, e, idx);
 }
 
 // A-advances of band [base, ...) before triangle t
@@ -404,7 +433,7 @@ __device__ __forceinline__ void put_pair(uint32_t *d, const uint32_t *f, const u
   d[24] = g[11] >> 16;   // high half of g11 | attribute 0
 }
 
-// one record through 2-byte stores (unaligned head triangles)
+// one record through 2-byte stores (unaligned hole triangles)
 __device__ __forceinline__ void put_rec16(unsigned char *dst, const uint32_t *f) {
   uint16_t *d = reinterpret_cast<uint16_t *>(dst);
 #pragma unroll
@@ -423,7 +452,11 @@ __device__ __forceinline__ void flush_group(WarpRing &w, int b0, int b1, unsigne
     const int h = (v0 << 3) - (b0 >> 1);          // head half-words
     if (lane < h) d16[(b0 >> 1) + lane] = s16[(b0 >> 1) + lane];
     uint4 *d = reinterpret_cast<uint4 *>(dst);
-    for (int k = v0 + lane; k < v1; k += 32) d[k] = w.stage[k];
+#pragma unroll
+    for (int i = 0; i < (GRP * REC / 16 + 31) / 32; i++) {
+      const int k = v0 + lane + 32 * i;
+      if (k < v1) d[k] = w.stage[k];
+    }
     const int t0 = v1 << 3, tn = (b1 >> 1) - t0;  // tail half-words
     if (lane < tn) d16[t0 + lane] = s16[t0 + lane];
   } else {                                          // range inside one 16-byte unit
@@ -436,9 +469,11 @@ __device__ __forceinline__ void flush_group(WarpRing &w, int b0, int b1, unsigne
 __device__ __forceinline__ void load_ring(WarpRing &w, int r, const LoopRec *le, int cnt, const ArcRec *arcs, int lane) {
   if (lane < cnt) {
     LoopRec L = le[lane];
+    const int N = le_N(L.arc_fwd), a = le_arc(L.arc_fwd);
     w.cum[r][lane] = L.cum;
-    w.nf[r][lane] = le_N(L.arc_fwd) | (le_fwd(L.arc_fwd) << 16);
-    w.ax[r][lane] = le_arc(L.arc_fwd);
+    w.nf[r][lane] = N | (le_fwd(L.arc_fwd) << 16);
+    w.ax[r][lane] = a;
+    w.stp[r][lane] = __ldg(&arcs[a].dt) / (float)N;
   }
   __syncwarp();
   const int nq = (cnt < MAXRA ? cnt : MAXRA) * 3;
@@ -446,62 +481,110 @@ __device__ __forceinline__ void load_ring(WarpRing &w, int r, const LoopRec *le,
   for (int k = lane; k < nq; k += 32) dst[k] = __ldg(reinterpret_cast<const float4 *>(arcs + w.ax[r][k / 3]) + (k % 3));
 }
 
-__device__ void emit_band(const TriParams &P, WarpRing &w, int s, int64_t first, int64_t last,
-                          unsigned char *out, int lane) {
-  const int64_t base = P.strut_off[s];
-  const int4 bd = P.band[s];
-  const int nA = bd.x, nB = bd.y, kB = bd.z;
+// band header: strut_off / band / ends (level 1), then the loop headers, node centres and
+// CSR offsets of both ends (level 2); the next band's loads are issued during this one
+struct BandHdr {
+  int64_t base;
+  int4 bd;
+  int2 e, ce;
+  int2 LA, LB;
+  float ax, ay, az, bx, by, bz;
+  int offA, offB;
+};
+
+__device__ __forceinline__ void hdr_l1(const TriParams &P, int s, BandHdr &h) {
+  h.base = P.strut_off[s]; h.bd = P.band[s]; h.e = P.ends[s]; h.ce = P.strut_csr[s];
+}
+__device__ __forceinline__ void hdr_l2(const TriParams &P, BandHdr &h) {
+  h.LA = P.loop_hdr[h.ce.x]; h.LB = P.loop_hdr[h.ce.y];
+  const float4 oa = P.node[h.e.x], ob = P.node[h.e.y];
+  h.ax = oa.x; h.ay = oa.y; h.az = oa.z; h.bx = ob.x; h.by = ob.y; h.bz = ob.z;
+  h.offA = P.csr_off[h.e.x]; h.offB = P.csr_off[h.e.y];
+}
+
+template <class Prefetch>
+__device__ void emit_band(const TriParams &P, WarpRing &w, const BandHdr &H, int64_t first, int64_t last,
+                          unsigned char *out, int lane, Prefetch prefetch) {
+  const int64_t base = H.base;
+  const int nA = H.bd.x, nB = H.bd.y, kB = H.bd.z;
   const int64_t ta = base > first ? base : first;
   const int64_t tb = base + nA + nB < last ? base + nA + nB : last;
-  if (ta >= tb) return;
-  const int2 e = P.ends[s];
-  const int2 ce = P.strut_csr[s];
-  const int2 LA = P.loop_hdr[ce.x], LB = P.loop_hdr[ce.y];
-  const float4 oa = P.node[e.x], ob = P.node[e.y];
+  if (ta >= tb) { prefetch(); return; }
   RingRef RA, RB;
-  RA.arcs = P.arc + abase(P.csr_off, e.x); RA.vs = P.vert + vbase(P.csr_off, e.x);
-  RA.ox = oa.x; RA.oy = oa.y; RA.oz = oa.z; RA.cnt = LA.y;
-  RB.arcs = P.arc + abase(P.csr_off, e.y); RB.vs = P.vert + vbase(P.csr_off, e.y);
-  RB.ox = ob.x; RB.oy = ob.y; RB.oz = ob.z; RB.cnt = LB.y;
-  load_ring(w, 0, P.loop + lbase(P.csr_off, e.x) + LA.x, LA.y, RA.arcs, lane);
-  load_ring(w, 1, P.loop + lbase(P.csr_off, e.y) + LB.x, LB.y, RB.arcs, lane);
+  RA.arcs = P.arc + slab_base(H.offA, H.e.x, SLAB_A_K, SLAB_A_K0);
+  RA.vs = P.vert + slab_base(H.offA, H.e.x, SLAB_V_K, SLAB_V_K0);
+  RA.ox = H.ax; RA.oy = H.ay; RA.oz = H.az; RA.cnt = H.LA.y;
+  RB.arcs = P.arc + slab_base(H.offB, H.e.y, SLAB_A_K, SLAB_A_K0);
+  RB.vs = P.vert + slab_base(H.offB, H.e.y, SLAB_V_K, SLAB_V_K0);
+  RB.ox = H.bx; RB.oy = H.by; RB.oz = H.bz; RB.cnt = H.LB.y;
+  load_ring(w, 0, P.loop + slab_base(H.offA, H.e.x, SLAB_L_K, SLAB_L_K0) + H.LA.x, H.LA.y, RA.arcs, lane);
+  load_ring(w, 1, P.loop + slab_base(H.offB, H.e.y, SLAB_L_K, SLAB_L_K0) + H.LB.x, H.LB.y, RB.arcs, lane);
   __syncwarp();
   const int qb = (int)(ta - base), qe = (int)(tb - base);
   const unsigned lt = (1u << lane) - 1u;
-  for (int q0 = qb, q1; q0 < qe; q0 = q1) {
-    q1 = q0 - (int)((base + q0 - first) & 7) + WIN;   // windows end on the 8-triangle grid
-    q1 = q1 < qe ? q1 : qe;
-    int i0 = 0, i1 = 0;
-    if (lane == 0) i0 = merge_rank(P, base, base + q0);
-    if (lane == 1) i1 = (q1 == nA + nB) ? nA : merge_rank(P, base, base + q1);
-    i0 = __shfl_sync(0xffffffffu, i0, 0);
-    i1 = __shfl_sync(0xffffffffu, i1, 1);
-    const int j0 = q0 - i0, j1 = q1 - i1;
-    const int na = i1 - i0 + 1, nb = j1 - j0 + 1;
-    for (int k = lane; k < na + nb; k += 32) {
-      const int r = k < na ? 0 : 1;                     // ring selected without branching
-      const int kk = r ? k - na : k;
-      const int n = r ? nB : nA;
-      int idx = r ? j0 + kk + kB : i0 + kk;
-      idx = idx >= n ? idx - n : idx;
-      idx = idx >= n ? idx - n : idx;
-      RingRef RR;
-      RR.arcs = r ? RB.arcs : RA.arcs; RR.vs = r ? RB.vs : RA.vs; RR.cnt = r ? RB.cnt : RA.cnt;
-      RR.ox = r ? RB.ox : RA.ox; RR.oy = r ? RB.oy : RA.oy; RR.oz = r ? RB.oz : RA.oz;
-      f3 p = ring_point(w, r, RR, idx);
-      w.px[r][kk] = p.x; w.py[r][kk] = p.y; w.pz[r][kk] = p.z;
+  const bool whole = nA + nB <= PMAX;
+  if (whole) {
+    // every point of both rings, natural order: ring A at [0, nA), ring B at [nA, nA + nB).
+    // The entry of combined point k is the number of entry starts <= k (ring A's starts
+    // after its first entry, then ring B's starts shifted by nA).
+    const int cA = (lane >= 1 && lane < RA.cnt) ? w.cum[0][lane] : 0x7fffffff;
+    const int cB = lane < RB.cnt ? nA + w.cum[1][lane] : 0x7fffffff;
+    for (int x = 0; x < nA + nB; x += 32) {
+      const int k = x + lane;
+      const unsigned bits = ((cA >= x && cA < x + 32) ? 1u << (cA - x) : 0u) | ((cB >= x && cB < x + 32) ? 1u << (cB - x) : 0u);
+      const unsigned M = __reduce_or_sync(0xffffffffu, bits);
+      const int ec = __popc(__ballot_sync(0xffffffffu, cA < x)) + __popc(__ballot_sync(0xffffffffu, cB < x)) +
+                     __popc(M & ((2u << lane) - 1u));
+      if (k < nA + nB) {
+        const bool rb = ec >= RA.cnt;
+        f3 p = rb ? ring_point_e(w, 1, RB, ec - RA.cnt, k - nA) : ring_point_e(w, 0, RA, ec, k);
+        w.px[k] = p.x; w.py[k] = p.y; w.pz[k] = p.z;
+      }
     }
+    prefetch();
     __syncwarp();
-    int irun = i0;
-    int qq = q0;
+  }
+  for (int q0 = qb, q1; q0 < qe; q0 = q1) {
+    int i0 = 0, na = 0;
+    if (whole) q1 = qe;
+    else {
+      q1 = q0 - (int)((base + q0 - first) & 7) + WIN;   // windows end on the 8-triangle grid
+      q1 = q1 < qe ? q1 : qe;
+      int i1 = 0;
+      if (lane == 0) i0 = merge_rank(P, base, base + q0);
+      if (lane == 1) i1 = (q1 == nA + nB) ? nA : merge_rank(P, base, base + q1);
+      i0 = __shfl_sync(0xffffffffu, i0, 0);
+      i1 = __shfl_sync(0xffffffffu, i1, 1);
+      const int j0 = q0 - i0, j1 = q1 - i1;
+      na = i1 - i0 + 1;
+      const int nb = j1 - j0 + 1;
+      for (int k = lane; k < na + nb; k += 32) {
+        const int r = k < na ? 0 : 1;
+        const int kk = r ? k - na : k;
+        const int n = r ? nB : nA;
+        int idx = r ? j0 + kk + kB : i0 + kk;
+        idx = idx >= n ? idx - n : idx;
+        idx = idx >= n ? idx - n : idx;
+        f3 p = r ? ring_point(w, 1, RB, idx) : ring_point(w, 0, RA, idx);
+        w.px[k] = p.x; w.py[k] = p.y; w.pz[k] = p.z;
+      }
+      __syncwarp();
+    }
+    // position in the point cache of A_i and B_j (whole: natural order, B rotated by kB)
+    auto posA = [&](int i) { return whole ? (i >= nA ? i - nA : i) : i - i0; };
+    auto posB = [&](int j) {
+      if (!whole) return na + (j - (q0 - i0));
+      int jr = j + kB;
+      jr = jr >= nB ? jr - nB : jr;
+      return nA + jr;
+    };
     // the record of step q is the triangle (A_i, A_i+1, B_j) or (A_i, B_j+1, B_j)
     auto tri = [&](int q, int i, bool advA, uint32_t *f) {
-      const int ia = i - i0, jb = (q - i) - j0;
-      f3 pa = F3(w.px[0][ia], w.py[0][ia], w.pz[0][ia]);
-      f3 pb = F3(w.px[1][jb], w.py[1][jb], w.pz[1][jb]);
-      if (advA) tri_words(pa, F3(w.px[0][ia + 1], w.py[0][ia + 1], w.pz[0][ia + 1]), pb, f);
-      else tri_words(pa, F3(w.px[1][jb + 1], w.py[1][jb + 1], w.pz[1][jb + 1]), pb, f);
+      const int pa = posA(i), pb = posB(q - i);
+      const int pc = advA ? posA(i + 1) : posB(q - i + 1);
+      tri_words(F3(w.px[pa], w.py[pa], w.pz[pa]), F3(w.px[pc], w.py[pc], w.pz[pc]), F3(w.px[pb], w.py[pb], w.pz[pb]), f);
     };
+    int irun = whole ? (q0 == 0 ? 0 : merge_rank(P, base, base + q0)) : i0;
     // groups on the 8-triangle output grid (16-byte aligned records); a band's first group
     // may start mid-grid: its lanes below the start stay idle and the flush begins with a
     // partial 16-byte unit.  Lane l takes steps g+2l and g+2l+1.
@@ -534,6 +617,7 @@ __device__ void emit_band(const TriParams &P, WarpRing &w, int s, int64_t first,
     }
     __syncwarp();
   }
+  if (!whole) prefetch();
 }
 
 __device__ void emit_hole(const TriParams &P, WarpRing &w, int g, int64_t first, int64_t last,
@@ -556,7 +640,9 @@ __device__ void emit_hole(const TriParams &P, WarpRing &w, int g, int64_t first,
   const HoleEnt *he = P.hole_ent + hebase(P.csr_off, n) + H.x;
   if (lane < H.y) {
     HoleEnt E = he[lane];
-    w.cum[0][lane] = E.cum; w.nf[0][lane] = le_N(E.arc_fwd) | (le_fwd(E.arc_fwd) << 16); w.ax[0][lane] = le_arc(E.arc_fwd);
+    const int N = le_N(E.arc_fwd), a = le_arc(E.arc_fwd);
+    w.cum[0][lane] = E.cum; w.nf[0][lane] = N | (le_fwd(E.arc_fwd) << 16); w.ax[0][lane] = a;
+    w.stp[0][lane] = __ldg(&RH.arcs[a].dt) / (float)N;
   }
   __syncwarp();
   {
@@ -571,7 +657,7 @@ __device__ void emit_hole(const TriParams &P, WarpRing &w, int g, int64_t first,
     for (int k = lane; k <= m1 - m0; k += 32) {
       int idx = m0 + k;
       f3 p = ring_point(w, 0, RH, idx >= M ? idx - M : idx);
-      w.px[0][k] = p.x; w.py[0][k] = p.y; w.pz[0][k] = p.z;
+      w.px[k] = p.x; w.py[k] = p.y; w.pz[k] = p.z;
     }
     __syncwarp();
     for (int mm = m0; mm < m1; mm += 32) {
@@ -579,7 +665,7 @@ __device__ void emit_hole(const TriParams &P, WarpRing &w, int g, int64_t first,
       if (m < m1) {
         int k = m - m0;
         uint32_t f[12];
-        tri_words(bp, F3(w.px[0][k], w.py[0][k], w.pz[0][k]), F3(w.px[0][k + 1], w.py[0][k + 1], w.pz[0][k + 1]), f);
+        tri_words(bp, F3(w.px[k], w.py[k], w.pz[k]), F3(w.px[k + 1], w.py[k + 1], w.pz[k + 1]), f);
         put_rec16(out + (hb + m - first) * REC, f);
       }
     }
@@ -596,7 +682,7 @@ __device__ __forceinline__ int64_t upper_bound64(const int64_t *a, int64_t lo, i
 }
 
 // units: bands [s0, s1) then holes [g0, g1) intersecting [first, last)
-__global__ void __launch_bounds__(EMIT_T, 8) k_emit(TriParams P, int64_t first, int64_t count, unsigned char *out,
+__global__ void __launch_bounds__(EMIT_T, 7) k_emit(TriParams P, int64_t first, int64_t count, unsigned char *out,
                                                  int64_t s0, int64_t s1, int64_t g0, int64_t g1) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -604,9 +690,16 @@ __global__ void __launch_bounds__(EMIT_T, 8) k_emit(TriParams P, int64_t first, 
   const int64_t last = first + count;
   const int64_t gw = (int64_t)blockIdx.x * EW + warp, nw = (int64_t)gridDim.x * EW;
   const int64_t nb = s1 - s0, nh = g1 - g0;
+  BandHdr cur;
+  if (gw < nb) { hdr_l1(P, (int)(s0 + gw), cur); hdr_l2(P, cur); }
   for (int64_t u = gw; u < nb + nh; u += nw) {
-    if (u < nb) emit_band(P, w, (int)(s0 + u), first, last, out, lane);
-    else emit_hole(P, w, (int)(g0 + u - nb), first, last, out, lane);
+    if (u < nb) {
+      BandHdr nxt;
+      const bool more = u + nw < nb;
+      if (more) hdr_l1(P, (int)(s0 + u + nw), nxt);
+      emit_band(P, w, cur, first, last, out, lane, [&] { if (more) hdr_l2(P, nxt); });
+      if (more) cur = nxt;
+    } else emit_hole(P, w, (int)(g0 + u - nb), first, last, out, lane);
   }
 }
 
