@@ -19,13 +19,18 @@
 namespace cg = cooperative_groups;
 
 #ifdef LMM_PHASE_TIMING
-__device__ unsigned long long g_phase_cycles[8];
+__device__ unsigned long long g_phase_cycles[16];
 extern "C" LMM_API int lmm_debug_phase_cycles(unsigned long long *out) {
   return cudaMemcpyFromSymbol(out, g_phase_cycles, sizeof(g_phase_cycles)) == cudaSuccess ? 0 : 2;
 }
 #endif
 
 namespace {
+
+// per-bucket capacities <MAXS, MAXJ, MAXV, MAXA, MAXLE, MAXH> (degree 1-8, 9-16, 17-31)
+#define LMM_B0_ARGS 9, 96, 18, 26, 52, 18
+#define LMM_B1_ARGS 17, 160, 34, 50, 100, 34
+#define LMM_B2_ARGS 32, 448, 64, 95, 190, 64
 
 struct MMParams {
   const float4 *node;
@@ -63,10 +68,9 @@ struct alignas(16) NodeWS {
   ArcRec arcs[MAXA];
   float atmid[MAXA];
   int adrop[MAXA];
-  // arc walk: incidences (cluster ids) counting-sorted by side pair
-  int pcnt[MAXS * (MAXS - 1) / 2], pofs[MAXS * (MAXS - 1) / 2], pfill[MAXS * (MAXS - 1) / 2];
+  // arc walk: active side pairs, each with the mask of the clusters holding both sides
+  unsigned long long pmask[MAXS * (MAXS - 1) / 2];
   int plist[MAXS * (MAXS - 1) / 2];
-  int inc[4 * MAXV];
   // loop entries of every (arc, side): phi start, span, forward flag
   float eps[2 * MAXA], edp[2 * MAXA];
   uint8_t efw[2 * MAXA];
@@ -252,20 +256,20 @@ __device__ __forceinline__ void unrank3(int t, int n, int *a, int *b, int *c) {
   *a = A; *b = B; *c = B + 1 + t;
 }
 
+// lexicographic pair t of {0..n-1} (a < b): row a from the quadratic's root, corrected
+// by one step for the rounding of the square root (arguments < 2^12: exact enough)
 __device__ __forceinline__ void unrank2(int t, int n, int *a, int *b) {
-  int A = 0;
-  for (;;) {
-    int cnt = n - 1 - A;
-    if (t < cnt) break;
-    t -= cnt;
-    A++;
-  }
-  *a = A; *b = A + 1 + t;
+  const float m = (float)(2 * n - 1);
+  int A = (int)floorf(0.5f * (m - sqrtf(m * m - 8.0f * (float)t)));
+  A = A < 0 ? 0 : (A > n - 2 ? n - 2 : A);
+  if ((A + 1) * (2 * n - A - 2) / 2 <= t) A++;
+  else if (A * (2 * n - A - 1) / 2 > t) A--;
+  *a = A;
+  *b = t - A * (2 * n - A - 1) / 2 + A + 1;
 }
 
 #define MAXQ 16
 #define MAXLOOP 32
-#define MAXINC (4 * MAXV)
 
 __device__ __forceinline__ int rank2(int a, int b, int n) {
   // lexicographic index of pair (a < b) among the pairs of {0..n-1}
@@ -454,130 +458,139 @@ __device__ void process_node(cg::thread_block_tile<G> &g, NodeWS<MAXS, MAXJ, MAX
 
   PHASE_MARK(3);
   // ---- 4. arcs: conics walked through their vertices, incidence-driven --------------
-  // Clusters enumerate the side pairs of their tie sets (counting sort by pair), the
-  // pairs with vertices -- plus pairs of sides that appear in no vertex (only these can
-  // carry a closed arc) -- are compacted in lexicographic order and walked densely.
+  // Each side pair collects the clusters whose tie set holds both sides (a bit mask);
+  // the pairs with vertices -- plus pairs of sides that appear in no vertex (only these
+  // can carry a closed arc) -- are compacted in lexicographic order and walked densely.
   if (status == 0 && d > 0) {
     const int npair = ns * (ns - 1) / 2;
     uint32_t um = 0;
     for (int q = lane; q < nc; q += G) um |= ws.vmask[q];
     um = cg::reduce(g, um, cg::bit_or<uint32_t>());
-    for (int p = lane; p < npair; p += G) { ws.pcnt[p] = 0; ws.pfill[p] = 0; }
-    g.sync();
-    for (int q = lane; q < nc; q += G) {
-      uint32_t m = ws.vmask[q];
-      for (uint32_t ma = m; ma; ma &= ma - 1) {
-        int a = __ffs(ma) - 1;
-        for (uint32_t mb = ma & (ma - 1); mb; mb &= mb - 1) {
-          int b = __ffs(mb) - 1;
-          atomicAdd(&ws.pcnt[rank2(a, b, ns)], 1);
-        }
-      }
-    }
-    g.sync();
-    int ninc = 0;
-    for (int base = 0; base < npair; base += G) {
-      int p = base + lane;
-      int v = p < npair ? ws.pcnt[p] : 0;
-      int tot;
-      int ex = excl_scan<G>(g, v, &tot);
-      if (p < npair) ws.pofs[p] = ninc + ex;
-      ninc += tot;
-    }
-    if (ninc > MAXINC) status = LMM_NODE_QCAP;
-    g.sync();
-    if (status == 0) {
-      for (int q = lane; q < nc; q += G) {
-        uint32_t m = ws.vmask[q];
-        for (uint32_t ma = m; ma; ma &= ma - 1) {
-          int a = __ffs(ma) - 1;
-          for (uint32_t mb = ma & (ma - 1); mb; mb &= mb - 1) {
-            int b = __ffs(mb) - 1;
-            int pr = rank2(a, b, ns);
-            ws.inc[ws.pofs[pr] + atomicAdd(&ws.pfill[pr], 1)] = q;
-          }
-        }
-      }
-      // active pairs, lexicographic order
-      int nact = 0;
+    // one lane per side pair: the clusters whose tie set holds both sides (nc <= MAXV <= 64)
+    int nact = 0;
+    {
       for (int base = 0; base < npair; base += G) {
-        int p = base + lane;
+        const int p = base + lane;
         bool act = false;
+        unsigned long long cm = 0ull;
         if (p < npair) {
-          if (ws.pcnt[p] > 0) act = true;
-          else {
-            int a, b;
-            unrank2(p, ns, &a, &b);
-            uint32_t strut_bits = a == 0 ? (1u << b) : ((1u << a) | (1u << b));
-            act = (um & strut_bits) == 0;
-          }
+          int a, b;
+          unrank2(p, ns, &a, &b);
+          const uint32_t pb = (1u << a) | (1u << b);
+          for (int q = 0; q < nc; q++) cm |= (unsigned long long)((ws.vmask[q] & pb) == pb) << q;
+          const uint32_t strut_bits = a == 0 ? (1u << b) : pb;
+          act = cm != 0ull || (um & strut_bits) == 0;
         }
-        unsigned am = g.ballot(act);
-        if (act) ws.plist[nact + __popc(am & ((1u << lane) - 1u))] = p;
+        const unsigned am = g.ballot(act);
+        if (act) {
+          const int k = nact + __popc(am & ((1u << lane) - 1u));
+          ws.plist[k] = p;
+          ws.pmask[k] = cm;
+        }
         nact += __popc(am);
       }
       g.sync();
+      PHASE_MARK(9);
+      constexpr int QL = MAXJ / G;
+      float *qx = ws.jx, *qy = ws.jy, *qz = ws.jz;
+      int *qt = ws.jlab;        // tangent length at the midpoint, float bits
+      uint32_t *qm = ws.jabc;   // side mask | sphere-point flag << 31
+      int *qok = ws.jcid;
       for (int base = 0; base < nact; base += G) {
         int k = base + lane;
-        int e = 0, cnt = 0, closed = 0;
+        int e = 0, cnt = 0, closed = 0, nint = 0;
         int a = 0, b = 0;
         f3 o = F3(0.f, 0.f, 0.f), av = o, bv = o;
         int vsv[MAXQ], vev[MAXQ];
         float t0v[MAXQ], dtv[MAXQ], tmv[MAXQ];
+        bool okv[MAXQ];
+        int p = 0, nq = 0;
+        unsigned long long cmk = 0ull;
+        bool conic_ok = true;
         if (k < nact) {
-          const int p = ws.plist[k];
+          p = ws.plist[k];
           unrank2(p, ns, &a, &b);
-          uint32_t pm = (1u << a) | (1u << b);
-          const int nq = ws.pcnt[p];
-          bool conic_ok = true;
+          cmk = ws.pmask[k];
+          nq = __popcll(cmk);
           if (a == 0) nd.circle(b, &o, &av, &bv);
           else conic_ok = nd.ellipse(a, b, &o, &av, &bv);
           if (!conic_ok) {
             if (nq > 0) e = LMM_NODE_CONIC;
           } else if (nq > MAXQ) {
             e = LMM_NODE_QCAP;
-          } else {
-            int Q[MAXQ];
-            float tq[MAXQ], us[MAXQ], uc[MAXQ];
-            for (int i = 0; i < nq; i++) {
-              int q = ws.inc[ws.pofs[p] + i];
-              float su, sc;
-              float t = conic_t(o, av, bv, nd.V(q), &su, &sc);
-              int j = i;   // insertion by (t, cluster index): order-independent
-              while (j > 0 && (t < tq[j - 1] || (t == tq[j - 1] && q < Q[j - 1]))) {
-                Q[j] = Q[j - 1]; tq[j] = tq[j - 1]; us[j] = us[j - 1]; uc[j] = uc[j - 1];
-                j--;
-              }
-              Q[j] = q; tq[j] = t; us[j] = su; uc[j] = sc;
+          } else nint = nq == 0 ? 1 : nq;
+        }
+        int qtot;
+        const int qbase = excl_scan<G>(g, nint < QL ? nint : QL, &qtot);
+        if (nint > 0) {
+          const uint32_t pm = (1u << a) | (1u << b);
+          int Q[MAXQ];
+          float tq[MAXQ], us[MAXQ], uc[MAXQ];
+          unsigned long long cmr = cmk;
+          for (int i = 0; i < nq; i++, cmr &= cmr - 1) {
+            const int q = __ffsll((long long)cmr) - 1;
+            float su, sc;
+            float t = conic_t(o, av, bv, nd.V(q), &su, &sc);
+            int j = i;   // insertion by (t, cluster index): order-independent
+            while (j > 0 && (t < tq[j - 1] || (t == tq[j - 1] && q < Q[j - 1]))) {
+              Q[j] = Q[j - 1]; tq[j] = tq[j - 1]; us[j] = us[j - 1]; uc[j] = uc[j - 1];
+              j--;
             }
-            int nint = nq == 0 ? 1 : nq;
-            for (int i = 0; i < nint; i++) {
-              float ms, mc, t0, dt;
-              int vs, ve;
-              if (nq == 0) { ms = 0.0f; mc = 1.0f; t0 = 0.0f; dt = LMM_TWO_PI_F; vs = ve = -1; }
-              else if (nq == 1) { ms = -us[0]; mc = -uc[0]; t0 = tq[0]; dt = LMM_TWO_PI_F; vs = ve = Q[0]; }
-              else {
-                int j = (i + 1) % nq;
-                dt = j == 0 ? (tq[0] + LMM_TWO_PI_F) - tq[nq - 1] : tq[j] - tq[i];
-                if (!(dt > 0.0f)) { e = LMM_NODE_CHAIN; break; }
-                float sx = us[i] + us[j], sc = uc[i] + uc[j];
-                float l2 = sx * sx + sc * sc;
-                if (l2 > 1e-6f) {
-                  float l = sqrtf(l2);
-                  ms = sx / l; mc = sc / l;
-                  if (dt > LMM_PI_F) { ms = -ms; mc = -mc; }
-                } else { ms = uc[i]; mc = -us[i]; }
-                t0 = tq[i]; vs = Q[i]; ve = Q[j];
-              }
-              f3 y = F3((o.x + av.x * ms) + bv.x * mc, (o.y + av.y * ms) + bv.y * mc, (o.z + av.z * ms) + bv.z * mc);
-              float tmid = a == 0 ? 0.0f : nd.h(a, y);
-              bool ok = a == 0 ? nd.valid_sphere_pt(pm, y, delta) : nd.valid_strut_pt(pm, y, tmid, delta);
-              if (!ok) continue;
-              vsv[cnt] = vs; vev[cnt] = ve; t0v[cnt] = t0; dtv[cnt] = dt; tmv[cnt] = tmid;
-              if (vs < 0) closed = 1;
-              cnt++;
+            Q[j] = q; tq[j] = t; us[j] = su; uc[j] = sc;
+          }
+          for (int i = 0; i < nint; i++) {
+            float ms, mc, t0, dt;
+            int vs, ve;
+            if (nq == 0) { ms = 0.0f; mc = 1.0f; t0 = 0.0f; dt = LMM_TWO_PI_F; vs = ve = -1; }
+            else if (nq == 1) { ms = -us[0]; mc = -uc[0]; t0 = tq[0]; dt = LMM_TWO_PI_F; vs = ve = Q[0]; }
+            else {
+              int j = (i + 1) % nq;
+              dt = j == 0 ? (tq[0] + LMM_TWO_PI_F) - tq[nq - 1] : tq[j] - tq[i];
+              if (!(dt > 0.0f)) { e = LMM_NODE_CHAIN; break; }
+              float sx = us[i] + us[j], sc = uc[i] + uc[j];
+              float l2 = sx * sx + sc * sc;
+              if (l2 > 1e-6f) {
+                float l = sqrtf(l2);
+                ms = sx / l; mc = sc / l;
+                if (dt > LMM_PI_F) { ms = -ms; mc = -mc; }
+              } else { ms = uc[i]; mc = -us[i]; }
+              t0 = tq[i]; vs = Q[i]; ve = Q[j];
+            }
+            f3 y = F3((o.x + av.x * ms) + bv.x * mc, (o.y + av.y * ms) + bv.y * mc, (o.z + av.z * ms) + bv.z * mc);
+            float tmid = a == 0 ? 0.0f : nd.h(a, y);
+            vsv[i] = vs; vev[i] = ve; t0v[i] = t0; dtv[i] = dt; tmv[i] = tmid;
+            if (i < QL) {
+              const int qi = qbase + i;
+              qx[qi] = y.x; qy[qi] = y.y; qz[qi] = y.z; qt[qi] = __float_as_int(tmid);
+              qm[qi] = pm | (a == 0 ? 0x80000000u : 0u);
+            } else {
+              okv[i] = a == 0 ? nd.valid_sphere_pt(pm, y, delta) : nd.valid_strut_pt(pm, y, tmid, delta);
             }
           }
+        }
+        g.sync();
+        PHASE_MARK(10);
+        // (2) queued midpoints: end-circle points strictly exposed (h_m - 0 > -delta
+        // rejects, as valid_sphere_pt), strut points within the tolerance (valid_strut_pt)
+        for (int qi = lane; qi < qtot; qi += G) {
+          const uint32_t m = qm[qi];
+          const bool sph = m >> 31;
+          const f3 y = F3(qx[qi], qy[qi], qz[qi]);
+          const float tau = __int_as_float(qt[qi]);
+          const float thr = sph ? -delta : delta;
+          bool ok = sph || !(tau < -delta);
+          for (int mm = 1; mm <= d; mm++) ok = ok && (((m >> mm) & 1u) || !(nd.hs(mm, y) - tau > thr));
+          qok[qi] = ok;
+        }
+        g.sync();
+        PHASE_MARK(11);
+        // (3) valid intervals become arcs
+        for (int i = 0; i < nint && !e; i++) {
+          const bool ok = i < QL ? qok[qbase + i] != 0 : okv[i];
+          if (!ok) continue;
+          vsv[cnt] = vsv[i]; vev[cnt] = vev[i]; t0v[cnt] = t0v[i]; dtv[cnt] = dtv[i]; tmv[cnt] = tmv[i];
+          if (vsv[cnt] < 0) closed = 1;
+          cnt++;
         }
         int tot, ctot;
         int pos = na + excl_scan<G>(g, e ? 0 : cnt, &tot);
@@ -603,6 +616,7 @@ __device__ void process_node(cg::thread_block_tile<G> &g, NodeWS<MAXS, MAXJ, MAX
         }
         na += tot;
         nv += ctot;
+        PHASE_MARK(12);
       }
     }
   }
@@ -903,6 +917,16 @@ int launch_bucket(lmm_ctx *c, MMParams P) {
 
 }  // namespace
 
+#ifdef LMM_PHASE_TIMING
+extern "C" LMM_API int lmm_debug_ws_bytes(int bucket) {
+  switch (bucket) {
+    case 0: return (int)sizeof(NodeWS<LMM_B0_ARGS>);
+    case 1: return (int)sizeof(NodeWS<LMM_B1_ARGS>);
+    default: return (int)sizeof(NodeWS<LMM_B2_ARGS>);
+  }
+}
+#endif
+
 int metamesh_run(lmm_ctx *c) {
   MMParams P;
   P.node = (const float4 *)c->node.p;
@@ -928,13 +952,13 @@ int metamesh_run(lmm_ctx *c) {
     // bucket b occupies bucket_nodes[bucket_off[b] .. bucket_off[b+1])
     P.node_list = bn + c->bucket_off[0];
     P.n_list = (int)(c->bucket_off[1] - c->bucket_off[0]);
-    if ((rc = launch_bucket<32, 9, 96, 18, 26, 52, 18>(c, P))) return rc;
+    if ((rc = launch_bucket<32, LMM_B0_ARGS>(c, P))) return rc;
     P.node_list = bn + c->bucket_off[1];
     P.n_list = (int)(c->bucket_off[2] - c->bucket_off[1]);
-    if ((rc = launch_bucket<32, 17, 192, 34, 50, 100, 34>(c, P))) return rc;
+    if ((rc = launch_bucket<32, LMM_B1_ARGS>(c, P))) return rc;
     P.node_list = bn + c->bucket_off[2];
     P.n_list = (int)(c->bucket_off[3] - c->bucket_off[2]);
-    if ((rc = launch_bucket<32, 32, 448, 64, 95, 190, 64>(c, P))) return rc;
+    if ((rc = launch_bucket<32, LMM_B2_ARGS>(c, P))) return rc;
   }
   return LMM_OK;
 }

@@ -16,10 +16,12 @@ h = B.lmm_create(0, torch.cuda.current_stream().cuda_stream)
 B.lmm_load_lattice(h, xyz, ends, rend)
 B.lmm_build_metamesh(h)
 torch.cuda.synchronize()
-out = (C.c_ulonglong * 8)()
+out = (C.c_ulonglong * 16)()
 lib.lmm_debug_phase_cycles(out)
-names = ["sides", "junctions", "clustering", "arcs", "drop+unref", "loops", "holes", "write"]
+names = ["sides", "junctions", "clustering", "arcs(rest)", "drop+unref", "loops", "holes", "write",
+         "arcs:pairs", "arcs:conic+int", "arcs:validity", "arcs:assemble", "p13", "p14", "p15", "p16"]
 tot = sum(out)
 print(cfg, lat.n_nodes, "nodes; cycles per node (lane-0 warps):", tot / lat.n_nodes)
 for k, v in zip(names, out):
+    if not v: continue
     print(f"  {k:12s} {100 * v / tot:5.1f}%  {v / lat.n_nodes:9.0f} cyc/node")
