@@ -137,6 +137,7 @@ template <class WS> struct Node {
   // branch-free over the sides (same boolean as the early-exit form)
   __device__ bool valid_strut_pt(uint32_t excl, f3 y, float tau, float delta) const {
     bool ok = !(tau < -delta);
+#pragma unroll 1
     for (int m = 1; m <= d; m++) {
       bool viol = hs(m, y) - tau > delta;
       ok = ok && (((excl >> m) & 1u) || !viol);
@@ -163,6 +164,7 @@ template <class WS> struct Node {
   // end-circle (cap) point: strictly exposed
   __device__ bool valid_sphere_pt(uint32_t excl, f3 y, float delta) const {
     bool ok = true;
+#pragma unroll 1
     for (int m = 1; m <= d; m++) ok = ok && (((excl >> m) & 1u) || !(hs(m, y) > -delta));
     return ok;
   }
@@ -305,6 +307,7 @@ __device__ void process_node(cg::thread_block_tile<G> &g, NodeWS<MAXS, MAXJ, MAX
     ws.w4[0] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
   }
   int err = 0;
+  #pragma unroll 1
   for (int k0 = 0; k0 < d; k0 += G) {
     int idx = k0 + lane;
     if (idx < d) {
@@ -352,6 +355,7 @@ __device__ void process_node(cg::thread_block_tile<G> &g, NodeWS<MAXS, MAXJ, MAX
   // ---- 2. triple junctions, lexicographic (a<b<c), root-minor ---------------------
   if (status == 0 && d > 0) {
     const int ntri = ns * (ns - 1) * (ns - 2) / 6;
+    #pragma unroll 1
     for (int base = 0; base < ntri; base += G) {
       int t = base + lane;
       bool v0 = false, v1 = false;
@@ -404,15 +408,18 @@ __device__ void process_node(cg::thread_block_tile<G> &g, NodeWS<MAXS, MAXJ, MAX
   // (label = lowest junction index of the component; junction coordinates travel by warp
   //  shuffles, so the O(nj^2) proximity tests touch no shared memory)
   if (status == 0 && nj > 0) {
+    #pragma unroll 1
     for (int j = lane; j < nj; j += G) ws.jlab[j] = j;
     g.sync();
     for (;;) {
       bool changed = false;
+      #pragma unroll 1
       for (int cj = 0; cj < nj; cj += G) {
         const int j = cj + lane;
         const bool vj = j < nj;
         const float yx = vj ? ws.jx[j] : 0.f, yy = vj ? ws.jy[j] : 0.f, yz = vj ? ws.jz[j] : 0.f;
         int lj = vj ? ws.jlab[j] : 0x7fffffff;
+        #pragma unroll 1
         for (int ck = 0; ck < nj; ck += G) {
           const int k = ck + lane;
           const float kx = k < nj ? ws.jx[k] : 0.f, ky = k < nj ? ws.jy[k] : 0.f, kz = k < nj ? ws.jz[k] : 0.f;
@@ -431,6 +438,7 @@ __device__ void process_node(cg::thread_block_tile<G> &g, NodeWS<MAXS, MAXJ, MAX
       if (!g.any(changed)) break;
     }
     // component roots in index order -> vertex ids
+    #pragma unroll 1
     for (int base = 0; base < nj; base += G) {
       int j = base + lane;
       bool root = j < nj && ws.jlab[j] == j;
@@ -445,6 +453,7 @@ __device__ void process_node(cg::thread_block_tile<G> &g, NodeWS<MAXS, MAXJ, MAX
     if (nc > MAXV) status = LMM_NODE_CCAP;
     g.sync();
     if (status == 0) {
+      #pragma unroll 1
       for (int j = lane; j < nj; j += G) {
         uint32_t code = ws.jabc[j];
         uint32_t bits = (1u << (code & 0xff)) | (1u << ((code >> 8) & 0xff)) | (1u << ((code >> 16) & 0xff));
@@ -464,11 +473,13 @@ __device__ void process_node(cg::thread_block_tile<G> &g, NodeWS<MAXS, MAXJ, MAX
   if (status == 0 && d > 0) {
     const int npair = ns * (ns - 1) / 2;
     uint32_t um = 0;
+    #pragma unroll 1
     for (int q = lane; q < nc; q += G) um |= ws.vmask[q];
     um = cg::reduce(g, um, cg::bit_or<uint32_t>());
     // one lane per side pair: the clusters whose tie set holds both sides (nc <= MAXV <= 64)
     int nact = 0;
     {
+      #pragma unroll 1
       for (int base = 0; base < npair; base += G) {
         const int p = base + lane;
         bool act = false;
@@ -496,6 +507,7 @@ __device__ void process_node(cg::thread_block_tile<G> &g, NodeWS<MAXS, MAXJ, MAX
       int *qt = ws.jlab;        // tangent length at the midpoint, float bits
       uint32_t *qm = ws.jabc;   // side mask | sphere-point flag << 31
       int *qok = ws.jcid;
+      #pragma unroll 1
       for (int base = 0; base < nact; base += G) {
         int k = base + lane;
         int e = 0, cnt = 0, closed = 0, nint = 0;
@@ -626,6 +638,7 @@ __device__ void process_node(cg::thread_block_tile<G> &g, NodeWS<MAXS, MAXJ, MAX
   // ambiguous strut-strut arcs running under a strictly exposed hole lune are dropped
   // (R10): midpoint tangent length < delta and both end circles join its ends
   if (status == 0 && na > 0) {
+    #pragma unroll 1
     for (int i = lane; i < na; i += G) {
       uint32_t ids = ws.arcs[i].ids;
       int lo = ids & 0xff, hi = (ids >> 8) & 0xff, vs = (ids >> 16) & 0xff, ve = ids >> 24;
@@ -646,6 +659,7 @@ __device__ void process_node(cg::thread_block_tile<G> &g, NodeWS<MAXS, MAXJ, MAX
     }
     g.sync();
     int w = 0;
+    #pragma unroll 1
     for (int base = 0; base < na; base += G) {
       int i = base + lane;
       bool keep = i < na && !ws.adrop[i];
@@ -664,6 +678,7 @@ __device__ void process_node(cg::thread_block_tile<G> &g, NodeWS<MAXS, MAXJ, MAX
   // every junction vertex must carry an arc
   if (status == 0) {
     int e = 0;
+    #pragma unroll 1
     for (int q0 = 0; q0 < nc; q0 += G) {
       int q = q0 + lane;
       if (q < nc) {
@@ -682,6 +697,7 @@ __device__ void process_node(cg::thread_block_tile<G> &g, NodeWS<MAXS, MAXJ, MAX
   // ---- 5. arc loops per strut end (ordered by angle around the strut axis) -----------
   if (status == 0 && d > 0) {
     // 5a: loop-entry data of every (arc, strut side), lanes over arcs
+    #pragma unroll 1
     for (int i = lane; i < na; i += G) {
       const ArcRec &A = ws.arcs[i];
       const int lo = A.ids & 0xff, hi = (A.ids >> 8) & 0xff;
@@ -712,8 +728,10 @@ __device__ void process_node(cg::thread_block_tile<G> &g, NodeWS<MAXS, MAXJ, MAX
     g.sync();
     // 5b: counting sort of the (arc, side) entries by strut side (shared atomics), then each
     // strut orders its few entries by (phi, arc index) and checks the chain
+    #pragma unroll 1
     for (int k = lane; k <= d; k += G) { ws.lcnt[k] = 0; ws.lfill[k] = 0; }
     g.sync();
+    #pragma unroll 1
     for (int i = lane; i < na; i += G) {
       uint32_t ids = ws.arcs[i].ids;
       int lo = ids & 0xff, hi = (ids >> 8) & 0xff;
@@ -723,6 +741,7 @@ __device__ void process_node(cg::thread_block_tile<G> &g, NodeWS<MAXS, MAXJ, MAX
     g.sync();
     {
       int run = 0;
+      #pragma unroll 1
       for (int k0 = 0; k0 <= d; k0 += G) {
         int k = k0 + lane;
         int v = k <= d ? ws.lcnt[k] : 0, tot;
@@ -732,6 +751,7 @@ __device__ void process_node(cg::thread_block_tile<G> &g, NodeWS<MAXS, MAXJ, MAX
       }
     }
     g.sync();
+    #pragma unroll 1
     for (int i = lane; i < na; i += G) {
       uint32_t ids = ws.arcs[i].ids;
       int lo = ids & 0xff, hi = (ids >> 8) & 0xff;
@@ -739,6 +759,7 @@ __device__ void process_node(cg::thread_block_tile<G> &g, NodeWS<MAXS, MAXJ, MAX
       ws.lslot[ws.lpos[hi] + atomicAdd(&ws.lfill[hi], 1)] = 2 * i + 1;
     }
     g.sync();
+    #pragma unroll 1
     for (int k0 = 0; k0 < d; k0 += G) {
       int k = k0 + lane + 1;
       int e = 0, cnt = 0;
@@ -854,16 +875,22 @@ __device__ void process_node(cg::thread_block_tile<G> &g, NodeWS<MAXS, MAXJ, MAX
   const int64_t lb = slab_base(off, n, SLAB_L_K, SLAB_L_K0);
   const int64_t hb = slab_base(off, n, SLAB_H_K, SLAB_H_K0);
   const int64_t heb = slab_base(off, n, SLAB_HE_K, SLAB_HE_K0);
+  #pragma unroll 1
   for (int q = lane; q < nv; q += G) P.vert[vb + q] = make_float4(ws.vx[q], ws.vy[q], ws.vz[q], __uint_as_float(ws.vmask[q]));
   {
     const uint32_t *src = reinterpret_cast<const uint32_t *>(ws.arcs);
     uint32_t *dst = reinterpret_cast<uint32_t *>(P.arc + ab);
+    #pragma unroll 1
     for (int q = lane; q < na * 12; q += G) dst[q] = src[q];
   }
+  #pragma unroll 1
   for (int q = lane; q < nle; q += G) P.loop[lb + q] = ws.le[q];
+  #pragma unroll 1
   for (int k = lane; k < d; k += G)
     P.loop_hdr[off + k] = status == 0 ? make_int2(ws.lfirst[k + 1], ws.lcount[k + 1]) : make_int2(0, 0);
+  #pragma unroll 1
   for (int h = lane; h < nh; h += G) P.hole_hdr[hb + h] = make_int2(ws.hoff[h], ws.hoff[h + 1] - ws.hoff[h]);
+  #pragma unroll 1
   for (int q = lane; q < nhe; q += G) { HoleEnt he; he.arc_fwd = ws.he[q]; he.cum = 0; P.hole_ent[heb + q] = he; }
   PHASE_MARK(8);
   g.sync();
