@@ -473,7 +473,7 @@ __device__ __forceinline__ void load_ring(WarpRing &w, int r, const LoopRec *le,
     w.cum[r][lane] = L.cum;
     w.nf[r][lane] = N | (le_fwd(L.arc_fwd) << 16);
     w.ax[r][lane] = a;
-    w.stp[r][lane] = __ldg(&arcs[a].dt) / (float)N;
+    w.stp[r][lane] = __fdividef(__ldg(&arcs[a].dt), (float)N);
   }
   __syncwarp();
   const int nq = (cnt < MAXRA ? cnt : MAXRA) * 3;
@@ -481,52 +481,74 @@ __device__ __forceinline__ void load_ring(WarpRing &w, int r, const LoopRec *le,
   for (int k = lane; k < nq; k += 32) dst[k] = __ldg(reinterpret_cast<const float4 *>(arcs + w.ax[r][k / 3]) + (k % 3));
 }
 
-// band header: strut_off / band / ends (level 1), then the loop headers, node centres and
-// CSR offsets of both ends (level 2); the next band's loads are issued during this one
-struct BandHdr {
-  int64_t base;
+// band header: band / strut_off / ends / strut_csr (level 1), then the loop headers, node
+// centres and CSR offsets of both ends (level 2).  The next band's header is fetched
+// with cp.async straight into shared memory while the current band is emitted, so no
+// registers are held across the band.
+struct __align__(16) BandHdr {
   int4 bd;
+  float4 oa, ob;
+  long long base;
   int2 e, ce;
   int2 LA, LB;
-  float ax, ay, az, bx, by, bz;
   int offA, offB;
 };
 
-__device__ __forceinline__ void hdr_l1(const TriParams &P, int s, BandHdr &h) {
-  h.base = P.strut_off[s]; h.bd = P.band[s]; h.e = P.ends[s]; h.ce = P.strut_csr[s];
+template <int BYTES>
+__device__ __forceinline__ void cp_async(void *sdst, const void *gsrc) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(sa), "l"(gsrc), "n"(BYTES) : "memory");
 }
-__device__ __forceinline__ void hdr_l2(const TriParams &P, BandHdr &h) {
-  h.LA = P.loop_hdr[h.ce.x]; h.LB = P.loop_hdr[h.ce.y];
-  const float4 oa = P.node[h.e.x], ob = P.node[h.e.y];
-  h.ax = oa.x; h.ay = oa.y; h.az = oa.z; h.bx = ob.x; h.by = ob.y; h.bz = ob.z;
-  h.offA = P.csr_off[h.e.x]; h.offB = P.csr_off[h.e.y];
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
 }
 
-template <class Prefetch>
-__device__ void emit_band(const TriParams &P, WarpRing &w, const BandHdr &H, int64_t first, int64_t last,
-                          unsigned char *out, int lane, Prefetch prefetch) {
-  const int64_t base = H.base;
-  const int nA = H.bd.x, nB = H.bd.y, kB = H.bd.z;
-  const int64_t ta = base > first ? base : first;
-  const int64_t tb = base + nA + nB < last ? base + nA + nB : last;
-  if (ta >= tb) { prefetch(); return; }
-  RingRef RA, RB;
-  RA.arcs = P.arc + slab_base(H.offA, H.e.x, SLAB_A_K, SLAB_A_K0);
-  RA.vs = P.vert + slab_base(H.offA, H.e.x, SLAB_V_K, SLAB_V_K0);
-  RA.ox = H.ax; RA.oy = H.ay; RA.oz = H.az; RA.cnt = H.LA.y;
-  RB.arcs = P.arc + slab_base(H.offB, H.e.y, SLAB_A_K, SLAB_A_K0);
-  RB.vs = P.vert + slab_base(H.offB, H.e.y, SLAB_V_K, SLAB_V_K0);
-  RB.ox = H.bx; RB.oy = H.by; RB.oz = H.bz; RB.cnt = H.LB.y;
-  load_ring(w, 0, P.loop + slab_base(H.offA, H.e.x, SLAB_L_K, SLAB_L_K0) + H.LA.x, H.LA.y, RA.arcs, lane);
-  load_ring(w, 1, P.loop + slab_base(H.offB, H.e.y, SLAB_L_K, SLAB_L_K0) + H.LB.x, H.LB.y, RB.arcs, lane);
-  __syncwarp();
-  const int qb = (int)(ta - base), qe = (int)(tb - base);
-  const unsigned lt = (1u << lane) - 1u;
-  const bool whole = nA + nB <= PMAX;
-  if (whole) {
-    // every point of both rings, natural order: ring A at [0, nA), ring B at [nA, nA + nB).
-    // The entry of combined point k is the number of entry starts <= k (ring A's starts
-    // after its first entry, then ring B's starts shifted by nA).
+__device__ __forceinline__ void hdr_l1(const TriParams &P, int s, BandHdr &h, int lane) {
+  if (lane == 0) cp_async<16>(&h.bd, &P.band[s]);
+  else if (lane == 1) cp_async<8>(&h.base, &P.strut_off[s]);
+  else if (lane == 2) cp_async<8>(&h.e, &P.ends[s]);
+  else if (lane == 3) cp_async<8>(&h.ce, &P.strut_csr[s]);
+}
+__device__ __forceinline__ void hdr_l2(const TriParams &P, BandHdr &h, int lane) {
+  if (lane < 6) {
+    const int2 e = h.e, ce = h.ce;
+    if (lane == 0) cp_async<8>(&h.LA, &P.loop_hdr[ce.x]);
+    else if (lane == 1) cp_async<8>(&h.LB, &P.loop_hdr[ce.y]);
+    else if (lane == 2) cp_async<16>(&h.oa, &P.node[e.x]);
+    else if (lane == 3) cp_async<16>(&h.ob, &P.node[e.y]);
+    else if (lane == 4) cp_async<4>(&h.offA, &P.csr_off[e.x]);
+    else cp_async<4>(&h.offB, &P.csr_off[e.y]);
+  }
+}
+
+// Eq. 12 interior formula for point idx of ring r (entry e cached in shared memory); the
+// entry's start point (a shared vertex) is overwritten afterwards by band_vertices
+__device__ __forceinline__ f3 ring_point_formula(const WarpRing &w, int r, const RingRef &R, int e, int idx) {
+  const int nf = w.nf[r][e];
+  const int N = nf & 0xffff, fwd = nf >> 16;
+  const int j = idx - w.cum[r][e];
+  const int jj = fwd ? j : N - j;
+  const ArcRec A = lds_arc(&w.arc[r][e]);
+  float t = A.t0 + (float)jj * w.stp[r][e];
+  t = t - LMM_TWO_PI_F * rintf(t * (1.0f / LMM_TWO_PI_F));
+  float sn, cs;
+  __sincosf(t, &sn, &cs);
+  return F3(R.ox + fmaf(A.ax, sn, fmaf(A.bx, cs, A.ox)), R.oy + fmaf(A.ay, sn, fmaf(A.by, cs, A.oy)),
+            R.oz + fmaf(A.az, sn, fmaf(A.bz, cs, A.oz)));
+}
+
+__device__ __forceinline__ void put_point(WarpRing &w, int k, f3 p) { w.px[k] = p.x; w.py[k] = p.y; w.pz[k] = p.z; }
+__device__ __forceinline__ f3 get_point(const WarpRing &w, int k) { return F3(w.px[k], w.py[k], w.pz[k]); }
+
+// Whole-band emission.  Point cache layout: A_i at i (i = 0..nA, A_nA = A_0) and B_j at
+// nA + 1 + j (j = 0..nB, B_j = ring-B point (j + kB) mod nB), so triangle positions need
+// no wrapping.  The band's merge-bit words are staged in shared memory.
+__device__ void emit_band_whole(const TriParams &P, WarpRing &w, const RingRef &RA, const RingRef &RB,
+                                int64_t base, int nA, int nB, int kB, int qb, int qe, int64_t first,
+                                unsigned char *out, int lane) {
+  const int oB = nA + 1;
+  {
     const int cA = (lane >= 1 && lane < RA.cnt) ? w.cum[0][lane] : 0x7fffffff;
     const int cB = lane < RB.cnt ? nA + w.cum[1][lane] : 0x7fffffff;
     for (int x = 0; x < nA + nB; x += 32) {
@@ -536,58 +558,149 @@ __device__ void emit_band(const TriParams &P, WarpRing &w, const BandHdr &H, int
       const int ec = __popc(__ballot_sync(0xffffffffu, cA < x)) + __popc(__ballot_sync(0xffffffffu, cB < x)) +
                      __popc(M & ((2u << lane) - 1u));
       if (k < nA + nB) {
-        const bool rb = ec >= RA.cnt;
-        f3 p = rb ? ring_point_e(w, 1, RB, ec - RA.cnt, k - nA) : ring_point_e(w, 0, RA, ec, k);
-        w.px[k] = p.x; w.py[k] = p.y; w.pz[k] = p.z;
+        if (ec < RA.cnt) {
+          const f3 p = ring_point_formula(w, 0, RA, ec, k);
+          put_point(w, k, p);
+          if (k == 0) put_point(w, nA, p);
+        } else {
+          const int idx = k - nA;
+          const f3 p = ring_point_formula(w, 1, RB, ec - RA.cnt, idx);
+          const int jr = idx - kB + (idx < kB ? nB : 0);
+          put_point(w, oB + jr, p);
+          if (jr == 0) put_point(w, oB + nB, p);
+        }
       }
     }
+    __syncwarp();
+    // entry start points are the shared meta-mesh vertices, bit for bit (watertight seams)
+    for (int r = 0; r < 2; r++) {
+      const RingRef &R = r ? RB : RA;
+      if (lane < R.cnt) {
+        const int nf = w.nf[r][lane];
+        const uint32_t ids = w.arc[r][lane].ids;
+        const int v = (nf >> 16) ? (ids >> 16) & 0xff : (ids >> 24);
+        const float4 q = __ldg(&R.vs[v]);
+        const f3 p = F3(R.ox + q.x, R.oy + q.y, R.oz + q.z);
+        const int idx = w.cum[r][lane];
+        if (r == 0) {
+          put_point(w, idx, p);
+          if (idx == 0) put_point(w, nA, p);
+        } else {
+          const int jr = idx - kB + (idx < kB ? nB : 0);
+          put_point(w, oB + jr, p);
+          if (jr == 0) put_point(w, oB + nB, p);
+        }
+      }
+    }
+  }
+  // merge-bit words of the band, one per lane
+  const int64_t w0 = base >> 5;
+  const int nwd = (int)(((base + nA + nB - 1) >> 5) - w0 + 1);
+  uint32_t mword = lane < nwd ? __ldg(&P.mbits[w0 + lane]) : 0u;
+  const unsigned lt = (1u << lane) - 1u;
+  int irun = qb == 0 ? 0 : merge_rank(P, base, base + qb);
+  const int sb = (int)(base & 31);
+  for (int gq = qb - (int)((base + qb - first) & 7); gq < qe; gq += GRP) {
+    const int qa = gq + 2 * lane, qb2 = qa + 1;
+    const int lo_q = gq > qb ? gq : qb;
+    const int hi_q = gq + GRP < qe ? gq + GRP : qe;
+    const bool va = qa >= lo_q && qa < hi_q, vb = qb2 >= lo_q && qb2 < hi_q;
+    // bit of step q: word (sb + q) >> 5 of the band's words, from the owning lane
+    const int ba = sb + (va ? qa : 0), bb = sb + (vb ? qb2 : 0);
+    const uint32_t wa = __shfl_sync(0xffffffffu, mword, ba >> 5), wb = __shfl_sync(0xffffffffu, mword, bb >> 5);
+    const bool aa = va && ((wa >> (ba & 31)) & 1u);
+    const bool ab = vb && ((wb >> (bb & 31)) & 1u);
+    const unsigned ma = __ballot_sync(0xffffffffu, aa), mb = __ballot_sync(0xffffffffu, ab);
+    const int ia = irun + __popc(ma & lt) + __popc(mb & lt);
+    irun += __popc(ma) + __popc(mb);
+    __syncwarp();
+    if (va || vb) {
+      // state before the lane's first valid step: A_i, B_j; each triangle (A_i, c, B_j)
+      // advances one ring onto its new point c
+      int i = ia, j = (va ? qa : qb2) - ia;
+      f3 pA = get_point(w, i), pB = get_point(w, oB + j);
+      uint32_t *d = reinterpret_cast<uint32_t *>(w.stage) + 25 * lane;   // records 2l, 2l+1
+      if (va) {
+        const f3 c = get_point(w, aa ? i + 1 : oB + j + 1);
+        uint32_t f[12];
+        tri_words(pA, c, pB, f);
+#pragma unroll
+        for (int t = 0; t < 12; t++) d[t] = f[t];
+        if (aa) { pA = c; i++; } else { pB = c; j++; }
+      }
+      if (vb) {
+        const f3 c = get_point(w, ab ? i + 1 : oB + j + 1);
+        uint32_t g[12];
+        tri_words(pA, c, pB, g);
+        d[12] = g[0] << 16;   // attribute 0 | low half of g0
+#pragma unroll
+        for (int t = 0; t < 11; t++) d[13 + t] = __funnelshift_r(g[t], g[t + 1], 16);
+        d[24] = g[11] >> 16;
+      } else d[12] = 0;
+    }
+    flush_group(w, (lo_q - gq) * REC, (hi_q - gq) * REC, out + (base + gq - first) * REC, lane);
+  }
+}
+
+template <class Prefetch>
+__device__ void emit_band(const TriParams &P, WarpRing &w, const BandHdr &H, int64_t first, int64_t last,
+                          unsigned char *out, int lane, Prefetch prefetch) {
+  const int64_t base = H.base;
+  const int4 bd = H.bd;
+  const int nA = bd.x, nB = bd.y, kB = bd.z;
+  const int64_t ta = base > first ? base : first;
+  const int64_t tb = base + nA + nB < last ? base + nA + nB : last;
+  if (ta >= tb) { prefetch(); return; }
+  const int2 e = H.e, LA = H.LA, LB = H.LB;
+  const int offA = H.offA, offB = H.offB;
+  const float4 oa = H.oa, ob = H.ob;
+  RingRef RA, RB;
+  RA.arcs = P.arc + slab_base(offA, e.x, SLAB_A_K, SLAB_A_K0);
+  RA.vs = P.vert + slab_base(offA, e.x, SLAB_V_K, SLAB_V_K0);
+  RA.ox = oa.x; RA.oy = oa.y; RA.oz = oa.z; RA.cnt = LA.y;
+  RB.arcs = P.arc + slab_base(offB, e.y, SLAB_A_K, SLAB_A_K0);
+  RB.vs = P.vert + slab_base(offB, e.y, SLAB_V_K, SLAB_V_K0);
+  RB.ox = ob.x; RB.oy = ob.y; RB.oz = ob.z; RB.cnt = LB.y;
+  load_ring(w, 0, P.loop + slab_base(offA, e.x, SLAB_L_K, SLAB_L_K0) + LA.x, LA.y, RA.arcs, lane);
+  load_ring(w, 1, P.loop + slab_base(offB, e.y, SLAB_L_K, SLAB_L_K0) + LB.x, LB.y, RB.arcs, lane);
+  __syncwarp();
+  const int qb = (int)(ta - base), qe = (int)(tb - base);
+  if (nA + nB + 2 <= PMAX && RA.cnt <= MAXRA && RB.cnt <= MAXRA && nA + nB <= 32 * 30) {
+    emit_band_whole(P, w, RA, RB, base, nA, nB, kB, qb, qe, first, out, lane);
     prefetch();
     __syncwarp();
+    return;
   }
+  const unsigned lt = (1u << lane) - 1u;
   for (int q0 = qb, q1; q0 < qe; q0 = q1) {
-    int i0 = 0, na = 0;
-    if (whole) q1 = qe;
-    else {
-      q1 = q0 - (int)((base + q0 - first) & 7) + WIN;   // windows end on the 8-triangle grid
-      q1 = q1 < qe ? q1 : qe;
-      int i1 = 0;
-      if (lane == 0) i0 = merge_rank(P, base, base + q0);
-      if (lane == 1) i1 = (q1 == nA + nB) ? nA : merge_rank(P, base, base + q1);
-      i0 = __shfl_sync(0xffffffffu, i0, 0);
-      i1 = __shfl_sync(0xffffffffu, i1, 1);
-      const int j0 = q0 - i0, j1 = q1 - i1;
-      na = i1 - i0 + 1;
-      const int nb = j1 - j0 + 1;
-      for (int k = lane; k < na + nb; k += 32) {
-        const int r = k < na ? 0 : 1;
-        const int kk = r ? k - na : k;
-        const int n = r ? nB : nA;
-        int idx = r ? j0 + kk + kB : i0 + kk;
-        idx = idx >= n ? idx - n : idx;
-        idx = idx >= n ? idx - n : idx;
-        f3 p = r ? ring_point(w, 1, RB, idx) : ring_point(w, 0, RA, idx);
-        w.px[k] = p.x; w.py[k] = p.y; w.pz[k] = p.z;
-      }
-      __syncwarp();
+    q1 = q0 - (int)((base + q0 - first) & 7) + WIN;   // windows end on the 8-triangle grid
+    q1 = q1 < qe ? q1 : qe;
+    int i0 = 0, i1 = 0;
+    if (lane == 0) i0 = merge_rank(P, base, base + q0);
+    if (lane == 1) i1 = (q1 == nA + nB) ? nA : merge_rank(P, base, base + q1);
+    i0 = __shfl_sync(0xffffffffu, i0, 0);
+    i1 = __shfl_sync(0xffffffffu, i1, 1);
+    const int j0 = q0 - i0, j1 = q1 - i1;
+    const int na = i1 - i0 + 1;
+    const int nb = j1 - j0 + 1;
+    for (int k = lane; k < na + nb; k += 32) {
+      const int r = k < na ? 0 : 1;
+      const int kk = r ? k - na : k;
+      const int n = r ? nB : nA;
+      int idx = r ? j0 + kk + kB : i0 + kk;
+      idx = idx >= n ? idx - n : idx;
+      idx = idx >= n ? idx - n : idx;
+      f3 p = r ? ring_point(w, 1, RB, idx) : ring_point(w, 0, RA, idx);
+      put_point(w, k, p);
     }
-    // position in the point cache of A_i and B_j (whole: natural order, B rotated by kB)
-    auto posA = [&](int i) { return whole ? (i >= nA ? i - nA : i) : i - i0; };
-    auto posB = [&](int j) {
-      if (!whole) return na + (j - (q0 - i0));
-      int jr = j + kB;
-      jr = jr >= nB ? jr - nB : jr;
-      return nA + jr;
-    };
+    __syncwarp();
     // the record of step q is the triangle (A_i, A_i+1, B_j) or (A_i, B_j+1, B_j)
     auto tri = [&](int q, int i, bool advA, uint32_t *f) {
-      const int pa = posA(i), pb = posB(q - i);
-      const int pc = advA ? posA(i + 1) : posB(q - i + 1);
-      tri_words(F3(w.px[pa], w.py[pa], w.pz[pa]), F3(w.px[pc], w.py[pc], w.pz[pc]), F3(w.px[pb], w.py[pb], w.pz[pb]), f);
+      const int pa = i - i0, pb = na + (q - i - j0);
+      const int pc = advA ? pa + 1 : pb + 1;
+      tri_words(get_point(w, pa), get_point(w, pc), get_point(w, pb), f);
     };
-    int irun = whole ? (q0 == 0 ? 0 : merge_rank(P, base, base + q0)) : i0;
-    // groups on the 8-triangle output grid (16-byte aligned records); a band's first group
-    // may start mid-grid: its lanes below the start stay idle and the flush begins with a
-    // partial 16-byte unit.  Lane l takes steps g+2l and g+2l+1.
+    int irun = i0;
     for (int gq = q0 - (int)((base + q0 - first) & 7); gq < q1; gq += GRP) {
       const int qa = gq + 2 * lane, qb2 = qa + 1;
       const int lo_q = gq > q0 ? gq : q0;
@@ -602,22 +715,14 @@ __device__ void emit_band(const TriParams &P, WarpRing &w, const BandHdr &H, int
       if (va || vb) {
         uint32_t f[12], g[12];
         if (va) tri(qa, ia, aa, f);
-        else {
-#pragma unroll
-          for (int i = 0; i < 12; i++) f[i] = 0;
-        }
         if (vb) tri(qb2, ia + (aa ? 1 : 0), ab, g);
-        else {
-#pragma unroll
-          for (int i = 0; i < 12; i++) g[i] = 0;
-        }
         put_pair(reinterpret_cast<uint32_t *>(w.stage) + 25 * lane, f, g);
       }
       flush_group(w, (lo_q - gq) * REC, (hi_q - gq) * REC, out + (base + gq - first) * REC, lane);
     }
     __syncwarp();
   }
-  if (!whole) prefetch();
+  prefetch();
 }
 
 __device__ void emit_hole(const TriParams &P, WarpRing &w, int g, int64_t first, int64_t last,
@@ -642,7 +747,7 @@ __device__ void emit_hole(const TriParams &P, WarpRing &w, int g, int64_t first,
     HoleEnt E = he[lane];
     const int N = le_N(E.arc_fwd), a = le_arc(E.arc_fwd);
     w.cum[0][lane] = E.cum; w.nf[0][lane] = N | (le_fwd(E.arc_fwd) << 16); w.ax[0][lane] = a;
-    w.stp[0][lane] = __ldg(&RH.arcs[a].dt) / (float)N;
+    w.stp[0][lane] = __fdividef(__ldg(&RH.arcs[a].dt), (float)N);
   }
   __syncwarp();
   {
@@ -690,15 +795,31 @@ __global__ void __launch_bounds__(EMIT_T, 7) k_emit(TriParams P, int64_t first, 
   const int64_t last = first + count;
   const int64_t gw = (int64_t)blockIdx.x * EW + warp, nw = (int64_t)gridDim.x * EW;
   const int64_t nb = s1 - s0, nh = g1 - g0;
-  BandHdr cur;
-  if (gw < nb) { hdr_l1(P, (int)(s0 + gw), cur); hdr_l2(P, cur); }
+  __shared__ BandHdr hdr[EW][2];
+  int cb = 0;
+  if (gw < nb) {
+    hdr_l1(P, (int)(s0 + gw), hdr[warp][0], lane);
+    cp_async_wait_all();
+    __syncwarp();
+    hdr_l2(P, hdr[warp][0], lane);
+    cp_async_wait_all();
+    __syncwarp();
+  }
   for (int64_t u = gw; u < nb + nh; u += nw) {
     if (u < nb) {
-      BandHdr nxt;
       const bool more = u + nw < nb;
-      if (more) hdr_l1(P, (int)(s0 + u + nw), nxt);
-      emit_band(P, w, cur, first, last, out, lane, [&] { if (more) hdr_l2(P, nxt); });
-      if (more) cur = nxt;
+      BandHdr &nx = hdr[warp][cb ^ 1];
+      if (more) hdr_l1(P, (int)(s0 + u + nw), nx, lane);
+      emit_band(P, w, hdr[warp][cb], first, last, out, lane, [&] {
+        if (more) {
+          cp_async_wait_all();
+          __syncwarp();
+          hdr_l2(P, nx, lane);
+        }
+      });
+      cp_async_wait_all();
+      __syncwarp();
+      cb ^= 1;
     } else emit_hole(P, w, (int)(g0 + u - nb), first, last, out, lane);
   }
 }
