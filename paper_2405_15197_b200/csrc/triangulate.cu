@@ -326,15 +326,20 @@ __device__ __forceinline__ void put_rec(unsigned char *dst, f3 a, f3 b, f3 c) {
 }
 
 // Warp-per-band emission.  Warps grid-stride over the strut bands (then the hole fans)
-// that intersect [first, first+count).  Per band the warp caches both rings' loop entries
-// and arc records in shared memory and computes every ring point once, in parallel (the
-// entry of a point comes from a ballot/redux count of the entry starts below it).  Bands
-// whose two rings exceed PMAX points are walked in windows of WIN merge steps instead.
+// that intersect [first, first+count).  A band's ring data -- both rings' loop entries and
+// arc records -- sits in shared memory; every ring point is computed once, in parallel
+// (the entry of a point comes from a ballot/redux count of the entry starts below it).
+// Bands whose rings exceed PMAX points are walked in windows of WIN merge steps instead.
 // Triangles then go in groups of 64 whose output offset is 16-byte aligned: lane l
 // assembles records 2l and 2l+1 (100 bytes = 25 aligned words), its ring positions
 // following from ballot prefix-popcounts of the merge bits; the group leaves the per-warp
-// staging buffer as 16-byte vector stores.  The next band's header loads are issued while
-// the current band is being emitted.  No block-level barriers.
+// staging buffer as 16-byte vector stores.
+//
+// The next band's data is fetched with cp.async straight into shared memory in four
+// dependent stages overlapped with the current band: header (before its points), loop
+// headers / centres / offsets (after its points), loop entries (after its first group)
+// and arc records (after its last group).  No registers are held across a band and no
+// block-level barriers are used.
 constexpr int EW = EMIT_T / 32;   // warps per CTA
 constexpr int PMAX = 160;         // ring points cached per band (both rings)
 constexpr int WIN = PMAX - 2;     // merge steps per window of a band with more points
@@ -344,13 +349,72 @@ constexpr int MAXRA = 12;         // arc records cached per ring
 
 struct __align__(16) WarpRing {
   ArcRec arc[2][MAXRA];
-  int cum[2][MAXRE];
-  int nf[2][MAXRE];     // N | fwd << 16
-  int ax[2][MAXRE];     // arc index in the node's arc slab
-  float stp[2][MAXRE];  // parameter step dt / N
+  LoopRec le[2][MAXRE];   // loop entries (arc | fwd | N, phs, dph, cum); holes: arc_fwd, cum
   float px[PMAX], py[PMAX], pz[PMAX];
   uint4 stage[GRP * REC / 16];
 };
+
+// band header: band / strut_off / ends / strut_csr (stage 1), then the loop headers, node
+// centres and CSR offsets of both ends (stage 2)
+struct __align__(16) BandHdr {
+  int4 bd;
+  float4 oa, ob;
+  long long base;
+  int2 e, ce;
+  int2 LA, LB;
+  int offA, offB;
+};
+
+template <int BYTES>
+__device__ __forceinline__ void cp_async(void *sdst, const void *gsrc) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(sa), "l"(gsrc), "n"(BYTES) : "memory");
+}
+// all of this thread's cp.async done, then visible to the warp
+__device__ __forceinline__ void cp_async_wait_warp() {
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  __syncwarp();
+}
+
+__device__ __forceinline__ void fetch_hdr(const TriParams &P, int s, BandHdr &h, int lane) {
+  if (lane == 0) cp_async<16>(&h.bd, &P.band[s]);
+  else if (lane == 1) cp_async<8>(&h.base, &P.strut_off[s]);
+  else if (lane == 2) cp_async<8>(&h.e, &P.ends[s]);
+  else if (lane == 3) cp_async<8>(&h.ce, &P.strut_csr[s]);
+}
+__device__ __forceinline__ void fetch_ends(const TriParams &P, BandHdr &h, int lane) {
+  if (lane < 6) {
+    const int2 e = h.e, ce = h.ce;
+    if (lane == 0) cp_async<8>(&h.LA, &P.loop_hdr[ce.x]);
+    else if (lane == 1) cp_async<8>(&h.LB, &P.loop_hdr[ce.y]);
+    else if (lane == 2) cp_async<16>(&h.oa, &P.node[e.x]);
+    else if (lane == 3) cp_async<16>(&h.ob, &P.node[e.y]);
+    else if (lane == 4) cp_async<4>(&h.offA, &P.csr_off[e.x]);
+    else cp_async<4>(&h.offB, &P.csr_off[e.y]);
+  }
+}
+__device__ __forceinline__ bool band_live(const BandHdr &h) { return h.bd.x + h.bd.y > 0; }
+__device__ __forceinline__ void fetch_entries(const TriParams &P, WarpRing &w, const BandHdr &h, int lane) {
+  if (!band_live(h)) return;
+  const int2 LA = h.LA, LB = h.LB;
+  if (lane < LA.y) cp_async<16>(&w.le[0][lane], P.loop + slab_base(h.offA, h.e.x, SLAB_L_K, SLAB_L_K0) + LA.x + lane);
+  if (lane < LB.y) cp_async<16>(&w.le[1][lane], P.loop + slab_base(h.offB, h.e.y, SLAB_L_K, SLAB_L_K0) + LB.x + lane);
+}
+__device__ __forceinline__ void fetch_arcs(const TriParams &P, WarpRing &w, const BandHdr &h, int lane) {
+  if (!band_live(h)) return;
+#pragma unroll
+  for (int r = 0; r < 2; r++) {
+    const int cnt = r ? h.LB.y : h.LA.y;
+    const ArcRec *arcs = P.arc + (r ? slab_base(h.offB, h.e.y, SLAB_A_K, SLAB_A_K0) : slab_base(h.offA, h.e.x, SLAB_A_K, SLAB_A_K0));
+    const int nq = (cnt < MAXRA ? cnt : MAXRA) * 3;
+    for (int k = lane; k < nq; k += 32) {
+      const int e = k / 3;
+      cp_async<16>(reinterpret_cast<float4 *>(&w.arc[r][e]) + (k - 3 * e),
+                   reinterpret_cast<const float4 *>(arcs + le_arc(w.le[r][e].arc_fwd)) + (k - 3 * e));
+    }
+  }
+}
 
 struct RingRef {
   const ArcRec *arcs;
@@ -371,19 +435,19 @@ __device__ __forceinline__ ArcRec lds_arc(const ArcRec *p) {
 
 // Eq. 12 point idx of ring r, whose loop entry is e; endpoints are the shared vertices
 __device__ __forceinline__ f3 ring_point_e(const WarpRing &w, int r, const RingRef &R, int e, int idx) {
-  const int nf = w.nf[r][e];
-  const int N = nf & 0xffff, fwd = nf >> 16;
-  const int j = idx - w.cum[r][e];
+  const LoopRec L = w.le[r][e];
+  const int N = le_N(L.arc_fwd), fwd = le_fwd(L.arc_fwd);
+  const int j = idx - L.cum;
   const int jj = fwd ? j : N - j;
   f3 p;
   if (jj == 0 || jj == N) {
-    const uint32_t ids = e < MAXRA ? w.arc[r][e].ids : __ldg(&R.arcs[w.ax[r][e]].ids);
+    const uint32_t ids = e < MAXRA ? w.arc[r][e].ids : __ldg(&R.arcs[le_arc(L.arc_fwd)].ids);
     const int v = jj == 0 ? (ids >> 16) & 0xff : (ids >> 24);
     const float4 q = __ldg(&R.vs[v]);
     p = F3(q.x, q.y, q.z);
   } else {
-    const ArcRec A = e < MAXRA ? lds_arc(&w.arc[r][e]) : load_arc(R.arcs + w.ax[r][e]);
-    float t = A.t0 + (float)jj * w.stp[r][e];
+    const ArcRec A = e < MAXRA ? lds_arc(&w.arc[r][e]) : load_arc(R.arcs + le_arc(L.arc_fwd));
+    float t = A.t0 + (float)jj * __fdividef(A.dt, (float)N);
     t = t - LMM_TWO_PI_F * rintf(t * (1.0f / LMM_TWO_PI_F));
     float sn, cs;
     __sincosf(t, &sn, &cs);
@@ -395,9 +459,28 @@ __device__ __forceinline__ f3 ring_point_e(const WarpRing &w, int r, const RingR
 // point idx of ring r, its entry found by a scan of the entry starts (windowed bands, holes)
 __device__ __forceinline__ f3 ring_point(const WarpRing &w, int r, const RingRef &R, int idx) {
   int e = 0;
-  for (int k = 1; k < R.cnt; k++) e += (w.cum[r][k] <= idx) ? 1 : 0;
+  for (int k = 1; k < R.cnt; k++) e += (w.le[r][k].cum <= idx) ? 1 : 0;
   return ring_point_e(w, r, R, e, idx);
 }
+
+// Eq. 12 interior formula (entry and arc cached); entry start points are overwritten with
+// the shared vertices afterwards
+__device__ __forceinline__ f3 ring_point_formula(const WarpRing &w, int r, const RingRef &R, int e, int idx) {
+  const LoopRec L = w.le[r][e];
+  const int N = le_N(L.arc_fwd), fwd = le_fwd(L.arc_fwd);
+  const int j = idx - L.cum;
+  const int jj = fwd ? j : N - j;
+  const ArcRec A = lds_arc(&w.arc[r][e]);
+  float t = A.t0 + (float)jj * __fdividef(A.dt, (float)N);
+  t = t - LMM_TWO_PI_F * rintf(t * (1.0f / LMM_TWO_PI_F));
+  float sn, cs;
+  __sincosf(t, &sn, &cs);
+  return F3(R.ox + fmaf(A.ax, sn, fmaf(A.bx, cs, A.ox)), R.oy + fmaf(A.ay, sn, fmaf(A.by, cs, A.oy)),
+            R.oz + fmaf(A.az, sn, fmaf(A.bz, cs, A.oz)));
+}
+
+__device__ __forceinline__ void put_point(WarpRing &w, int k, f3 p) { w.px[k] = p.x; w.py[k] = p.y; w.pz[k] = p.z; }
+__device__ __forceinline__ f3 get_point(const WarpRing &w, int k) { return F3(w.px[k], w.py[k], w.pz[k]); }
 
 // A-advances of band [base, ...) before triangle t
 __device__ __forceinline__ int merge_rank(const TriParams &P, int64_t base, int64_t t) {
@@ -423,14 +506,16 @@ __device__ __forceinline__ void tri_words(f3 a, f3 b, f3 c, uint32_t *f) {
   f[9] = __float_as_uint(c.x); f[10] = __float_as_uint(c.y); f[11] = __float_as_uint(c.z);
 }
 
-// two consecutive 50-byte records as 25 aligned words
-__device__ __forceinline__ void put_pair(uint32_t *d, const uint32_t *f, const uint32_t *g) {
+// records 2l (f) and 2l+1 (g) as 25 aligned words: f, then attribute 0 | g shifted by 16
+__device__ __forceinline__ void put_first(uint32_t *d, const uint32_t *f) {
 #pragma unroll
   for (int i = 0; i < 12; i++) d[i] = f[i];
-  d[12] = g[0] << 16;   // attribute 0 | low half of g0
+}
+__device__ __forceinline__ void put_second(uint32_t *d, const uint32_t *g) {
+  d[12] = g[0] << 16;
 #pragma unroll
   for (int i = 0; i < 11; i++) d[13 + i] = __funnelshift_r(g[i], g[i + 1], 16);
-  d[24] = g[11] >> 16;   // high half of g11 | attribute 0
+  d[24] = g[11] >> 16;
 }
 
 // one record through 2-byte stores (unaligned hole triangles)
@@ -466,91 +551,20 @@ __device__ __forceinline__ void flush_group(WarpRing &w, int b0, int b1, unsigne
   __syncwarp();
 }
 
-__device__ __forceinline__ void load_ring(WarpRing &w, int r, const LoopRec *le, int cnt, const ArcRec *arcs, int lane) {
-  if (lane < cnt) {
-    LoopRec L = le[lane];
-    const int N = le_N(L.arc_fwd), a = le_arc(L.arc_fwd);
-    w.cum[r][lane] = L.cum;
-    w.nf[r][lane] = N | (le_fwd(L.arc_fwd) << 16);
-    w.ax[r][lane] = a;
-    w.stp[r][lane] = __fdividef(__ldg(&arcs[a].dt), (float)N);
-  }
-  __syncwarp();
-  const int nq = (cnt < MAXRA ? cnt : MAXRA) * 3;
-  float4 *dst = reinterpret_cast<float4 *>(w.arc[r]);
-  for (int k = lane; k < nq; k += 32) dst[k] = __ldg(reinterpret_cast<const float4 *>(arcs + w.ax[r][k / 3]) + (k % 3));
-}
-
-// band header: band / strut_off / ends / strut_csr (level 1), then the loop headers, node
-// centres and CSR offsets of both ends (level 2).  The next band's header is fetched
-// with cp.async straight into shared memory while the current band is emitted, so no
-// registers are held across the band.
-struct __align__(16) BandHdr {
-  int4 bd;
-  float4 oa, ob;
-  long long base;
-  int2 e, ce;
-  int2 LA, LB;
-  int offA, offB;
-};
-
-template <int BYTES>
-__device__ __forceinline__ void cp_async(void *sdst, const void *gsrc) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(sa), "l"(gsrc), "n"(BYTES) : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.commit_group;\n" ::: "memory");
-  asm volatile("cp.async.wait_all;\n" ::: "memory");
-}
-
-__device__ __forceinline__ void hdr_l1(const TriParams &P, int s, BandHdr &h, int lane) {
-  if (lane == 0) cp_async<16>(&h.bd, &P.band[s]);
-  else if (lane == 1) cp_async<8>(&h.base, &P.strut_off[s]);
-  else if (lane == 2) cp_async<8>(&h.e, &P.ends[s]);
-  else if (lane == 3) cp_async<8>(&h.ce, &P.strut_csr[s]);
-}
-__device__ __forceinline__ void hdr_l2(const TriParams &P, BandHdr &h, int lane) {
-  if (lane < 6) {
-    const int2 e = h.e, ce = h.ce;
-    if (lane == 0) cp_async<8>(&h.LA, &P.loop_hdr[ce.x]);
-    else if (lane == 1) cp_async<8>(&h.LB, &P.loop_hdr[ce.y]);
-    else if (lane == 2) cp_async<16>(&h.oa, &P.node[e.x]);
-    else if (lane == 3) cp_async<16>(&h.ob, &P.node[e.y]);
-    else if (lane == 4) cp_async<4>(&h.offA, &P.csr_off[e.x]);
-    else cp_async<4>(&h.offB, &P.csr_off[e.y]);
-  }
-}
-
-// Eq. 12 interior formula for point idx of ring r (entry e cached in shared memory); the
-// entry's start point (a shared vertex) is overwritten afterwards by band_vertices
-__device__ __forceinline__ f3 ring_point_formula(const WarpRing &w, int r, const RingRef &R, int e, int idx) {
-  const int nf = w.nf[r][e];
-  const int N = nf & 0xffff, fwd = nf >> 16;
-  const int j = idx - w.cum[r][e];
-  const int jj = fwd ? j : N - j;
-  const ArcRec A = lds_arc(&w.arc[r][e]);
-  float t = A.t0 + (float)jj * w.stp[r][e];
-  t = t - LMM_TWO_PI_F * rintf(t * (1.0f / LMM_TWO_PI_F));
-  float sn, cs;
-  __sincosf(t, &sn, &cs);
-  return F3(R.ox + fmaf(A.ax, sn, fmaf(A.bx, cs, A.ox)), R.oy + fmaf(A.ay, sn, fmaf(A.by, cs, A.oy)),
-            R.oz + fmaf(A.az, sn, fmaf(A.bz, cs, A.oz)));
-}
-
-__device__ __forceinline__ void put_point(WarpRing &w, int k, f3 p) { w.px[k] = p.x; w.py[k] = p.y; w.pz[k] = p.z; }
-__device__ __forceinline__ f3 get_point(const WarpRing &w, int k) { return F3(w.px[k], w.py[k], w.pz[k]); }
-
 // Whole-band emission.  Point cache layout: A_i at i (i = 0..nA, A_nA = A_0) and B_j at
 // nA + 1 + j (j = 0..nB, B_j = ring-B point (j + kB) mod nB), so triangle positions need
-// no wrapping.  The band's merge-bit words are staged in shared memory.
+// no wrapping.  The band's merge-bit words are held one per lane.
+template <class Prefetch>
 __device__ void emit_band_whole(const TriParams &P, WarpRing &w, const RingRef &RA, const RingRef &RB,
                                 int64_t base, int nA, int nB, int kB, int qb, int qe, int64_t first,
-                                unsigned char *out, int lane) {
+                                unsigned char *out, int lane, Prefetch &prefetch) {
   const int oB = nA + 1;
+  const int64_t w0 = base >> 5;
+  const int nwd = (int)(((base + nA + nB - 1) >> 5) - w0 + 1);
+  const uint32_t mword = lane < nwd ? __ldg(&P.mbits[w0 + lane]) : 0u;
   {
-    const int cA = (lane >= 1 && lane < RA.cnt) ? w.cum[0][lane] : 0x7fffffff;
-    const int cB = lane < RB.cnt ? nA + w.cum[1][lane] : 0x7fffffff;
+    const int cA = (lane >= 1 && lane < RA.cnt) ? w.le[0][lane].cum : 0x7fffffff;
+    const int cB = lane < RB.cnt ? nA + w.le[1][lane].cum : 0x7fffffff;
     for (int x = 0; x < nA + nB; x += 32) {
       const int k = x + lane;
       const unsigned bits = ((cA >= x && cA < x + 32) ? 1u << (cA - x) : 0u) | ((cB >= x && cB < x + 32) ? 1u << (cB - x) : 0u);
@@ -573,15 +587,16 @@ __device__ void emit_band_whole(const TriParams &P, WarpRing &w, const RingRef &
     }
     __syncwarp();
     // entry start points are the shared meta-mesh vertices, bit for bit (watertight seams)
+#pragma unroll
     for (int r = 0; r < 2; r++) {
       const RingRef &R = r ? RB : RA;
       if (lane < R.cnt) {
-        const int nf = w.nf[r][lane];
+        const LoopRec L = w.le[r][lane];
         const uint32_t ids = w.arc[r][lane].ids;
-        const int v = (nf >> 16) ? (ids >> 16) & 0xff : (ids >> 24);
+        const int v = le_fwd(L.arc_fwd) ? (ids >> 16) & 0xff : (ids >> 24);
         const float4 q = __ldg(&R.vs[v]);
         const f3 p = F3(R.ox + q.x, R.oy + q.y, R.oz + q.z);
-        const int idx = w.cum[r][lane];
+        const int idx = L.cum;
         if (r == 0) {
           put_point(w, idx, p);
           if (idx == 0) put_point(w, nA, p);
@@ -592,14 +607,13 @@ __device__ void emit_band_whole(const TriParams &P, WarpRing &w, const RingRef &
         }
       }
     }
+    __syncwarp();
   }
-  // merge-bit words of the band, one per lane
-  const int64_t w0 = base >> 5;
-  const int nwd = (int)(((base + nA + nB - 1) >> 5) - w0 + 1);
-  uint32_t mword = lane < nwd ? __ldg(&P.mbits[w0 + lane]) : 0u;
+  prefetch(1);   // the ring data of this band is dead from here on
   const unsigned lt = (1u << lane) - 1u;
   int irun = qb == 0 ? 0 : merge_rank(P, base, base + qb);
   const int sb = (int)(base & 31);
+  bool second = false;
   for (int gq = qb - (int)((base + qb - first) & 7); gq < qe; gq += GRP) {
     const int qa = gq + 2 * lane, qb2 = qa + 1;
     const int lo_q = gq > qb ? gq : qb;
@@ -613,7 +627,6 @@ __device__ void emit_band_whole(const TriParams &P, WarpRing &w, const RingRef &
     const unsigned ma = __ballot_sync(0xffffffffu, aa), mb = __ballot_sync(0xffffffffu, ab);
     const int ia = irun + __popc(ma & lt) + __popc(mb & lt);
     irun += __popc(ma) + __popc(mb);
-    __syncwarp();
     if (va || vb) {
       // state before the lane's first valid step: A_i, B_j; each triangle (A_i, c, B_j)
       // advances one ring onto its new point c
@@ -624,22 +637,21 @@ __device__ void emit_band_whole(const TriParams &P, WarpRing &w, const RingRef &
         const f3 c = get_point(w, aa ? i + 1 : oB + j + 1);
         uint32_t f[12];
         tri_words(pA, c, pB, f);
-#pragma unroll
-        for (int t = 0; t < 12; t++) d[t] = f[t];
+        put_first(d, f);
         if (aa) { pA = c; i++; } else { pB = c; j++; }
       }
       if (vb) {
         const f3 c = get_point(w, ab ? i + 1 : oB + j + 1);
         uint32_t g[12];
         tri_words(pA, c, pB, g);
-        d[12] = g[0] << 16;   // attribute 0 | low half of g0
-#pragma unroll
-        for (int t = 0; t < 11; t++) d[13 + t] = __funnelshift_r(g[t], g[t + 1], 16);
-        d[24] = g[11] >> 16;
-      } else d[12] = 0;
+        put_second(d, g);
+      }
     }
     flush_group(w, (lo_q - gq) * REC, (hi_q - gq) * REC, out + (base + gq - first) * REC, lane);
+    if (!second) { prefetch(2); second = true; }
   }
+  if (!second) prefetch(2);
+  prefetch(3);
 }
 
 template <class Prefetch>
@@ -650,7 +662,7 @@ __device__ void emit_band(const TriParams &P, WarpRing &w, const BandHdr &H, int
   const int nA = bd.x, nB = bd.y, kB = bd.z;
   const int64_t ta = base > first ? base : first;
   const int64_t tb = base + nA + nB < last ? base + nA + nB : last;
-  if (ta >= tb) { prefetch(); return; }
+  if (ta >= tb) { prefetch(1); prefetch(2); prefetch(3); return; }
   const int2 e = H.e, LA = H.LA, LB = H.LB;
   const int offA = H.offA, offB = H.offB;
   const float4 oa = H.oa, ob = H.ob;
@@ -661,16 +673,12 @@ __device__ void emit_band(const TriParams &P, WarpRing &w, const BandHdr &H, int
   RB.arcs = P.arc + slab_base(offB, e.y, SLAB_A_K, SLAB_A_K0);
   RB.vs = P.vert + slab_base(offB, e.y, SLAB_V_K, SLAB_V_K0);
   RB.ox = ob.x; RB.oy = ob.y; RB.oz = ob.z; RB.cnt = LB.y;
-  load_ring(w, 0, P.loop + slab_base(offA, e.x, SLAB_L_K, SLAB_L_K0) + LA.x, LA.y, RA.arcs, lane);
-  load_ring(w, 1, P.loop + slab_base(offB, e.y, SLAB_L_K, SLAB_L_K0) + LB.x, LB.y, RB.arcs, lane);
-  __syncwarp();
   const int qb = (int)(ta - base), qe = (int)(tb - base);
-  if (nA + nB + 2 <= PMAX && RA.cnt <= MAXRA && RB.cnt <= MAXRA && nA + nB <= 32 * 30) {
-    emit_band_whole(P, w, RA, RB, base, nA, nB, kB, qb, qe, first, out, lane);
-    prefetch();
-    __syncwarp();
+  if (nA + nB + 2 <= PMAX && RA.cnt <= MAXRA && RB.cnt <= MAXRA) {
+    emit_band_whole(P, w, RA, RB, base, nA, nB, kB, qb, qe, first, out, lane, prefetch);
     return;
   }
+  // windowed: the ring data stays in use to the end, the next band's stages follow it
   const unsigned lt = (1u << lane) - 1u;
   for (int q0 = qb, q1; q0 < qe; q0 = q1) {
     q1 = q0 - (int)((base + q0 - first) & 7) + WIN;   // windows end on the 8-triangle grid
@@ -713,16 +721,18 @@ __device__ void emit_band(const TriParams &P, WarpRing &w, const BandHdr &H, int
       const int ia = irun + __popc(ma & lt) + __popc(mb & lt);
       irun += __popc(ma) + __popc(mb);
       if (va || vb) {
-        uint32_t f[12], g[12];
-        if (va) tri(qa, ia, aa, f);
-        if (vb) tri(qb2, ia + (aa ? 1 : 0), ab, g);
-        put_pair(reinterpret_cast<uint32_t *>(w.stage) + 25 * lane, f, g);
+        uint32_t *d = reinterpret_cast<uint32_t *>(w.stage) + 25 * lane;
+        uint32_t f[12];
+        if (va) { tri(qa, ia, aa, f); put_first(d, f); }
+        if (vb) { tri(qb2, ia + (aa ? 1 : 0), ab, f); put_second(d, f); }
       }
       flush_group(w, (lo_q - gq) * REC, (hi_q - gq) * REC, out + (base + gq - first) * REC, lane);
     }
     __syncwarp();
   }
-  prefetch();
+  prefetch(1);
+  prefetch(2);
+  prefetch(3);
 }
 
 __device__ void emit_hole(const TriParams &P, WarpRing &w, int g, int64_t first, int64_t last,
@@ -741,19 +751,20 @@ __device__ void emit_hole(const TriParams &P, WarpRing &w, int g, int64_t first,
   RingRef RH;
   RH.arcs = P.arc + abase(P.csr_off, n); RH.vs = P.vert + vbase(P.csr_off, n);
   RH.ox = on.x; RH.oy = on.y; RH.oz = on.z; RH.cnt = H.y;
-  // hole entries: (arc_fwd, cum) as in loop entries
+  // hole entries (arc_fwd, cum) in the loop-entry slots of ring 0
   const HoleEnt *he = P.hole_ent + hebase(P.csr_off, n) + H.x;
+  __syncwarp();
   if (lane < H.y) {
     HoleEnt E = he[lane];
-    const int N = le_N(E.arc_fwd), a = le_arc(E.arc_fwd);
-    w.cum[0][lane] = E.cum; w.nf[0][lane] = N | (le_fwd(E.arc_fwd) << 16); w.ax[0][lane] = a;
-    w.stp[0][lane] = __fdividef(__ldg(&RH.arcs[a].dt), (float)N);
+    LoopRec L;
+    L.arc_fwd = E.arc_fwd; L.phs = 0.0f; L.dph = 0.0f; L.cum = E.cum;
+    w.le[0][lane] = L;
   }
   __syncwarp();
   {
     const int nq = (H.y < MAXRA ? H.y : MAXRA) * 3;
     float4 *dst = reinterpret_cast<float4 *>(w.arc[0]);
-    for (int k = lane; k < nq; k += 32) dst[k] = __ldg(reinterpret_cast<const float4 *>(RH.arcs + w.ax[0][k / 3]) + (k % 3));
+    for (int k = lane; k < nq; k += 32) dst[k] = __ldg(reinterpret_cast<const float4 *>(RH.arcs + le_arc(w.le[0][k / 3].arc_fwd)) + (k % 3));
   }
   __syncwarp();
   const int mb = (int)(ta - hb), me = (int)(tb - hb);
@@ -761,8 +772,7 @@ __device__ void emit_hole(const TriParams &P, WarpRing &w, int g, int64_t first,
     const int m1 = m0 + WIN < me ? m0 + WIN : me;
     for (int k = lane; k <= m1 - m0; k += 32) {
       int idx = m0 + k;
-      f3 p = ring_point(w, 0, RH, idx >= M ? idx - M : idx);
-      w.px[k] = p.x; w.py[k] = p.y; w.pz[k] = p.z;
+      put_point(w, k, ring_point(w, 0, RH, idx >= M ? idx - M : idx));
     }
     __syncwarp();
     for (int mm = m0; mm < m1; mm += 32) {
@@ -770,7 +780,7 @@ __device__ void emit_hole(const TriParams &P, WarpRing &w, int g, int64_t first,
       if (m < m1) {
         int k = m - m0;
         uint32_t f[12];
-        tri_words(bp, F3(w.px[k], w.py[k], w.pz[k]), F3(w.px[k + 1], w.py[k + 1], w.pz[k + 1]), f);
+        tri_words(bp, get_point(w, k), get_point(w, k + 1), f);
         put_rec16(out + (hb + m - first) * REC, f);
       }
     }
@@ -778,47 +788,40 @@ __device__ void emit_hole(const TriParams &P, WarpRing &w, int g, int64_t first,
   }
 }
 
-__device__ __forceinline__ int64_t upper_bound64(const int64_t *a, int64_t lo, int64_t hi, int64_t x) {
-  while (lo < hi) {
-    int64_t m = (lo + hi) >> 1;
-    if (__ldg(&a[m]) <= x) lo = m + 1; else hi = m;
-  }
-  return lo;
-}
-
 // units: bands [s0, s1) then holes [g0, g1) intersecting [first, last)
 __global__ void __launch_bounds__(EMIT_T, 7) k_emit(TriParams P, int64_t first, int64_t count, unsigned char *out,
                                                  int64_t s0, int64_t s1, int64_t g0, int64_t g1) {
   extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ BandHdr hdr[EW][2];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   WarpRing &w = reinterpret_cast<WarpRing *>(smem)[warp];
   const int64_t last = first + count;
   const int64_t gw = (int64_t)blockIdx.x * EW + warp, nw = (int64_t)gridDim.x * EW;
   const int64_t nb = s1 - s0, nh = g1 - g0;
-  __shared__ BandHdr hdr[EW][2];
   int cb = 0;
-  if (gw < nb) {
-    hdr_l1(P, (int)(s0 + gw), hdr[warp][0], lane);
-    cp_async_wait_all();
-    __syncwarp();
-    hdr_l2(P, hdr[warp][0], lane);
-    cp_async_wait_all();
-    __syncwarp();
+  if (gw < nb) {   // first band: all four stages up front
+    fetch_hdr(P, (int)(s0 + gw), hdr[warp][0], lane);
+    cp_async_wait_warp();
+    fetch_ends(P, hdr[warp][0], lane);
+    cp_async_wait_warp();
+    fetch_entries(P, w, hdr[warp][0], lane);
+    cp_async_wait_warp();
+    fetch_arcs(P, w, hdr[warp][0], lane);
+    cp_async_wait_warp();
   }
   for (int64_t u = gw; u < nb + nh; u += nw) {
     if (u < nb) {
       const bool more = u + nw < nb;
       BandHdr &nx = hdr[warp][cb ^ 1];
-      if (more) hdr_l1(P, (int)(s0 + u + nw), nx, lane);
-      emit_band(P, w, hdr[warp][cb], first, last, out, lane, [&] {
-        if (more) {
-          cp_async_wait_all();
-          __syncwarp();
-          hdr_l2(P, nx, lane);
-        }
+      if (more) fetch_hdr(P, (int)(s0 + u + nw), nx, lane);
+      emit_band(P, w, hdr[warp][cb], first, last, out, lane, [&](int stage) {
+        if (!more) return;
+        cp_async_wait_warp();
+        if (stage == 1) fetch_ends(P, nx, lane);
+        else if (stage == 2) fetch_entries(P, w, nx, lane);
+        else fetch_arcs(P, w, nx, lane);
       });
-      cp_async_wait_all();
-      __syncwarp();
+      cp_async_wait_warp();
       cb ^= 1;
     } else emit_hole(P, w, (int)(g0 + u - nb), first, last, out, lane);
   }
