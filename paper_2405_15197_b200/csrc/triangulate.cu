@@ -562,6 +562,18 @@ __device__ void emit_band_whole(const TriParams &P, WarpRing &w, const RingRef &
   const int64_t w0 = base >> 5;
   const int nwd = (int)(((base + nA + nB - 1) >> 5) - w0 + 1);
   const uint32_t mword = lane < nwd ? __ldg(&P.mbits[w0 + lane]) : 0u;
+  // entry start vertices: loads issued before the formula pass, stored after it
+  float4 vq[2];
+#pragma unroll
+  for (int r = 0; r < 2; r++) {
+    const RingRef &R = r ? RB : RA;
+    vq[r] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (lane < R.cnt) {
+      const uint32_t ids = w.arc[r][lane].ids;
+      const int v = le_fwd(w.le[r][lane].arc_fwd) ? (ids >> 16) & 0xff : (ids >> 24);
+      vq[r] = __ldg(&R.vs[v]);
+    }
+  }
   {
     const int cA = (lane >= 1 && lane < RA.cnt) ? w.le[0][lane].cum : 0x7fffffff;
     const int cB = lane < RB.cnt ? nA + w.le[1][lane].cum : 0x7fffffff;
@@ -591,12 +603,9 @@ __device__ void emit_band_whole(const TriParams &P, WarpRing &w, const RingRef &
     for (int r = 0; r < 2; r++) {
       const RingRef &R = r ? RB : RA;
       if (lane < R.cnt) {
-        const LoopRec L = w.le[r][lane];
-        const uint32_t ids = w.arc[r][lane].ids;
-        const int v = le_fwd(L.arc_fwd) ? (ids >> 16) & 0xff : (ids >> 24);
-        const float4 q = __ldg(&R.vs[v]);
+        const float4 q = vq[r];
         const f3 p = F3(R.ox + q.x, R.oy + q.y, R.oz + q.z);
-        const int idx = L.cum;
+        const int idx = w.le[r][lane].cum;
         if (r == 0) {
           put_point(w, idx, p);
           if (idx == 0) put_point(w, nA, p);
@@ -662,7 +671,7 @@ __device__ void emit_band(const TriParams &P, WarpRing &w, const BandHdr &H, int
   const int nA = bd.x, nB = bd.y, kB = bd.z;
   const int64_t ta = base > first ? base : first;
   const int64_t tb = base + nA + nB < last ? base + nA + nB : last;
-  if (ta >= tb) { prefetch(1); prefetch(2); prefetch(3); return; }
+  if (ta >= tb) { prefetch(0); prefetch(1); prefetch(2); prefetch(3); return; }
   const int2 e = H.e, LA = H.LA, LB = H.LB;
   const int offA = H.offA, offB = H.offB;
   const float4 oa = H.oa, ob = H.ob;
@@ -674,6 +683,7 @@ __device__ void emit_band(const TriParams &P, WarpRing &w, const BandHdr &H, int
   RB.vs = P.vert + slab_base(offB, e.y, SLAB_V_K, SLAB_V_K0);
   RB.ox = ob.x; RB.oy = ob.y; RB.oz = ob.z; RB.cnt = LB.y;
   const int qb = (int)(ta - base), qe = (int)(tb - base);
+  prefetch(0);
   if (nA + nB + 2 <= PMAX && RA.cnt <= MAXRA && RB.cnt <= MAXRA) {
     emit_band_whole(P, w, RA, RB, base, nA, nB, kB, qb, qe, first, out, lane, prefetch);
     return;
@@ -792,14 +802,16 @@ __device__ void emit_hole(const TriParams &P, WarpRing &w, int g, int64_t first,
 __global__ void __launch_bounds__(EMIT_T, 7) k_emit(TriParams P, int64_t first, int64_t count, unsigned char *out,
                                                  int64_t s0, int64_t s1, int64_t g0, int64_t g1) {
   extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ BandHdr hdr[EW][2];
+  __shared__ BandHdr hdr[EW][3];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   WarpRing &w = reinterpret_cast<WarpRing *>(smem)[warp];
   const int64_t last = first + count;
   const int64_t gw = (int64_t)blockIdx.x * EW + warp, nw = (int64_t)gridDim.x * EW;
   const int64_t nb = s1 - s0, nh = g1 - g0;
+  // band u+nw: header at band u-nw's start, loop headers/centres at band u's start, entries
+  // after band u's points, arc records after its first group
   int cb = 0;
-  if (gw < nb) {   // first band: all four stages up front
+  if (gw < nb) {   // first band: all stages up front, the second band's header too
     fetch_hdr(P, (int)(s0 + gw), hdr[warp][0], lane);
     cp_async_wait_warp();
     fetch_ends(P, hdr[warp][0], lane);
@@ -807,22 +819,27 @@ __global__ void __launch_bounds__(EMIT_T, 7) k_emit(TriParams P, int64_t first, 
     fetch_entries(P, w, hdr[warp][0], lane);
     cp_async_wait_warp();
     fetch_arcs(P, w, hdr[warp][0], lane);
+    if (gw + nw < nb) fetch_hdr(P, (int)(s0 + gw + nw), hdr[warp][1], lane);
     cp_async_wait_warp();
   }
   for (int64_t u = gw; u < nb + nh; u += nw) {
     if (u < nb) {
-      const bool more = u + nw < nb;
-      BandHdr &nx = hdr[warp][cb ^ 1];
-      if (more) fetch_hdr(P, (int)(s0 + u + nw), nx, lane);
+      const bool more = u + nw < nb, more2 = u + 2 * nw < nb;
+      BandHdr &nx = hdr[warp][cb == 2 ? 0 : cb + 1];
+      BandHdr &nx2 = hdr[warp][cb == 0 ? 2 : cb - 1];
       emit_band(P, w, hdr[warp][cb], first, last, out, lane, [&](int stage) {
+        if (stage == 0) {
+          if (more) fetch_ends(P, nx, lane);
+          if (more2) fetch_hdr(P, (int)(s0 + u + 2 * nw), nx2, lane);
+          return;
+        }
         if (!more) return;
         cp_async_wait_warp();
-        if (stage == 1) fetch_ends(P, nx, lane);
-        else if (stage == 2) fetch_entries(P, w, nx, lane);
-        else fetch_arcs(P, w, nx, lane);
+        if (stage == 1) fetch_entries(P, w, nx, lane);
+        else if (stage == 2) fetch_arcs(P, w, nx, lane);
       });
       cp_async_wait_warp();
-      cb ^= 1;
+      cb = cb == 2 ? 0 : cb + 1;
     } else emit_hole(P, w, (int)(g0 + u - nb), first, last, out, lane);
   }
 }
