@@ -61,6 +61,8 @@ struct lmm_ctx {
   // scratch
   DevBuf tmp64;      // int64 scan scratch
   DevBuf scratch;    // misc
+  DevBuf mm_side;    // float4 [2S][5] side records between the meta-mesh parts
+  DevBuf mm_state;   // int4 [N] node state between the meta-mesh parts
   DevBuf scan_tmp;   // scan tile sums (all recursion levels)
   int64_t *pinned_scalar = nullptr;   // pinned host words for scan totals / flags
   unsigned long long *pinned_hist = nullptr;   // pinned degree histogram + bucket bases

@@ -46,10 +46,15 @@ struct MMParams {
   LoopRec *loop;
   int2 *hole_hdr;
   HoleEnt *hole_ent;
+  float4 *side;    // [2S][5] side records between the parts (csr entry order)
+  int4 *state;     // [N] status, clusters, vertices, arcs between the parts
 };
 
-template <int MAXS, int MAXJ, int MAXV, int MAXA, int MAXLE, int MAXH>
-struct alignas(16) NodeWS {
+// Per-warp shared-memory workspaces.  The meta-mesh of a node is built by three kernels
+// (A: sides, junctions, vertex clusters; B: arcs; C: loops, holes, slab write) so that each
+// kernel's code fits the instruction caches; every part keeps the sides and vertices.
+template <int MAXS, int MAXV>
+struct alignas(16) WSCore {
   // sides: 0 = nodal sphere, 1..d = incident struts in ascending strut id;
   // w4[k] = (w_k, e_k) of h_k(y) = w_k . y - e_k, one 16-byte load per side test
   float4 w4[MAXS];
@@ -58,19 +63,38 @@ struct alignas(16) NodeWS {
   float e1x[MAXS], e1y[MAXS], e1z[MAXS];
   float e2x[MAXS], e2y[MAXS], e2z[MAXS];
   int sign[MAXS];
-  // junctions
-  float jx[MAXJ], jy[MAXJ], jz[MAXJ];
-  uint32_t jabc[MAXJ];
-  int jlab[MAXJ], jcid[MAXJ];
   // vertices: clusters then seams
   float vx[MAXV], vy[MAXV], vz[MAXV];
   uint32_t vmask[MAXV];
+};
+
+template <int MAXS, int MAXJ, int MAXV, int MAXA, int MAXLE, int MAXH>
+struct alignas(16) WS_A : WSCore<MAXS, MAXV> {
+  float jx[MAXJ], jy[MAXJ], jz[MAXJ];
+  uint32_t jabc[MAXJ];
+  int jlab[MAXJ], jcid[MAXJ];
+};
+
+constexpr int QL = 3;   // arc-interval midpoints queued per lane and round (part B)
+
+template <int MAXS, int MAXJ, int MAXV, int MAXA, int MAXLE, int MAXH>
+struct alignas(16) WS_B : WSCore<MAXS, MAXV> {
   ArcRec arcs[MAXA];
   float atmid[MAXA];
   int adrop[MAXA];
-  // arc walk: active side pairs, each with the mask of the clusters holding both sides
+  // active side pairs, each with the mask of the clusters holding both sides
   unsigned long long pmask[MAXS * (MAXS - 1) / 2];
   int plist[MAXS * (MAXS - 1) / 2];
+  // queued interval midpoints
+  float qx[32 * QL], qy[32 * QL], qz[32 * QL];
+  int qt[32 * QL];
+  uint32_t qm[32 * QL];
+  int qok[32 * QL];
+};
+
+template <int MAXS, int MAXJ, int MAXV, int MAXA, int MAXLE, int MAXH>
+struct alignas(16) WS_C : WSCore<MAXS, MAXV> {
+  ArcRec arcs[MAXA];
   // loop entries of every (arc, side): phi start, span, forward flag
   float eps[2 * MAXA], edp[2 * MAXA];
   uint8_t efw[2 * MAXA];
@@ -278,10 +302,58 @@ __device__ __forceinline__ int rank2(int a, int b, int n) {
   return a * (2 * n - a - 1) / 2 + (b - a - 1);
 }
 
-template <int G, int MAXS, int MAXJ, int MAXV, int MAXA, int MAXLE, int MAXH>
-__device__ void process_node(cg::thread_block_tile<G> &g, NodeWS<MAXS, MAXJ, MAXV, MAXA, MAXLE, MAXH> &ws,
-                             const MMParams &P, int n) {
-  using WS = NodeWS<MAXS, MAXJ, MAXV, MAXA, MAXLE, MAXH>;
+// side records between the parts: 5 float4 per CSR entry
+template <int G, class WS>
+__device__ void store_sides(cg::thread_block_tile<G> &g, const WS &ws, float4 *side, int off, int d) {
+  #pragma unroll 1
+  for (int idx = g.thread_rank(); idx < d; idx += G) {
+    const int k = idx + 1;
+    float4 *r = side + 5 * (int64_t)(off + idx);
+    r[0] = ws.w4[k];
+    r[1] = make_float4(ws.ux[k], ws.uy[k], ws.uz[k], ws.s[k]);
+    r[2] = make_float4(ws.asx[k], ws.asy[k], ws.asz[k], ws.c[k]);
+    r[3] = make_float4(ws.e1x[k], ws.e1y[k], ws.e1z[k], ws.L[k]);
+    r[4] = make_float4(ws.e2x[k], ws.e2y[k], ws.e2z[k], __int_as_float(ws.sign[k]));
+  }
+}
+template <int G, class WS>
+__device__ void load_sides(cg::thread_block_tile<G> &g, WS &ws, const float4 *side, int off, int d) {
+  if (g.thread_rank() == 0) ws.w4[0] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+  #pragma unroll 1
+  for (int idx = g.thread_rank(); idx < d; idx += G) {
+    const int k = idx + 1;
+    const float4 *r = side + 5 * (int64_t)(off + idx);
+    const float4 r0 = r[0], r1 = r[1], r2 = r[2], r3 = r[3], r4 = r[4];
+    ws.w4[k] = r0;
+    ws.ux[k] = r1.x; ws.uy[k] = r1.y; ws.uz[k] = r1.z; ws.s[k] = r1.w;
+    ws.asx[k] = r2.x; ws.asy[k] = r2.y; ws.asz[k] = r2.z; ws.c[k] = r2.w;
+    ws.e1x[k] = r3.x; ws.e1y[k] = r3.y; ws.e1z[k] = r3.z; ws.L[k] = r3.w;
+    ws.e2x[k] = r4.x; ws.e2y[k] = r4.y; ws.e2z[k] = r4.z; ws.sign[k] = __float_as_int(r4.w);
+  }
+}
+template <int G, class WS>
+__device__ void store_verts(cg::thread_block_tile<G> &g, const WS &ws, float4 *vert, int q0, int q1) {
+  #pragma unroll 1
+  for (int q = q0 + g.thread_rank(); q < q1; q += G) vert[q] = make_float4(ws.vx[q], ws.vy[q], ws.vz[q], __uint_as_float(ws.vmask[q]));
+}
+template <int G, class WS>
+__device__ void load_verts(cg::thread_block_tile<G> &g, WS &ws, const float4 *vert, int nv) {
+  #pragma unroll 1
+  for (int q = g.thread_rank(); q < nv; q += G) {
+    const float4 v = vert[q];
+    ws.vx[q] = v.x; ws.vy[q] = v.y; ws.vz[q] = v.z; ws.vmask[q] = __float_as_uint(v.w);
+  }
+}
+template <int G>
+__device__ void copy_arcs(cg::thread_block_tile<G> &g, ArcRec *dst, const ArcRec *src, int na) {
+  const float4 *s4 = reinterpret_cast<const float4 *>(src);
+  float4 *d4 = reinterpret_cast<float4 *>(dst);
+  #pragma unroll 1
+  for (int q = g.thread_rank(); q < na * 3; q += G) d4[q] = s4[q];
+}
+
+template <int G, int MAXS, int MAXJ, int MAXV, int MAXA, int MAXLE, int MAXH, class WS>
+__device__ void part_a(cg::thread_block_tile<G> &g, WS &ws, const MMParams &P, int n) {
   const int lane = g.thread_rank();
   const int off = P.csr_off[n];
   const int d = P.csr_off[n + 1] - off;
@@ -289,8 +361,8 @@ __device__ void process_node(cg::thread_block_tile<G> &g, NodeWS<MAXS, MAXJ, MAX
   Node<WS> nd{ws, d, on.w};
   const float R = on.w;
   const float delta = LMM_TOL_REL * R, dc = LMM_CTOL_REL * R;
+  (void)dc;
   int status = 0;
-
 #ifdef LMM_PHASE_TIMING
   long long ph_t = clock64();
 #define PHASE_MARK(k)                                                    \
@@ -466,6 +538,48 @@ __device__ void process_node(cg::thread_block_tile<G> &g, NodeWS<MAXS, MAXJ, MAX
   g.sync();
 
   PHASE_MARK(3);
+  // vertices to their slab, sides to the side records, state for part B
+  if (status == 0 && nc > slab_cap(d, SLAB_V_K, SLAB_V_K0)) status = LMM_NODE_ACAP;
+  if (status == 0) {
+    store_sides<G>(g, ws, P.side, off, d);
+    store_verts<G>(g, ws, P.vert + slab_base(off, n, SLAB_V_K, SLAB_V_K0), 0, nc);
+  }
+  if (lane == 0) P.state[n] = make_int4(status, nc, nc, 0);
+  (void)nj; (void)na; (void)nle; (void)nh; (void)nhe;
+  g.sync();
+}
+
+template <int G, int MAXS, int MAXJ, int MAXV, int MAXA, int MAXLE, int MAXH, class WS>
+__device__ void part_b(cg::thread_block_tile<G> &g, WS &ws, const MMParams &P, int n) {
+  const int lane = g.thread_rank();
+  const int off = P.csr_off[n];
+  const int d = P.csr_off[n + 1] - off;
+  const float4 on = P.node[n];
+  Node<WS> nd{ws, d, on.w};
+  const float R = on.w;
+  const float delta = LMM_TOL_REL * R, dc = LMM_CTOL_REL * R;
+  (void)dc;
+  const int4 st = P.state[n];
+  int status = st.x;
+  if (status != 0) return;
+  const int nc = st.y;
+  int nv = st.z, na = 0;
+  const int ns = d + 1;
+  float4 *vslab = P.vert + slab_base(off, n, SLAB_V_K, SLAB_V_K0);
+  load_sides<G>(g, ws, P.side, off, d);
+  load_verts<G>(g, ws, vslab, nv);
+  g.sync();
+#ifdef LMM_PHASE_TIMING
+  long long ph_t = clock64();
+#define PHASE_MARK(k)                                                    \
+  do {                                                                   \
+    long long ph_n = clock64();                                          \
+    if (lane == 0) atomicAdd(&g_phase_cycles[(k) - 1], (unsigned long long)(ph_n - ph_t)); \
+    ph_t = ph_n;                                                         \
+  } while (0)
+#else
+#define PHASE_MARK(k) do { } while (0)
+#endif
   // ---- 4. arcs: conics walked through their vertices, incidence-driven --------------
   // Each side pair collects the clusters whose tie set holds both sides (a bit mask);
   // the pairs with vertices -- plus pairs of sides that appear in no vertex (only these
@@ -502,11 +616,10 @@ __device__ void process_node(cg::thread_block_tile<G> &g, NodeWS<MAXS, MAXJ, MAX
       }
       g.sync();
       PHASE_MARK(9);
-      constexpr int QL = MAXJ / G;
-      float *qx = ws.jx, *qy = ws.jy, *qz = ws.jz;
-      int *qt = ws.jlab;        // tangent length at the midpoint, float bits
-      uint32_t *qm = ws.jabc;   // side mask | sphere-point flag << 31
-      int *qok = ws.jcid;
+      float *qx = ws.qx, *qy = ws.qy, *qz = ws.qz;
+      int *qt = ws.qt;          // tangent length at the midpoint, float bits
+      uint32_t *qm = ws.qm;     // side mask | sphere-point flag << 31
+      int *qok = ws.qok;
       #pragma unroll 1
       for (int base = 0; base < nact; base += G) {
         int k = base + lane;
@@ -693,7 +806,47 @@ __device__ void process_node(cg::thread_block_tile<G> &g, NodeWS<MAXS, MAXJ, MAX
     if (g.any(e != 0)) status = LMM_NODE_UNREF;
   }
 
-  PHASE_MARK(5);
+  // seam vertices and arcs to their slabs, state for part C
+  if (status == 0 && (nv > slab_cap(d, SLAB_V_K, SLAB_V_K0) || na > slab_cap(d, SLAB_A_K, SLAB_A_K0)))
+    status = LMM_NODE_ACAP;
+  if (status == 0) {
+    store_verts<G>(g, ws, vslab, nc, nv);
+    copy_arcs<G>(g, P.arc + slab_base(off, n, SLAB_A_K, SLAB_A_K0), ws.arcs, na);
+  }
+  if (lane == 0) P.state[n] = make_int4(status, nc, nv, na);
+  g.sync();
+}
+
+template <int G, int MAXS, int MAXJ, int MAXV, int MAXA, int MAXLE, int MAXH, class WS>
+__device__ void part_c(cg::thread_block_tile<G> &g, WS &ws, const MMParams &P, int n) {
+  const int lane = g.thread_rank();
+  const int off = P.csr_off[n];
+  const int d = P.csr_off[n + 1] - off;
+  const float4 on = P.node[n];
+  Node<WS> nd{ws, d, on.w};
+  const float R = on.w;
+  const float delta = LMM_TOL_REL * R, dc = LMM_CTOL_REL * R;
+  (void)dc;
+  const int4 st = P.state[n];
+  int status = st.x;
+  int nv = status == 0 ? st.z : 0, na = status == 0 ? st.w : 0, nle = 0, nh = 0, nhe = 0;
+  if (status == 0) {
+    load_sides<G>(g, ws, P.side, off, d);
+    load_verts<G>(g, ws, P.vert + slab_base(off, n, SLAB_V_K, SLAB_V_K0), nv);
+    copy_arcs<G>(g, ws.arcs, P.arc + slab_base(off, n, SLAB_A_K, SLAB_A_K0), na);
+  }
+  g.sync();
+#ifdef LMM_PHASE_TIMING
+  long long ph_t = clock64();
+#define PHASE_MARK(k)                                                    \
+  do {                                                                   \
+    long long ph_n = clock64();                                          \
+    if (lane == 0) atomicAdd(&g_phase_cycles[(k) - 1], (unsigned long long)(ph_n - ph_t)); \
+    ph_t = ph_n;                                                         \
+  } while (0)
+#else
+#define PHASE_MARK(k) do { } while (0)
+#endif
   // ---- 5. arc loops per strut end (ordered by angle around the strut axis) -----------
   if (status == 0 && d > 0) {
     // 5a: loop-entry data of every (arc, strut side), lanes over arcs
@@ -870,19 +1023,9 @@ __device__ void process_node(cg::thread_block_tile<G> &g, NodeWS<MAXS, MAXJ, MAX
   if (status != 0) { nv = na = nle = nh = nhe = 0; }
   if (lane == 0)
     P.node_hdr[n] = make_int4(status | (d << 8), nv | (na << 16), nh | (nle << 16), nhe);
-  const int64_t vb = slab_base(off, n, SLAB_V_K, SLAB_V_K0);
-  const int64_t ab = slab_base(off, n, SLAB_A_K, SLAB_A_K0);
   const int64_t lb = slab_base(off, n, SLAB_L_K, SLAB_L_K0);
   const int64_t hb = slab_base(off, n, SLAB_H_K, SLAB_H_K0);
   const int64_t heb = slab_base(off, n, SLAB_HE_K, SLAB_HE_K0);
-  #pragma unroll 1
-  for (int q = lane; q < nv; q += G) P.vert[vb + q] = make_float4(ws.vx[q], ws.vy[q], ws.vz[q], __uint_as_float(ws.vmask[q]));
-  {
-    const uint32_t *src = reinterpret_cast<const uint32_t *>(ws.arcs);
-    uint32_t *dst = reinterpret_cast<uint32_t *>(P.arc + ab);
-    #pragma unroll 1
-    for (int q = lane; q < na * 12; q += G) dst[q] = src[q];
-  }
   #pragma unroll 1
   for (int q = lane; q < nle; q += G) P.loop[lb + q] = ws.le[q];
   #pragma unroll 1
@@ -896,9 +1039,18 @@ __device__ void process_node(cg::thread_block_tile<G> &g, NodeWS<MAXS, MAXJ, MAX
   g.sync();
 }
 
+template <int PART, int G, int MAXS, int MAXJ, int MAXV, int MAXA, int MAXLE, int MAXH>
+struct PartWS;
 template <int G, int MAXS, int MAXJ, int MAXV, int MAXA, int MAXLE, int MAXH>
+struct PartWS<0, G, MAXS, MAXJ, MAXV, MAXA, MAXLE, MAXH> { using T = WS_A<MAXS, MAXJ, MAXV, MAXA, MAXLE, MAXH>; };
+template <int G, int MAXS, int MAXJ, int MAXV, int MAXA, int MAXLE, int MAXH>
+struct PartWS<1, G, MAXS, MAXJ, MAXV, MAXA, MAXLE, MAXH> { using T = WS_B<MAXS, MAXJ, MAXV, MAXA, MAXLE, MAXH>; };
+template <int G, int MAXS, int MAXJ, int MAXV, int MAXA, int MAXLE, int MAXH>
+struct PartWS<2, G, MAXS, MAXJ, MAXV, MAXA, MAXLE, MAXH> { using T = WS_C<MAXS, MAXJ, MAXV, MAXA, MAXLE, MAXH>; };
+
+template <int PART, int G, int MAXS, int MAXJ, int MAXV, int MAXA, int MAXLE, int MAXH>
 __global__ void __launch_bounds__(128) metamesh_kernel(MMParams P) {
-  using WS = NodeWS<MAXS, MAXJ, MAXV, MAXA, MAXLE, MAXH>;
+  using WS = typename PartWS<PART, G, MAXS, MAXJ, MAXV, MAXA, MAXLE, MAXH>::T;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   auto block = cg::this_thread_block();
   cg::thread_block_tile<G> g = cg::tiled_partition<G>(block);
@@ -907,7 +1059,11 @@ __global__ void __launch_bounds__(128) metamesh_kernel(MMParams P) {
   const int groups_per_block = blockDim.x / G;
   const int gid = blockIdx.x * groups_per_block + gid_in_block;
   const int ngroups = gridDim.x * groups_per_block;
-  for (int i = gid; i < P.n_list; i += ngroups) process_node<G>(g, ws, P, P.node_list[i]);
+  for (int i = gid; i < P.n_list; i += ngroups) {
+    if constexpr (PART == 0) part_a<G, MAXS, MAXJ, MAXV, MAXA, MAXLE, MAXH>(g, ws, P, P.node_list[i]);
+    else if constexpr (PART == 1) part_b<G, MAXS, MAXJ, MAXV, MAXA, MAXLE, MAXH>(g, ws, P, P.node_list[i]);
+    else part_c<G, MAXS, MAXJ, MAXV, MAXA, MAXLE, MAXH>(g, ws, P, P.node_list[i]);
+  }
 }
 
 // nodes of degree 0 or > LMM_MAXD
@@ -922,14 +1078,13 @@ __global__ void trivial_nodes_kernel(const int *csr_off, int N, int4 *node_hdr, 
   }
 }
 
-template <int G, int MAXS, int MAXJ, int MAXV, int MAXA, int MAXLE, int MAXH>
-int launch_bucket(lmm_ctx *c, MMParams P) {
-  using WS = NodeWS<MAXS, MAXJ, MAXV, MAXA, MAXLE, MAXH>;
-  if (P.n_list <= 0) return LMM_OK;
+template <int PART, int G, int MAXS, int MAXJ, int MAXV, int MAXA, int MAXLE, int MAXH>
+int launch_part(lmm_ctx *c, const MMParams &P) {
+  using WS = typename PartWS<PART, G, MAXS, MAXJ, MAXV, MAXA, MAXLE, MAXH>::T;
   const int threads = 128;
   const int groups = threads / G;
   size_t smem = sizeof(WS) * groups;
-  auto kern = metamesh_kernel<G, MAXS, MAXJ, MAXV, MAXA, MAXLE, MAXH>;
+  auto kern = metamesh_kernel<PART, G, MAXS, MAXJ, MAXV, MAXA, MAXLE, MAXH>;
   CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 0;
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem));
@@ -942,14 +1097,29 @@ int launch_bucket(lmm_ctx *c, MMParams P) {
   return LMM_OK;
 }
 
+template <int G, int MAXS, int MAXJ, int MAXV, int MAXA, int MAXLE, int MAXH>
+int launch_bucket(lmm_ctx *c, MMParams P) {
+  if (P.n_list <= 0) return LMM_OK;
+  int rc;
+  if ((rc = launch_part<0, G, MAXS, MAXJ, MAXV, MAXA, MAXLE, MAXH>(c, P))) return rc;
+  if ((rc = launch_part<1, G, MAXS, MAXJ, MAXV, MAXA, MAXLE, MAXH>(c, P))) return rc;
+  return launch_part<2, G, MAXS, MAXJ, MAXV, MAXA, MAXLE, MAXH>(c, P);
+}
+
 }  // namespace
 
 #ifdef LMM_PHASE_TIMING
-extern "C" LMM_API int lmm_debug_ws_bytes(int bucket) {
-  switch (bucket) {
-    case 0: return (int)sizeof(NodeWS<LMM_B0_ARGS>);
-    case 1: return (int)sizeof(NodeWS<LMM_B1_ARGS>);
-    default: return (int)sizeof(NodeWS<LMM_B2_ARGS>);
+extern "C" LMM_API int lmm_debug_ws_bytes(int bucket, int part) {
+  switch (bucket * 3 + part) {
+    case 0: return (int)sizeof(WS_A<LMM_B0_ARGS>);
+    case 1: return (int)sizeof(WS_B<LMM_B0_ARGS>);
+    case 2: return (int)sizeof(WS_C<LMM_B0_ARGS>);
+    case 3: return (int)sizeof(WS_A<LMM_B1_ARGS>);
+    case 4: return (int)sizeof(WS_B<LMM_B1_ARGS>);
+    case 5: return (int)sizeof(WS_C<LMM_B1_ARGS>);
+    case 6: return (int)sizeof(WS_A<LMM_B2_ARGS>);
+    case 7: return (int)sizeof(WS_B<LMM_B2_ARGS>);
+    default: return (int)sizeof(WS_C<LMM_B2_ARGS>);
   }
 }
 #endif
@@ -967,6 +1137,13 @@ int metamesh_run(lmm_ctx *c) {
   P.loop = (LoopRec *)c->loop.p;
   P.hole_hdr = (int2 *)c->hole_hdr.p;
   P.hole_ent = (HoleEnt *)c->hole_ent.p;
+  {
+    int rc0;
+    if ((rc0 = dev_alloc(c->mm_side, sizeof(float4) * 5 * (2 * c->S + 1)))) return rc0;
+    if ((rc0 = dev_alloc(c->mm_state, sizeof(int4) * (c->N + 1)))) return rc0;
+  }
+  P.side = (float4 *)c->mm_side.p;
+  P.state = (int4 *)c->mm_state.p;
   const int *bn = (const int *)c->bucket_nodes.p;
   int rc;
   {
