@@ -61,6 +61,7 @@ struct lmm_ctx {
   // scratch
   DevBuf tmp64;      // int64 scan scratch
   DevBuf scratch;    // misc
+  DevBuf tri3;       // uint32 lexicographic triple table (meta-mesh junction enumeration)
   DevBuf mm_side;    // float4 [2S][5] side records between the meta-mesh parts
   DevBuf mm_state;   // int4 [N] node state between the meta-mesh parts
   DevBuf scan_tmp;   // scan tile sums (all recursion levels)

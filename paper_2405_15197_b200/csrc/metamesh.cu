@@ -46,6 +46,7 @@ struct MMParams {
   LoopRec *loop;
   int2 *hole_hdr;
   HoleEnt *hole_ent;
+  const uint32_t *tri3;   // lexicographic triples a | b << 8 | c << 16 of n sides at C(n,4)
   float4 *side;    // [2S][5] side records between the parts (csr entry order)
   int4 *state;     // [N] status, clusters, vertices, arcs between the parts
 };
@@ -70,6 +71,8 @@ struct alignas(16) WSCore {
 
 template <int MAXS, int MAXJ, int MAXV, int MAXA, int MAXLE, int MAXH>
 struct alignas(16) WS_A : WSCore<MAXS, MAXV> {
+  // side k as broadcast pairs for the two-root junction test: (wx,wx,wy,wy), (wz,wz,-e,-e)
+  float4 wp[MAXS][2];
   float jx[MAXJ], jy[MAXJ], jz[MAXJ];
   uint32_t jabc[MAXJ];
   int jlab[MAXJ], jcid[MAXJ];
@@ -105,6 +108,24 @@ struct alignas(16) WS_C : WSCore<MAXS, MAXV> {
   int hoff[MAXH + 1];
   uint32_t he[MAXA];
 };
+
+// packed fp32 pairs (sm_100 add/mul .f32x2, round-to-nearest per lane)
+__device__ __forceinline__ unsigned long long f2u(float2 a) {
+  return (unsigned long long)__float_as_uint(a.x) | ((unsigned long long)__float_as_uint(a.y) << 32);
+}
+__device__ __forceinline__ float2 u2f(unsigned long long u) {
+  return make_float2(__uint_as_float((unsigned)u), __uint_as_float((unsigned)(u >> 32)));
+}
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
+  unsigned long long r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2u(a)), "l"(f2u(b)));
+  return u2f(r);
+}
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+  unsigned long long r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2u(a)), "l"(f2u(b)));
+  return u2f(r);
+}
 
 template <class WS> struct Node {
   WS &w;
@@ -170,18 +191,23 @@ template <class WS> struct Node {
   }
   // both roots of a triple junction in one pass over the sides: strut junctions
   // (valid_strut_pt) or, for a sphere triple (tau taken as 0; h - 0 == h exactly), the
-  // tolerant sphere-junction test "no other strut above the sphere by more than delta"
+  // tolerant sphere-junction test "no other strut above the sphere by more than delta".
+  // The two roots go through packed f32x2 operations: every lane of those rounds like the
+  // scalar op (same bits as hs(m, y) - tau), h - e as h + (-e), h - tau as h + (-tau).
   __device__ void valid_junction_pair(bool sphere, uint32_t excl, f3 y0, float t0, f3 y1, float t1, float delta,
                                       bool *ok0, bool *ok1) const {
     bool k0 = *ok0 && (sphere || !(t0 < -delta)), k1 = *ok1 && (sphere || !(t1 < -delta));
     if (sphere) { t0 = 0.0f; t1 = 0.0f; }
+    const float2 Yx = make_float2(y0.x, y1.x), Yy = make_float2(y0.y, y1.y), Yz = make_float2(y0.z, y1.z);
+    const float2 nT = make_float2(-t0, -t1);
     for (int m = 1; m <= d; m++) {
-      const float4 q = w.w4[m];
+      const float4 p0 = w.wp[m][0], p1 = w.wp[m][1];
       const bool ex = (excl >> m) & 1u;
-      const float h0 = ((q.x * y0.x + q.y * y0.y) + q.z * y0.z) - q.w;
-      const float h1 = ((q.x * y1.x + q.y * y1.y) + q.z * y1.z) - q.w;
-      k0 = k0 && (ex || !(h0 - t0 > delta));
-      k1 = k1 && (ex || !(h1 - t1 > delta));
+      float2 h = add2(mul2(make_float2(p0.x, p0.y), Yx), mul2(make_float2(p0.z, p0.w), Yy));
+      h = add2(h, mul2(make_float2(p1.x, p1.y), Yz));
+      h = add2(add2(h, make_float2(p1.z, p1.w)), nT);
+      k0 = k0 && (ex || !(h.x > delta));
+      k1 = k1 && (ex || !(h.y > delta));
     }
     *ok0 = k0; *ok1 = k1;
   }
@@ -399,7 +425,10 @@ __device__ void part_a(cg::thread_block_tile<G> &g, WS &ws, const MMParams &P, i
         else {
           float c = sqrtf(1.0f - s * s);
           f3 wv = f_div(u, c);
-          ws.w4[k] = make_float4(wv.x, wv.y, wv.z, (R * s) / c);
+          const float ek = (R * s) / c;
+          ws.w4[k] = make_float4(wv.x, wv.y, wv.z, ek);
+          ws.wp[k][0] = make_float4(wv.x, wv.x, wv.y, wv.y);
+          ws.wp[k][1] = make_float4(wv.z, wv.z, -ek, -ek);
           ws.ux[k] = u.x; ws.uy[k] = u.y; ws.uz[k] = u.z;
           ws.s[k] = s; ws.c[k] = c; ws.L[k] = Ln;
           ws.sign[k] = endbit ? -1 : 1;
@@ -427,6 +456,7 @@ __device__ void part_a(cg::thread_block_tile<G> &g, WS &ws, const MMParams &P, i
   // ---- 2. triple junctions, lexicographic (a<b<c), root-minor ---------------------
   if (status == 0 && d > 0) {
     const int ntri = ns * (ns - 1) * (ns - 2) / 6;
+    const uint32_t *t3 = P.tri3 + ns * (ns - 1) * (ns - 2) * (ns - 3) / 24;   // triples of ns sides
     #pragma unroll 1
     for (int base = 0; base < ntri; base += G) {
       int t = base + lane;
@@ -436,7 +466,8 @@ __device__ void part_a(cg::thread_block_tile<G> &g, WS &ws, const MMParams &P, i
       float tau[2];
       bool sh0 = false, sh1 = false;
       if (t < ntri) {
-        unrank3(t, ns, &a, &b, &c);
+        const uint32_t code = __ldg(&t3[t]);
+        a = code & 0xff; b = (code >> 8) & 0xff; c = code >> 16;
         if (nd.junction(a, b, c, y, tau)) {
           const uint32_t excl = (1u << a) | (1u << b) | (1u << c);
           v0 = v1 = true;
@@ -1142,6 +1173,17 @@ int metamesh_run(lmm_ctx *c) {
     if ((rc0 = dev_alloc(c->mm_side, sizeof(float4) * 5 * (2 * c->S + 1)))) return rc0;
     if ((rc0 = dev_alloc(c->mm_state, sizeof(int4) * (c->N + 1)))) return rc0;
   }
+  if (!c->tri3.p) {   // triple table for up to LMM_MAXD + 1 sides
+    std::vector<uint32_t> t3;
+    for (int n = 3; n <= LMM_MAXD + 1; n++)
+      for (int a = 0; a < n; a++)
+        for (int b = a + 1; b < n; b++)
+          for (int cc = b + 1; cc < n; cc++) t3.push_back((uint32_t)a | ((uint32_t)b << 8) | ((uint32_t)cc << 16));
+    int rc0;
+    if ((rc0 = dev_alloc(c->tri3, sizeof(uint32_t) * t3.size()))) return rc0;
+    CUDA_TRY(cudaMemcpy(c->tri3.p, t3.data(), sizeof(uint32_t) * t3.size(), cudaMemcpyHostToDevice));
+  }
+  P.tri3 = (const uint32_t *)c->tri3.p;
   P.side = (float4 *)c->mm_side.p;
   P.state = (int4 *)c->mm_state.p;
   const int *bn = (const int *)c->bucket_nodes.p;
