@@ -9,11 +9,19 @@ RAW = ["dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum"
        "smsp__thread_inst_executed.sum", "sm__warps_active.avg.pct_of_peak_sustained_active"]
 
 
+KFILTER = []
+
+
 def ncu(rep, *args):
-    return subprocess.run(["ncu", "-i", rep, *args], capture_output=True, text=True).stdout
+    return subprocess.run(["ncu", "-i", rep, *KFILTER, *args], capture_output=True, text=True).stdout
 
 
-def main(rep, out, title, units=None):
+def main(rep, out, title, units=None, kernel=None):
+    """kernel: optional ncu -k filter (e.g. 'regex:k_emit') selecting one kernel of the report."""
+    KFILTER[:] = []
+    if kernel:   # "regex:NAME" or "regex:NAME@SKIP" (SKIP-th matching launch)
+        k, _, skip = kernel.partition("@")
+        KFILTER[:] = ["-k", k, "--launch-skip", skip or "0", "--launch-count", "1"]
     det = list(csv.reader(io.StringIO(ncu(rep, "--page", "details", "--csv"))))
     hdr = det[0]
     rows = [dict(zip(hdr, r)) for r in det[1:]]
@@ -26,7 +34,8 @@ def main(rep, out, title, units=None):
     if len(sass) > 2:
         h = sass[1]
         cols = [c for c in h if c.startswith("stall_") and "Not Issued" not in c]
-        tot = {c: sum(int(r[h.index(c)] or 0) for r in sass[2:]) for c in cols}
+        body = [r for r in sass[2:] if len(r) == len(h)]
+        tot = {c: sum(int(r[h.index(c)]) if r[h.index(c)].isdigit() else 0 for r in body) for c in cols}
         T = sum(tot.values()) or 1
         stalls = {c: 100 * v / T for c, v in sorted(tot.items(), key=lambda kv: -kv[1])[:8]}
     with open(out, "w") as f:
@@ -55,4 +64,5 @@ def main(rep, out, title, units=None):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2], sys.argv[3], float(sys.argv[4]) if len(sys.argv) > 4 else None)
+    main(sys.argv[1], sys.argv[2], sys.argv[3], float(sys.argv[4]) if len(sys.argv) > 4 and sys.argv[4] else None,
+         sys.argv[5] if len(sys.argv) > 5 else None)
