@@ -145,13 +145,21 @@ def lmm_sync(h):
     _check(load_library().lmm_sync(h))
 
 
-def lmm_buffer(h, buf_id: int, dtype, cols: int | None = None) -> np.ndarray:
+def lmm_buffer(h, buf_id: int, dtype, cols: int | None = None, first: int = 0,
+               rows: int | None = None) -> np.ndarray:
+    """Host copy of an internal buffer (rows [first, first+rows) when given; a row is
+    `cols` elements of `dtype`, or one element)."""
     lib = load_library()
     n = C.c_int64()
     _check(lib.lmm_buffer_size(h, buf_id, C.byref(n)))
-    a = np.zeros(n.value // np.dtype(dtype).itemsize, dtype=dtype)
-    if n.value:
-        _check(lib.lmm_copy_buffer(h, buf_id, 0, n.value, a.ctypes.data_as(C.c_void_p)))
+    row = np.dtype(dtype).itemsize * (cols or 1)
+    total = n.value // row
+    rows = total - first if rows is None else rows
+    if first < 0 or rows < 0 or first + rows > total:
+        raise LmmError(f"buffer {buf_id}: rows [{first}, {first + rows}) outside [0, {total})")
+    a = np.zeros(rows * (cols or 1), dtype=dtype)
+    if rows:
+        _check(lib.lmm_copy_buffer(h, buf_id, first * row, rows * row, a.ctypes.data_as(C.c_void_p)))
     return a.reshape(-1, cols) if cols else a
 
 

@@ -74,6 +74,28 @@ class MetaMesher:
             hole_ent=B.lmm_buffer(h, B.LMM_BUF_HOLE_ENT, np.uint32, 2),
         )
 
+    def node_buffers(self, n: int) -> dict:
+        """The slabs of node n only (rows copied by offset), in the layout decode_node
+        expects for node index 0 -- for sampled parity checks on lattices too large to
+        copy out whole."""
+        h = self.h
+        off = B.lmm_buffer(h, B.LMM_BUF_CSR_OFF, np.int32, None, n, 2).astype(np.int64)
+        d = int(off[1] - off[0])
+
+        def slab(buf, key, dtype, cols):
+            k, k0 = B.SLAB[key]
+            return B.lmm_buffer(h, buf, dtype, cols, k * int(off[0]) + k0 * n, k * d + k0)
+        return dict(
+            csr_off=np.array([0, d], np.int32),
+            node_hdr=B.lmm_buffer(h, B.LMM_BUF_NODE_HDR, np.int32, 4, n, 1),
+            vert=slab(B.LMM_BUF_VERT, "v", np.float32, 4),
+            arc=slab(B.LMM_BUF_ARC, "a", np.uint32, 12),
+            loop_hdr=B.lmm_buffer(h, B.LMM_BUF_LOOP_HDR, np.int32, 2, int(off[0]), d),
+            loop=slab(B.LMM_BUF_LOOP_ENT, "l", np.uint32, 4),
+            hole_hdr=slab(B.LMM_BUF_HOLE_HDR, "h", np.int32, 2),
+            hole_ent=slab(B.LMM_BUF_HOLE_ENT, "he", np.uint32, 2),
+        )
+
     def tri_buffers(self) -> dict:
         h = self.h
         return dict(

@@ -1,0 +1,38 @@
+"""Shared parity assertions of the GPU tests (CUDA path vs CPU oracle, per node / per band)."""
+import numpy as np
+
+# north_star: geometry within 1e-4 x the minimum strut radius (binary32 kernel vs binary64 oracle)
+GEOM_TOL = 1e-4
+
+
+def assert_node_parity(g: dict, o: dict, tol: float, n) -> None:
+    """Topology bit-exact (counts, masks, endpoints, loop order, binary32 decision values),
+    geometry within `tol`."""
+    assert (g["status"], g["d"]) == (o["status"], o["d"]), (n, g["status"], o["status"])
+    if o["status"]:
+        return
+    assert (g["nv"], g["na"], g["nh"]) == (o["nv"], o["na"], o["nh"]), n
+    assert np.array_equal(g["v_mask"], o["v_mask"]), n
+    assert np.array_equal(g["v_pos32"].view(np.uint32), o["v_pos32"].view(np.uint32)), n
+    assert np.array_equal(g["a_int"], o["a_int"]), n
+    assert np.array_equal(g["a_f32"].view(np.uint32), o["a_f32"].view(np.uint32)), n   # t0, dt, conic (binary32)
+    assert np.array_equal(g["loop_off"], o["loop_off"]), n
+    assert np.array_equal(g["l_int"], o["l_int"]), n
+    assert np.array_equal(g["l_f32"].view(np.uint32), o["l_f32"].view(np.uint32)), n
+    assert np.array_equal(g["hole_off"], o["hole_off"]) and np.array_equal(g["h_int"], o["h_int"]), n
+    if g["nv"]:
+        assert np.max(np.abs(g["v_pos32"] - o["v_pos64"])) < tol, n
+    if g["na"]:
+        assert np.max(np.abs(g["a_f32"][:, 2:] - o["a_f64"][:, 2:])) < tol, n
+
+
+def assert_triangles_close(tri: np.ndarray, ref: np.ndarray, r_min: float, what) -> None:
+    """Triangle vertices: binary32 kernel vs binary64 oracle within 1e-4 r_min plus the
+    binary32 rounding of absolute coordinates."""
+    assert tri.shape == ref.shape, (what, tri.shape, ref.shape)
+    if len(tri) == 0:
+        return
+    tri = tri.astype(np.float64)
+    tol = GEOM_TOL * r_min + 4e-7 * np.abs(ref[:, 1:]).max()
+    err = np.max(np.abs(tri[:, 1:] - ref[:, 1:]))
+    assert err < tol, (what, err, tol)

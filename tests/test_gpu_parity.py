@@ -11,10 +11,10 @@ import pytest
 
 import oracle
 import synth
+from _parity import GEOM_TOL, assert_node_parity
 
 pytestmark = pytest.mark.gpu
 
-GEOM_TOL = 1e-4
 
 
 def _lat(name):
@@ -64,24 +64,7 @@ def test_metamesh_topology_bit_exact_and_geometry(built, name):
     lat, mm, orc, bufs = built(name)
     tol = GEOM_TOL * float(lat.node_r.min())
     for n in range(lat.n_nodes):
-        g, o = decode_node(bufs, n), orc.node(n)
-        assert (g["status"], g["d"]) == (o["status"], o["d"]), (n, g["status"], o["status"])
-        if o["status"]:
-            continue
-        assert (g["nv"], g["na"], g["nh"]) == (o["nv"], o["na"], o["nh"]), n
-        assert np.array_equal(g["v_mask"], o["v_mask"]), n
-        assert np.array_equal(g["v_pos32"].view(np.uint32), o["v_pos32"].view(np.uint32)), n
-        assert np.array_equal(g["a_int"], o["a_int"]), n
-        assert np.array_equal(g["a_f32"].view(np.uint32), o["a_f32"].view(np.uint32)), n   # t0, dt, conic (binary32)
-        assert np.array_equal(g["loop_off"], o["loop_off"]), n
-        assert np.array_equal(g["l_int"], o["l_int"]), n
-        assert np.array_equal(g["l_f32"].view(np.uint32), o["l_f32"].view(np.uint32)), n
-        assert np.array_equal(g["hole_off"], o["hole_off"]) and np.array_equal(g["h_int"], o["h_int"]), n
-        # geometry: binary32 kernel vs binary64 oracle
-        if g["nv"]:
-            assert np.max(np.abs(g["v_pos32"] - o["v_pos64"])) < tol, n
-        if g["na"]:
-            assert np.max(np.abs(g["a_f32"][:, 2:] - o["a_f64"][:, 2:])) < tol, n
+        assert_node_parity(decode_node(bufs, n), orc.node(n), tol, n)
 
 
 def _mesh_edges_ok(tris):
