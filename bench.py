@@ -47,6 +47,31 @@ def make_config(name: str, rank: int = 0, world: int = 1):
         masks = P.emit_masks(lat.ijk[:, 2], lat.ends, rank, world, k_top) if world > 1 else (None, None)
         desc = (f"octet-truss {n}x{n}x{n} cells per GPU (global {n}x{n}x{n * world}), conical struts "
                 f"(node radii graded 0.03-0.06 along x, pitch 1)")
+    elif name == "bcc250":
+        # configs[3]: the ~1B-strut BCC lattice of 8 GPUs = 8 blocks of 250^3 cells (125M struts each)
+        n = 250
+        k_top = 2 * n * world
+        k_lo, k_hi = P.window(rank, world, k_top) if world > 1 else (0, k_top)
+        lat = synth.bcc_window(n, n, n * world, k_lo, k_hi, radius=0.05)
+        masks = P.emit_masks(lat.ijk[:, 2], lat.ends, rank, world, k_top) if world > 1 else (None, None)
+        desc = (f"BCC {n}x{n}x{n} cells per GPU (global {n}x{n}x{n * world}, {8 * n ** 3 * world / 1e9:.3f}B struts), "
+                f"uniform radius 0.05, pitch 1")
+    elif name == "stoch290":
+        # configs[2]: stochastic Voronoi-style lattice, degrees 3..30, ~1e8 struts; ranks get
+        # independent lattices (seed = rank), so there is nothing to exchange
+        lat = synth.stochastic(290, seed=rank)
+        masks = (None, None)
+        desc = ("stochastic Voronoi-style lattice per GPU: jittered 290^3 grid, Zipf target degrees 3-30, "
+                "cone radii U(0.02, 0.04), >=25 deg between struts at a node (synth.stochastic, seed = rank)")
+    elif name == "octet160":
+        # configs[4]: one fixed ~100M-strut meta-mesh (octet 160^3 cells, 98.3M struts)
+        n = 160
+        k_top = 2 * n * world
+        k_lo, k_hi = P.window(rank, world, k_top) if world > 1 else (0, k_top)
+        lat = synth.octet_window(n, n, n * world, k_lo, k_hi, radius=0.03, r_max=0.06)
+        masks = P.emit_masks(lat.ijk[:, 2], lat.ends, rank, world, k_top) if world > 1 else (None, None)
+        desc = (f"octet-truss {n}x{n}x{n} cells per GPU (global {n}x{n}x{n * world}), conical struts "
+                f"(node radii graded 0.03-0.06 along x, pitch 1)")
     elif name == "bcc10":
         lat = synth.bcc(10, 10, 10)
         masks = (None, None)
@@ -116,26 +141,45 @@ def peaks():
         return 6650.0, "fallback"
 
 
-def cpu_baseline(ce: float, budget_s: float = 20.0):
+def _sample_lattice(config: str, n: int):
+    """A small lattice of the same family as `config` (for the oracle's bounded samples)."""
+    if config.startswith("bcc"):
+        return synth.bcc(n, n, n), f"bcc {n}x{n}x{n}"
+    if config.startswith("stoch"):
+        side = int(round((n ** 3 * 8) ** (1 / 3)))
+        return synth.stochastic(side, seed=0), f"stochastic {side}^3"
+    return synth.graded_radii(synth.octet(n, n, n), 0.03, 0.06, axis=0), f"octet {n}x{n}x{n} graded"
+
+
+def cpu_baseline(ce, config: str = "octet100", sweep=None, budget_s: float = 20.0):
     """The oracle as it stands, single-threaded on this host, on a bounded sample of the
-    same workload family (graded octet truss) -- a reported baseline, not the target."""
+    same workload family -- a reported baseline, not the target."""
     import oracle
     oracle.build_oracle()
+    ces = sweep or [ce]
     n = 6
     while True:
-        lat = synth.graded_radii(synth.octet(n, n, n), 0.03, 0.06, axis=0)
+        lat, name = _sample_lattice(config, n)
         t0 = time.perf_counter()
         orc = oracle.Oracle.from_lattice(lat)
-        orc.metamesh()
-        T = orc.triangulate(ce)
-        for f in range(0, T, 1 << 21):
-            orc.write_triangles(f, min(1 << 21, T - f))
+        if not sweep:
+            orc.metamesh()
+        else:
+            orc.metamesh()
+            t0 = time.perf_counter()    # sweep: the meta-mesh is built outside the timed region
+        T = 0
+        for c in ces:
+            Tc = orc.triangulate(c)
+            for f in range(0, Tc, 1 << 21):
+                orc.write_triangles(f, min(1 << 21, Tc - f))
+            T += Tc
         dt = time.perf_counter() - t0
         if dt > budget_s / 4 or n >= 24:
             break
         n = int(n * 1.5)
-    return {"value": lat.n_struts / dt, "unit": "struts/s", "cores": 1, "kind": "oracle",
-            "sample": f"octet {n}x{n}x{n} graded ({lat.n_struts} struts, {T} triangles, CE={ce}) in {dt:.1f} s",
+    v, unit = (T / dt, "triangles/s") if sweep else (lat.n_struts / dt, "struts/s")
+    return {"value": v, "unit": unit, "cores": 1, "kind": "oracle",
+            "sample": f"{name} ({lat.n_struts} struts, {T} triangles, CE={ces}) in {dt:.1f} s",
             "triangles_per_s": T / dt}
 
 
@@ -146,14 +190,23 @@ def run_reference(args):
         return
     import oracle
     oracle.build_oracle()
-    lat = synth.graded_radii(synth.octet(8, 8, 8), 0.03, 0.06, axis=0)
+    lat, name = _sample_lattice(args.config, 8)
+    sweep = [float(x) for x in args.ce_sweep.split(",") if x] if args.ce_sweep else None
+    fixed = oracle.Oracle.from_lattice(lat) if sweep else None
+    if sweep:
+        fixed.metamesh()     # the sweep re-triangulates one meta-mesh built outside the timed region
 
     def step():
-        orc = oracle.Oracle.from_lattice(lat)
-        orc.metamesh()
-        T = orc.triangulate(args.ce)
-        for f in range(0, T, 1 << 21):
-            orc.write_triangles(f, min(1 << 21, T - f))
+        orc = fixed
+        if orc is None:
+            orc = oracle.Oracle.from_lattice(lat)
+            orc.metamesh()
+        T = 0
+        for ce in sweep or [args.ce]:
+            Tc = orc.triangulate(ce)
+            for f in range(0, Tc, 1 << 21):
+                orc.write_triangles(f, min(1 << 21, Tc - f))
+            T += Tc
         return T
     for _ in range(args.warmup):
         step()
@@ -161,15 +214,15 @@ def run_reference(args):
     for _ in range(args.steps):
         T = step()
     dt = (time.perf_counter() - t0) / args.steps
-    v = lat.n_struts / dt
-    sample = f"octet 8x8x8 graded ({lat.n_struts} struts, {T} triangles) per step"
+    v, unit = (T / dt, "triangles/s") if sweep else (lat.n_struts / dt, "struts/s")
+    sample = f"{name} ({lat.n_struts} struts, {T} triangles) per step"
     print(json.dumps({
-        "impl": "reference", "metric": METRIC, "value": v, "unit": "struts/s", "n_gpus": args.gpus,
+        "impl": "reference", "metric": METRIC, "value": v, "unit": unit, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": sample, "chord_error": args.ce},
-        "cpu_baseline": {"value": v, "unit": "struts/s", "cores": 1, "kind": "oracle", "sample": sample},
-        "e2e": {"value": v, "unit": "struts/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "config": {"workload": sample, "chord_error": sweep or args.ce},
+        "cpu_baseline": {"value": v, "unit": unit, "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": v, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
 
 
@@ -181,6 +234,9 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="octet100")
     ap.add_argument("--ce", type=float, default=1e-3)
+    ap.add_argument("--ce-sweep", default="",
+                    help="comma-separated chord errors: re-triangulate ONE meta-mesh (built before the timed "
+                         "region) at each CE per step (configs[4], multi-resolution reuse)")
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
@@ -224,21 +280,36 @@ def main():
     cnts = torch.zeros(world, dtype=torch.int64, device=coll_dev)
     offsets = {"base": 0, "total": 0}
 
-    def step():
+    sweep = [float(x) for x in args.ce_sweep.split(",") if x] if args.ce_sweep else None
+    ces = sweep or [args.ce]
+    per_ce = {}
+
+    def load_and_build():
         B.lmm_load_lattice(h, xyz_d, ends_d, rend_d)
         if world > 1:
             B.lmm_set_emit_mask(h, nmask_d, smask_d)
         B.lmm_build_metamesh(h)
-        T = B.lmm_triangulate(h, args.ce)
-        if world > 1:   # global output offsets: all-gather of the per-rank triangle counts
-            cnt.fill_(T)
-            parts = list(cnts.split(1))
-            dist.all_gather(parts, cnt)
-            c = [int(x) for x in torch.cat(parts).tolist()]
-            offsets["base"], offsets["total"] = sum(c[:rank]), sum(c)
-        for f in range(0, T, EMIT_CHUNK):
-            B.lmm_write_triangles(h, f, min(EMIT_CHUNK, T - f), out)
+
+    def step():
+        if not sweep:
+            load_and_build()
+        T = 0
+        for ce in ces:
+            Tc = B.lmm_triangulate(h, ce)
+            if world > 1:   # global output offsets: all-gather of the per-rank triangle counts
+                cnt.fill_(Tc)
+                parts = list(cnts.split(1))
+                dist.all_gather(parts, cnt)
+                c = [int(x) for x in torch.cat(parts).tolist()]
+                offsets["base"], offsets["total"] = sum(c[:rank]), sum(c)
+            for f in range(0, Tc, EMIT_CHUNK):
+                B.lmm_write_triangles(h, f, min(EMIT_CHUNK, Tc - f), out)
+            per_ce[ce] = Tc
+            T += Tc
         return T
+
+    if sweep:
+        load_and_build()    # the fixed meta-mesh: built once, outside the timed region
 
     for _ in range(max(args.warmup, 0)):
         T = step()
@@ -273,7 +344,7 @@ def main():
 
     # ---- e2e: host inputs (pinned) -> device -> host triangle records, through the C-ABI
     e2e = None
-    if args.e2e_steps > 0:
+    if args.e2e_steps > 0 and not sweep:
         ring = torch.empty((1 << 24) * STL, dtype=torch.uint8).pin_memory()
         h2 = B.lmm_create(local, stream.cuda_stream)
         chunk = 1 << 24
@@ -319,11 +390,12 @@ def main():
     achieved = emit_bytes / (emit_ms / 1e3) / 1e9 if emit_ms > 0 else None
     mm_ms = kt["csr"][0] + kt["bucket"][0] + kt["metamesh"][0]
     tri_ms = kt["count"][0] + kt["scan"][0] + kt["emit"][0]
-    traffic = None
+    traffic, bpt = None, None
     try:
         with open(os.path.join(ROOT, "profiles", "emit_traffic.json")) as f:
-            traffic = json.load(f).get("bytes_per_triangle")
-    except (OSError, ValueError):
+            bpt = json.load(f).get("bytes_per_triangle")
+        traffic = bpt * float(T) * args.steps / emit_n if emit_n else None   # DRAM bytes per launch
+    except (OSError, ValueError, TypeError):
         pass
     res = {
         "metric": METRIC,
@@ -349,14 +421,24 @@ def main():
         "kernel_ms_per_step": {k: v[0] / args.steps for k, v in kt.items()},
         "roofline": {"bound": "hbm", "kernel": "k_emit", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak if achieved else None, "peak_source": src,
-                     "traffic": traffic, "algorithmic_bytes_per_triangle": STL,
+                     "traffic": traffic, "traffic_bytes_per_triangle": bpt, "algorithmic_bytes_per_triangle": STL,
                      "launches": emit_n, "avg_launch_ms": emit_ms / emit_n if emit_n else None},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
         "e2e": e2e,
     }
     if not args.no_cpu_baseline:
-        res["cpu_baseline"] = cpu_baseline(args.ce)
+        res["cpu_baseline"] = cpu_baseline(args.ce, args.config, sweep)
+    if sweep:   # configs[4]: re-triangulation of the fixed meta-mesh, triangles/s over the sweep
+        res["value"] = T_all / (ms_max / 1e3)
+        res["unit"] = "triangles/s"
+        res["config"]["chord_error"] = sweep
+        res["config"]["triangles_per_ce"] = {str(k): int(v) for k, v in per_ce.items()}
+        res["config"]["metamesh"] = "built once before the timed region (multi-resolution reuse)"
+        res["metamesh_struts_per_s"] = None
+    if args.config.startswith("stoch"):
+        dh = [int(x) for x in st["degree_hist"]]
+        res["config"]["degree_hist"] = {str(d): c for d, c in enumerate(dh) if c}
     print(json.dumps(res))
     B.lmm_destroy(h)
     if world > 1:

@@ -65,10 +65,9 @@ class Lattice:
 
 def _finish(xyz, ends, node_r, name) -> Lattice:
     ends = np.asarray(ends, dtype=np.int64).reshape(-1, 2)
-    lo = np.minimum(ends[:, 0], ends[:, 1])
-    hi = np.maximum(ends[:, 0], ends[:, 1])
-    order = np.lexsort((hi, lo))
-    ends = np.stack([lo[order], hi[order]], axis=1)
+    n = max(len(xyz), 1)
+    key = np.sort(np.minimum(ends[:, 0], ends[:, 1]) * n + np.maximum(ends[:, 0], ends[:, 1]))
+    ends = np.stack([key // n, key % n], axis=1)   # sorted by (min endpoint, max endpoint)
     return Lattice(np.ascontiguousarray(xyz, dtype=np.float32), np.ascontiguousarray(ends),
                    np.ascontiguousarray(node_r, dtype=np.float32), name)
 
@@ -258,3 +257,91 @@ def voronoi_like(n_nodes: int, seed: int = 0, deg_min: int = 3, deg_max: int = 3
         deg[b] += 1
         ends.append((a, b))
     return _finish(xyz, ends, _radii(n_nodes, radius), f"voronoi{n_nodes}")
+
+
+_STOCH_LIB = None
+
+
+def _stoch_lib():
+    """gcc-built helper of stochastic() (strut selection loop; input generation only)."""
+    global _STOCH_LIB
+    if _STOCH_LIB is None:
+        import ctypes
+        import os
+        import subprocess
+        here = os.path.dirname(os.path.abspath(__file__))
+        src, so = os.path.join(here, "_stochastic.c"), os.path.join(here, "_stochastic.so")
+        if not os.path.exists(so) or os.path.getmtime(so) < os.path.getmtime(src):
+            tmp = so + f".tmp{os.getpid()}"
+            subprocess.check_call(["gcc", "-O2", "-std=c11", "-shared", "-fPIC", "-o", tmp, src, "-lm"])
+            os.replace(tmp, so)
+        lib = ctypes.CDLL(so)
+        P = ctypes.c_void_p
+        lib.stoch_struts.restype = ctypes.c_int64
+        lib.stoch_struts.argtypes = [P, ctypes.c_int64, P, P, ctypes.c_double, ctypes.c_int64, P]
+        _STOCH_LIB = lib
+    return _STOCH_LIB
+
+
+def stochastic(side: int, seed: int = 0, deg_min: int = 3, deg_max: int = 30, r_min: float = 0.02,
+               r_max: float = 0.04, min_angle_deg: float = 25.0, zipf: float = 1.1) -> Lattice:
+    """Stochastic Voronoi-style lattice with skewed node degrees 3..30 (BASELINE.json
+    configs[2]: "~100M struts, load-balance stress"; side = 300 gives ~1e8 struts).
+
+    Nodes: a side^3 grid jittered by U(-0.3, 0.3) per axis.  Each node draws a target
+    degree from a Zipf-like law p(k) ~ (k - deg_min + 1)^-zipf on [deg_min, deg_max] and
+    a sphere radius U(r_min, r_max) (so struts are cones).  Struts: nodes in descending
+    target order take their nearest neighbours (5x5x5 surrounding cells) while both ends
+    are under target and every two struts at a node stay >= min_angle_deg apart
+    (synth/_stochastic.c).  Isolated nodes are possible and carry no surface."""
+    rng = np.random.default_rng(seed)
+    n = side ** 3
+    g = np.stack(np.meshgrid(np.arange(side), np.arange(side), np.arange(side), indexing="ij"), -1).reshape(-1, 3)
+    xyz = g + rng.uniform(-0.3, 0.3, size=g.shape)
+    del g
+    ks = np.arange(deg_min, deg_max + 1)
+    p = 1.0 / (ks - deg_min + 1.0) ** zipf
+    target = rng.choice(ks, size=n, p=p / p.sum()).astype(np.int32)
+    radius = rng.uniform(r_min, r_max, size=n)
+    order = np.argsort(-target, kind="stable").astype(np.int64)
+    cap = int(target.astype(np.int64).sum() // 2) + 1
+    ends = np.zeros((cap, 2), np.int64)
+    xyz = np.ascontiguousarray(xyz, np.float64)
+    S = _stoch_lib().stoch_struts(xyz.ctypes.data, side, target.ctypes.data, order.ctypes.data,
+                                  float(np.cos(np.deg2rad(min_angle_deg))), cap, ends.ctypes.data)
+    if S < 0:
+        raise RuntimeError(f"stochastic lattice generator failed ({S})")
+    return _finish(xyz, ends[:S], radius, f"stochastic{side}^3")
+
+
+def bcc_window(nx: int, ny: int, nz: int, k_lo: int, k_hi: int, pitch: float = 1.0,
+               radius: float = 0.05) -> Lattice:
+    """The part of the BCC lattice of nx*ny*nz cells whose nodes have half-pitch z index k in
+    [k_lo, k_hi] (clipped to [0, 2nz]), with the struts among them (spatial blocks of the
+    multi-GPU partition, BASELINE.json configs[3]).  In half-pitch integer coordinates the
+    cell corners are the all-even points and the cell centres the all-odd ones; each centre
+    joins its 8 corners (offsets (+-1, +-1, +-1)).  Nodes ascend in global id
+    gid = (i*(2ny+1) + j)*(2nz+1) + k, struts in (gid, gid), as octet_window."""
+    k_lo, k_hi = max(0, k_lo), min(2 * nz, k_hi)
+    I, J, K = np.meshgrid(np.arange(2 * nx + 1, dtype=np.int32), np.arange(2 * ny + 1, dtype=np.int32),
+                          np.arange(k_lo, k_hi + 1, dtype=np.int32), indexing="ij")
+    par = (I & 1)
+    keep = (par == (J & 1)) & (par == (K & 1))
+    g = np.stack([I[keep], J[keep], K[keep]], -1)      # meshgrid order = ascending gid
+    del I, J, K, par, keep
+    nk = k_hi - k_lo + 1
+    lut = -np.ones((2 * nx + 1, 2 * ny + 1, nk), dtype=np.int64)
+    lut[g[:, 0], g[:, 1], g[:, 2] - k_lo] = np.arange(len(g))
+    cen = np.nonzero(g[:, 0] & 1)[0]
+    gc = g[cen]
+    ends = []
+    for o in [(a, b, c) for a in (-1, 1) for b in (-1, 1) for c in (-1, 1)]:
+        q = gc + np.array(o, np.int32)
+        m = (q[:, 2] >= k_lo) & (q[:, 2] <= k_hi)        # x, y stay inside: centres are interior
+        ends.append(np.stack([cen[m], lut[q[m, 0], q[m, 1], q[m, 2] - k_lo]], 1))
+    del lut
+    xyz = g.astype(np.float64) * (0.5 * pitch)
+    lat = _finish(xyz, np.concatenate(ends), np.full(len(g), radius), f"bccwin{nx}x{ny}x{nz}[{k_lo}:{k_hi}]")
+    lat.ijk = g.astype(np.int64)
+    lat.gid = (lat.ijk[:, 0] * (2 * ny + 1) + lat.ijk[:, 1]) * (2 * nz + 1) + lat.ijk[:, 2]
+    return lat

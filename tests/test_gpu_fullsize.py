@@ -1,7 +1,9 @@
-"""Parity at BASELINE.json's full single-GPU size, in the launch configuration bench.py
-times (configs[1]: 100x100x100-cell graded octet truss, 24.12M struts, CE = 1e-3; the
-meta-mesh of every node in one lmm_build_metamesh, the triangles emitted into a device
-buffer in bench.py's 2^28-triangle chunks).
+"""Parity at BASELINE.json's full single-GPU sizes, in the launch configuration bench.py
+times (the meta-mesh of every node in one lmm_build_metamesh, the triangles emitted into a
+device buffer in bench.py's 2^28-triangle chunks), CE = 1e-3:
+  octet100 -- configs[1]: 100^3-cell graded octet truss, 24.12M struts (the headline bench);
+  bcc250   -- configs[3]: one GPU's 250^3-cell block of the 1B-strut BCC lattice, 125M struts;
+  stoch290 -- configs[2]: stochastic lattice, degrees 3..30, 102M struts.
 
 The oracle cannot meta-mesh 4M nodes in seconds, so it computes SAMPLED outputs one by
 one (orc_metamesh on a node subset; a band needs only its two end nodes):
@@ -27,17 +29,19 @@ N_NODES_SAMPLE = 4000
 N_STRUTS_SAMPLE = 4000
 
 
-@pytest.fixture(scope="module")
-def full():
+@pytest.fixture(scope="module", params=["octet100", "bcc250", "stoch290"])
+def full(request):
     import torch
     from paper_2405_15197_b200 import MetaMesher
-    lat, _, _ = bench.make_config("octet100")
+    lat, _, _ = bench.make_config(request.param)
     mm = MetaMesher(0).load_lattice(lat).build()
     T = mm.triangulate(CE)
     orc = oracle.Oracle.from_lattice(lat)
     out = torch.empty(bench.EMIT_CHUNK * bench.STL, dtype=torch.uint8, device="cuda")
     yield lat, mm, T, orc, out
     mm.close()
+    del out
+    torch.cuda.empty_cache()
 
 
 def _sample_nodes(lat, rng):
@@ -56,7 +60,7 @@ def _sample_nodes(lat, rng):
 def test_fullsize_whole_output_properties(full):
     lat, mm, T, orc, _ = full
     st = mm.stats()
-    assert st["n_error_nodes"] == 0 and st["n_struts"] == 24_120_000
+    assert st["n_error_nodes"] == 0 and st["n_struts"] == lat.n_struts and st["n_nodes"] == lat.n_nodes
     tb = mm.tri_buffers()
     band = tb["band"].astype(np.int64)
     soff = tb["strut_off"]

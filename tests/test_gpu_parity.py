@@ -31,13 +31,16 @@ def _lat(name):
         "bcc3-jitter": lambda: synth.jitter(synth.bcc(3, 3, 3), 0.05, 1),
         "cubic4-graded-jitter": lambda: synth.jitter(synth.graded_radii(synth.cubic(4, 4, 4), 0.06, 0.12, 2), 0.04, 2),
         "voronoi": lambda: synth.voronoi_like(300, seed=3, radius=0.05),
+        # configs[2] shape: skewed degrees 3..30, cones; configs[3] shape: a BCC spatial block
+        "stochastic9": lambda: synth.stochastic(9, seed=7),
+        "bccwin": lambda: synth.bcc_window(4, 3, 5, 3, 8),
         # BASELINE.json configs[0]: 10x10x10 BCC, uniform radius, eps = 1e-3 r
         "bcc10": lambda: synth.bcc(10, 10, 10),
     }[name]()
 
 
 NAMES = ["single", "cone", "chain-bent", "star-bcc", "cubic3", "bcc3", "octet2", "octet2-graded", "bcc3-jitter",
-         "cubic4-graded-jitter", "voronoi", "bcc10"]
+         "cubic4-graded-jitter", "voronoi", "stochastic9", "bccwin", "bcc10"]
 
 
 @pytest.fixture(scope="module")
@@ -155,7 +158,8 @@ def test_csr_offsets_are_the_degree_prefix_sum(built):
     assert np.array_equal(ent[:, 0].astype(np.int64), o_st)
 
 
-def test_two_virtual_ranks_union_equals_global_gpu():
+@pytest.mark.parametrize("family", ["octet", "bcc"])
+def test_virtual_ranks_union_equals_global_gpu(family):
     """The multi-GPU path on one device: slab windows with halo recompute + emit masks.  The
     union of the per-rank STL outputs equals the single-lattice output bitwise (as a set),
     so the global mesh is seamless across rank boundaries."""
@@ -163,14 +167,16 @@ def test_two_virtual_ranks_union_equals_global_gpu():
     from paper_2405_15197_b200 import partition as P
     nx, ny, nz = 4, 3, 6
     k_top = 2 * nz
-    full = synth.octet_window(nx, ny, nz, 0, k_top, radius=0.03, r_max=0.06)
+    gen = (lambda lo, hi: synth.octet_window(nx, ny, nz, lo, hi, radius=0.03, r_max=0.06)) if family == "octet" \
+        else (lambda lo, hi: synth.bcc_window(nx, ny, nz, lo, hi, radius=0.05))
+    full = gen(0, k_top)
     mm = MetaMesher(0).load_lattice(full).build()
     T = mm.triangulate(5e-3)
     ref = mm.triangles(0, T)
     parts, counts = [], []
     for r in range(3):
         k_lo, k_hi = P.window(r, 3, k_top)
-        lat = synth.octet_window(nx, ny, nz, k_lo, k_hi, radius=0.03, r_max=0.06)
+        lat = gen(k_lo, k_hi)
         nm, sm = P.emit_masks(lat.ijk[:, 2], lat.ends, r, 3, k_top)
         m = MetaMesher(0).load_lattice(lat).build().set_emit_mask(nm, sm)
         Tr = m.triangulate(5e-3)

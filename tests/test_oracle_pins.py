@@ -332,6 +332,8 @@ LATTICES = {
     "bcc3-jitter": lambda: synth.jitter(synth.bcc(3, 3, 3), 0.05, 1),
     "cubic4-graded-jitter": lambda: synth.jitter(synth.graded_radii(synth.cubic(4, 4, 4), 0.06, 0.12, 2), 0.04, 2),
     "voronoi": lambda: synth.voronoi_like(200, seed=3, radius=0.05),
+    "stochastic6": lambda: synth.stochastic(6, seed=5),
+    "bccwin": lambda: synth.bcc_window(3, 2, 2, 1, 3),
 }
 
 
