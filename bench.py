@@ -39,39 +39,32 @@ def make_config(name: str, rank: int = 0, world: int = 1):
     `world` blocks stacked along z; rank r gets its slab plus a 2-layer halo and the emit
     masks of the nodes / struts it owns (paper_2405_15197_b200.partition)."""
     from paper_2405_15197_b200 import partition as P
-    if name in ("octet100", "octet40"):
-        n = 100 if name == "octet100" else 40
+    import re
+    m = re.fullmatch(r"(octet|bcc|stoch)(\d+)", name)
+    fam, n = (m.group(1), int(m.group(2))) if m else (name, 0)
+    if fam == "octet":
+        # configs[1] (octet100: 24.12M struts) and configs[4]'s fixed meta-mesh (octet160: 98.6M)
         k_top = 2 * n * world
         k_lo, k_hi = P.window(rank, world, k_top) if world > 1 else (0, k_top)
         lat = synth.octet_window(n, n, n * world, k_lo, k_hi, radius=0.03, r_max=0.06)
         masks = P.emit_masks(lat.ijk[:, 2], lat.ends, rank, world, k_top) if world > 1 else (None, None)
         desc = (f"octet-truss {n}x{n}x{n} cells per GPU (global {n}x{n}x{n * world}), conical struts "
                 f"(node radii graded 0.03-0.06 along x, pitch 1)")
-    elif name == "bcc250":
+    elif fam == "bcc" and name != "bcc10":
         # configs[3]: the ~1B-strut BCC lattice of 8 GPUs = 8 blocks of 250^3 cells (125M struts each)
-        n = 250
         k_top = 2 * n * world
         k_lo, k_hi = P.window(rank, world, k_top) if world > 1 else (0, k_top)
         lat = synth.bcc_window(n, n, n * world, k_lo, k_hi, radius=0.05)
         masks = P.emit_masks(lat.ijk[:, 2], lat.ends, rank, world, k_top) if world > 1 else (None, None)
         desc = (f"BCC {n}x{n}x{n} cells per GPU (global {n}x{n}x{n * world}, {8 * n ** 3 * world / 1e9:.3f}B struts), "
                 f"uniform radius 0.05, pitch 1")
-    elif name == "stoch290":
-        # configs[2]: stochastic Voronoi-style lattice, degrees 3..30, ~1e8 struts; ranks get
-        # independent lattices (seed = rank), so there is nothing to exchange
-        lat = synth.stochastic(290, seed=rank)
+    elif fam == "stoch":
+        # configs[2]: stochastic Voronoi-style lattice, degrees 3..30, ~1e8 struts at n = 290; ranks
+        # get independent lattices (seed = rank), so there is nothing to exchange
+        lat = synth.stochastic(n, seed=rank)
         masks = (None, None)
-        desc = ("stochastic Voronoi-style lattice per GPU: jittered 290^3 grid, Zipf target degrees 3-30, "
+        desc = (f"stochastic Voronoi-style lattice per GPU: jittered {n}^3 grid, Zipf target degrees 3-30, "
                 "cone radii U(0.02, 0.04), >=25 deg between struts at a node (synth.stochastic, seed = rank)")
-    elif name == "octet160":
-        # configs[4]: one fixed ~100M-strut meta-mesh (octet 160^3 cells, 98.3M struts)
-        n = 160
-        k_top = 2 * n * world
-        k_lo, k_hi = P.window(rank, world, k_top) if world > 1 else (0, k_top)
-        lat = synth.octet_window(n, n, n * world, k_lo, k_hi, radius=0.03, r_max=0.06)
-        masks = P.emit_masks(lat.ijk[:, 2], lat.ends, rank, world, k_top) if world > 1 else (None, None)
-        desc = (f"octet-truss {n}x{n}x{n} cells per GPU (global {n}x{n}x{n * world}), conical struts "
-                f"(node radii graded 0.03-0.06 along x, pitch 1)")
     elif name == "bcc10":
         lat = synth.bcc(10, 10, 10)
         masks = (None, None)

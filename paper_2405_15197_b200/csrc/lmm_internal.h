@@ -56,6 +56,7 @@ struct lmm_ctx {
   DevBuf mbits;      // uint32 merge bits (1 per band triangle)
   DevBuf macc;       // int per merge word
   DevBuf cmap;       // int per emit chunk
+  DevBuf brec;       // 64-byte emit record per strut band
   int64_t H = 0, n_tri = 0, n_tri_band = 0;
   bool tri_ok = false;
   // scratch

@@ -25,6 +25,17 @@ constexpr int TPC = 1024;       // triangles per emit chunk (51 200 B of records
 constexpr int EMIT_T = 128;     // threads per emit CTA
 constexpr int REC = 50;
 
+// Everything the emit pass needs to start a band, written once per strut by k_band_merge
+// (after the offsets scan), so that a band is fetched as one 64-byte record + its offset.
+struct __align__(16) BandRec {
+  int nA, nB, kB, lAc;   // ring sizes, ring-B rotation; lAc = first loop entry of ring A in
+  int lBc;               //   its node's loop slab | entry count << 16 (lBc: ring B)
+  unsigned aA, aB;       // arc slab base of each end node (3 off + 2 n; loop slab = 2 a)
+  unsigned pA, pB;       // off + n of each end node (vertex slab = 2 p)
+  float oax, oay, oaz, obx, oby, obz, pad;   // node centres
+};
+static_assert(sizeof(BandRec) == 64, "band record is 4 x 16 bytes");
+
 struct TriParams {
   const float4 *node;
   const int *csr_off;
@@ -52,6 +63,7 @@ struct TriParams {
   uint32_t *mbits;          // merge bits, bit t = triangle t advances ring A
   int *macc;                // [word] A-advances of the band before the word's first bit
   int *cmap;                // [chunk] first band (band region) / hole (hole region)
+  BandRec *brec;            // [S] emit records
   const uint8_t *node_mask; // [N] or null
   const uint8_t *strut_mask;// [S] or null
   int64_t n_chunks;
@@ -179,10 +191,19 @@ __global__ void k_band_merge(TriParams P) {
   if (s >= P.S) return;
   int4 bd = P.band[s];
   const int nA = bd.x, nB = bd.y;
-  if (nA + nB == 0) return;
+  float4 *rq = reinterpret_cast<float4 *>(P.brec + s);
+  if (nA + nB == 0) { rq[0] = make_float4(0.f, 0.f, 0.f, 0.f); return; }
   int2 e = P.ends[s];
   int2 ce = P.strut_csr[s];
   int2 LA = P.loop_hdr[ce.x], LB = P.loop_hdr[ce.y];
+  {
+    const int offA = P.csr_off[e.x], offB = P.csr_off[e.y];
+    const float4 na = P.node[e.x], nb = P.node[e.y];
+    rq[1] = make_float4(__int_as_float(LB.x | (LB.y << 16)), __uint_as_float(3u * offA + 2u * e.x),
+                        __uint_as_float(3u * offB + 2u * e.y), __uint_as_float((unsigned)(offA + e.x)));
+    rq[2] = make_float4(__uint_as_float((unsigned)(offB + e.y)), na.x, na.y, na.z);
+    rq[3] = make_float4(nb.x, nb.y, nb.z, 0.0f);
+  }
   KeyCursor A, B;
   A.le = P.loop + lbase(P.csr_off, e.x) + LA.x; A.cnt = LA.y; A.load(0);
   B.le = P.loop + lbase(P.csr_off, e.y) + LB.x; B.cnt = LB.y; B.load(0);
@@ -196,6 +217,7 @@ __global__ void k_band_merge(TriParams P) {
       if (j == 0 || r < best) { best = r; kB = j; }
     }
     P.band[s].z = kB;
+    rq[0] = make_float4(__int_as_float(nA), __int_as_float(nB), __int_as_float(kB), __int_as_float(LA.x | (LA.y << 16)));
   }
   const float b0 = wrap_rel(B.key(kB), a0);
   const int64_t base = P.strut_off[s];
@@ -354,17 +376,6 @@ struct __align__(16) WarpRing {
   uint4 stage[GRP * REC / 16];
 };
 
-// band header: band / strut_off / ends / strut_csr (stage 1), then the loop headers, node
-// centres and CSR offsets of both ends (stage 2)
-struct __align__(16) BandHdr {
-  int4 bd;
-  float4 oa, ob;
-  long long base;
-  int2 e, ce;
-  int2 LA, LB;
-  int offA, offB;
-};
-
 template <int BYTES>
 __device__ __forceinline__ void cp_async(void *sdst, const void *gsrc) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
@@ -377,36 +388,27 @@ __device__ __forceinline__ void cp_async_wait_warp() {
   __syncwarp();
 }
 
-__device__ __forceinline__ void fetch_hdr(const TriParams &P, int s, BandHdr &h, int lane) {
-  if (lane == 0) cp_async<16>(&h.bd, &P.band[s]);
-  else if (lane == 1) cp_async<8>(&h.base, &P.strut_off[s]);
-  else if (lane == 2) cp_async<8>(&h.e, &P.ends[s]);
-  else if (lane == 3) cp_async<8>(&h.ce, &P.strut_csr[s]);
+// stage 1 of a band: its record (lanes 0-3) and triangle offset (lane 4)
+__device__ __forceinline__ void fetch_rec(const TriParams &P, int s, BandRec &h, long long &base, int lane) {
+  if (lane < 4) cp_async<16>(reinterpret_cast<float4 *>(&h) + lane, reinterpret_cast<const float4 *>(P.brec + s) + lane);
+  else if (lane == 4) cp_async<8>(&base, &P.strut_off[s]);
 }
-__device__ __forceinline__ void fetch_ends(const TriParams &P, BandHdr &h, int lane) {
-  if (lane < 6) {
-    const int2 e = h.e, ce = h.ce;
-    if (lane == 0) cp_async<8>(&h.LA, &P.loop_hdr[ce.x]);
-    else if (lane == 1) cp_async<8>(&h.LB, &P.loop_hdr[ce.y]);
-    else if (lane == 2) cp_async<16>(&h.oa, &P.node[e.x]);
-    else if (lane == 3) cp_async<16>(&h.ob, &P.node[e.y]);
-    else if (lane == 4) cp_async<4>(&h.offA, &P.csr_off[e.x]);
-    else cp_async<4>(&h.offB, &P.csr_off[e.y]);
-  }
-}
-__device__ __forceinline__ bool band_live(const BandHdr &h) { return h.bd.x + h.bd.y > 0; }
-__device__ __forceinline__ void fetch_entries(const TriParams &P, WarpRing &w, const BandHdr &h, int lane) {
+__device__ __forceinline__ bool band_live(const BandRec &h) { return h.nA + h.nB > 0; }
+__device__ __forceinline__ int rec_cnt(int lc) { return lc >> 16; }
+__device__ __forceinline__ int rec_first(int lc) { return lc & 0xffff; }
+// stage 2: loop entries of both rings
+__device__ __forceinline__ void fetch_entries(const TriParams &P, WarpRing &w, const BandRec &h, int lane) {
   if (!band_live(h)) return;
-  const int2 LA = h.LA, LB = h.LB;
-  if (lane < LA.y) cp_async<16>(&w.le[0][lane], P.loop + slab_base(h.offA, h.e.x, SLAB_L_K, SLAB_L_K0) + LA.x + lane);
-  if (lane < LB.y) cp_async<16>(&w.le[1][lane], P.loop + slab_base(h.offB, h.e.y, SLAB_L_K, SLAB_L_K0) + LB.x + lane);
+  if (lane < rec_cnt(h.lAc)) cp_async<16>(&w.le[0][lane], P.loop + 2 * (int64_t)h.aA + rec_first(h.lAc) + lane);
+  if (lane < rec_cnt(h.lBc)) cp_async<16>(&w.le[1][lane], P.loop + 2 * (int64_t)h.aB + rec_first(h.lBc) + lane);
 }
-__device__ __forceinline__ void fetch_arcs(const TriParams &P, WarpRing &w, const BandHdr &h, int lane) {
+// stage 3: the arc records of the entries (first MAXRA of each ring)
+__device__ __forceinline__ void fetch_arcs(const TriParams &P, WarpRing &w, const BandRec &h, int lane) {
   if (!band_live(h)) return;
 #pragma unroll
   for (int r = 0; r < 2; r++) {
-    const int cnt = r ? h.LB.y : h.LA.y;
-    const ArcRec *arcs = P.arc + (r ? slab_base(h.offB, h.e.y, SLAB_A_K, SLAB_A_K0) : slab_base(h.offA, h.e.x, SLAB_A_K, SLAB_A_K0));
+    const int cnt = rec_cnt(r ? h.lBc : h.lAc);
+    const ArcRec *arcs = P.arc + (r ? h.aB : h.aA);
     const int nq = (cnt < MAXRA ? cnt : MAXRA) * 3;
     for (int k = lane; k < nq; k += 32) {
       const int e = k / 3;
@@ -664,24 +666,19 @@ __device__ void emit_band_whole(const TriParams &P, WarpRing &w, const RingRef &
 }
 
 template <class Prefetch>
-__device__ void emit_band(const TriParams &P, WarpRing &w, const BandHdr &H, int64_t first, int64_t last,
+__device__ void emit_band(const TriParams &P, WarpRing &w, const BandRec &H, int64_t base, int64_t first, int64_t last,
                           unsigned char *out, int lane, Prefetch prefetch) {
-  const int64_t base = H.base;
-  const int4 bd = H.bd;
-  const int nA = bd.x, nB = bd.y, kB = bd.z;
+  const int nA = H.nA, nB = H.nB, kB = H.kB;
   const int64_t ta = base > first ? base : first;
   const int64_t tb = base + nA + nB < last ? base + nA + nB : last;
   if (ta >= tb) { prefetch(0); prefetch(1); prefetch(2); prefetch(3); return; }
-  const int2 e = H.e, LA = H.LA, LB = H.LB;
-  const int offA = H.offA, offB = H.offB;
-  const float4 oa = H.oa, ob = H.ob;
   RingRef RA, RB;
-  RA.arcs = P.arc + slab_base(offA, e.x, SLAB_A_K, SLAB_A_K0);
-  RA.vs = P.vert + slab_base(offA, e.x, SLAB_V_K, SLAB_V_K0);
-  RA.ox = oa.x; RA.oy = oa.y; RA.oz = oa.z; RA.cnt = LA.y;
-  RB.arcs = P.arc + slab_base(offB, e.y, SLAB_A_K, SLAB_A_K0);
-  RB.vs = P.vert + slab_base(offB, e.y, SLAB_V_K, SLAB_V_K0);
-  RB.ox = ob.x; RB.oy = ob.y; RB.oz = ob.z; RB.cnt = LB.y;
+  RA.arcs = P.arc + H.aA;
+  RA.vs = P.vert + 2 * (int64_t)H.pA;
+  RA.ox = H.oax; RA.oy = H.oay; RA.oz = H.oaz; RA.cnt = rec_cnt(H.lAc);
+  RB.arcs = P.arc + H.aB;
+  RB.vs = P.vert + 2 * (int64_t)H.pB;
+  RB.ox = H.obx; RB.oy = H.oby; RB.oz = H.obz; RB.cnt = rec_cnt(H.lBc);
   const int qb = (int)(ta - base), qe = (int)(tb - base);
   prefetch(0);
   if (nA + nB + 2 <= PMAX && RA.cnt <= MAXRA && RB.cnt <= MAXRA) {
@@ -802,35 +799,31 @@ __device__ void emit_hole(const TriParams &P, WarpRing &w, int g, int64_t first,
 __global__ void __launch_bounds__(EMIT_T, 7) k_emit(TriParams P, int64_t first, int64_t count, unsigned char *out,
                                                  int64_t s0, int64_t s1, int64_t g0, int64_t g1) {
   extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ BandHdr hdr[EW][3];
+  __shared__ BandRec rec[EW][2];
+  __shared__ long long rbase[EW][2];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   WarpRing &w = reinterpret_cast<WarpRing *>(smem)[warp];
   const int64_t last = first + count;
   const int64_t gw = (int64_t)blockIdx.x * EW + warp, nw = (int64_t)gridDim.x * EW;
   const int64_t nb = s1 - s0, nh = g1 - g0;
-  // band u+nw: header at band u-nw's start, loop headers/centres at band u's start, entries
-  // after band u's points, arc records after its first group
+  // band u+nw: record at band u's start, loop entries after band u's points, arc records
+  // after its first group (three dependent stages overlapped with band u)
   int cb = 0;
-  if (gw < nb) {   // first band: all stages up front, the second band's header too
-    fetch_hdr(P, (int)(s0 + gw), hdr[warp][0], lane);
+  if (gw < nb) {   // first band: all stages up front
+    fetch_rec(P, (int)(s0 + gw), rec[warp][0], rbase[warp][0], lane);
     cp_async_wait_warp();
-    fetch_ends(P, hdr[warp][0], lane);
+    fetch_entries(P, w, rec[warp][0], lane);
     cp_async_wait_warp();
-    fetch_entries(P, w, hdr[warp][0], lane);
-    cp_async_wait_warp();
-    fetch_arcs(P, w, hdr[warp][0], lane);
-    if (gw + nw < nb) fetch_hdr(P, (int)(s0 + gw + nw), hdr[warp][1], lane);
+    fetch_arcs(P, w, rec[warp][0], lane);
     cp_async_wait_warp();
   }
   for (int64_t u = gw; u < nb + nh; u += nw) {
     if (u < nb) {
-      const bool more = u + nw < nb, more2 = u + 2 * nw < nb;
-      BandHdr &nx = hdr[warp][cb == 2 ? 0 : cb + 1];
-      BandHdr &nx2 = hdr[warp][cb == 0 ? 2 : cb - 1];
-      emit_band(P, w, hdr[warp][cb], first, last, out, lane, [&](int stage) {
+      const bool more = u + nw < nb;
+      BandRec &nx = rec[warp][cb ^ 1];
+      emit_band(P, w, rec[warp][cb], rbase[warp][cb], first, last, out, lane, [&](int stage) {
         if (stage == 0) {
-          if (more) fetch_ends(P, nx, lane);
-          if (more2) fetch_hdr(P, (int)(s0 + u + 2 * nw), nx2, lane);
+          if (more) fetch_rec(P, (int)(s0 + u + nw), nx, rbase[warp][cb ^ 1], lane);
           return;
         }
         if (!more) return;
@@ -839,7 +832,7 @@ __global__ void __launch_bounds__(EMIT_T, 7) k_emit(TriParams P, int64_t first, 
         else if (stage == 2) fetch_arcs(P, w, nx, lane);
       });
       cp_async_wait_warp();
-      cb = cb == 2 ? 0 : cb + 1;
+      cb ^= 1;
     } else emit_hole(P, w, (int)(g0 + u - nb), first, last, out, lane);
   }
 }
@@ -874,6 +867,7 @@ TriParams make_params(lmm_ctx *c) {
   P.mbits = (uint32_t *)c->mbits.p;
   P.macc = (int *)c->macc.p;
   P.cmap = (int *)c->cmap.p;
+  P.brec = (BandRec *)c->brec.p;
   P.node_mask = c->has_node_mask ? (const uint8_t *)c->node_mask.p : nullptr;
   P.strut_mask = c->has_strut_mask ? (const uint8_t *)c->strut_mask.p : nullptr;
   P.n_chunks = (c->n_tri + TPC - 1) / TPC;
@@ -908,6 +902,7 @@ int triangulate_count(lmm_ctx *c) {
   const int64_t nwords = c->n_tri_band / 32 + 2;
   if ((rc = dev_alloc(c->mbits, sizeof(uint32_t) * nwords))) return rc;
   if ((rc = dev_alloc(c->macc, sizeof(int) * nwords))) return rc;
+  if ((rc = dev_alloc(c->brec, sizeof(BandRec) * (S + 1)))) return rc;
   P = make_params(c);
   {
     KTimer t(c, LMM_K_COUNT);

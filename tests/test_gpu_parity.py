@@ -109,7 +109,10 @@ def test_triangulation_parity(built, name, ce):
     verr = np.max(np.abs(tri[:, 1:] - ref[:, 1:]), axis=(1, 2))
     ok = alt > 0
     nerr = np.max(np.abs(tri[ok, 0] - ref[ok, 0]), axis=1)
-    assert np.all(nerr <= 4 * verr[ok] / alt[ok] + 1e-5)
+    # the kernel's normal comes from the binary32 vertices it writes, each off the binary64
+    # point by its own error plus the 2^-24 |x| rounding of the absolute coordinate
+    rep = 2.0 ** -24 * np.max(np.abs(ref[:, 1:]), axis=(1, 2))
+    assert np.all(nerr <= 4 * (verr[ok] + rep[ok]) / alt[ok] + 1e-5)
     # the kernel's own output is watertight: welded by exact binary32 coordinates
     counts, chi = _mesh_edges_ok(mm.triangles(0, T))
     assert counts == {2}
