@@ -365,9 +365,9 @@ __device__ __forceinline__ void put_rec(unsigned char *dst, f3 a, f3 b, f3 c) {
 constexpr int EW = EMIT_T / 32;   // warps per CTA
 constexpr int PMAX = 160;         // ring points cached per band (both rings)
 constexpr int WIN = PMAX - 2;     // merge steps per window of a band with more points
-constexpr int GRP = 64;           // triangles per aligned group (3200 B)
+constexpr int GRP = 56;           // triangles per aligned group (2800 B; 28 lanes x 2 records)
 constexpr int MAXRE = 32;         // ring entries per ring (>= MAXLOOP of the meta-mesh)
-constexpr int MAXRA = 12;         // arc records cached per ring
+constexpr int MAXRA = 10;         // arc records cached per ring
 
 struct __align__(16) WarpRing {
   ArcRec arc[2][MAXRA];
@@ -796,7 +796,7 @@ __device__ void emit_hole(const TriParams &P, WarpRing &w, int g, int64_t first,
 }
 
 // units: bands [s0, s1) then holes [g0, g1) intersecting [first, last)
-__global__ void __launch_bounds__(EMIT_T, 7) k_emit(TriParams P, int64_t first, int64_t count, unsigned char *out,
+__global__ void __launch_bounds__(EMIT_T, 8) k_emit(TriParams P, int64_t first, int64_t count, unsigned char *out,
                                                  int64_t s0, int64_t s1, int64_t g0, int64_t g1) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ BandRec rec[EW][2];
