@@ -529,7 +529,13 @@ __device__ __forceinline__ void put_rec16(unsigned char *dst, const uint32_t *f)
 }
 
 // staged group bytes [b0, b1) -> dst + [b0, b1), dst 16-byte aligned: 2-byte head up to the
-// first 16-byte boundary, 16-byte vectors, 2-byte tail (b0, b1 even)
+// first 16-byte boundary and 2-byte tail through the LSU, the 16-byte-aligned body as one
+// TMA bulk copy (cp.async.bulk.global.shared::cta) issued by lane 0 -- the body bypasses
+// the L1/LSU path.  The staging buffer may be rewritten after stage_wait().
+__device__ __forceinline__ void stage_wait(int lane) {
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+  __syncwarp();
+}
 __device__ __forceinline__ void flush_group(WarpRing &w, int b0, int b1, unsigned char *dst, int lane) {
   __syncwarp();
   const int v0 = (b0 + 15) >> 4, v1 = b1 >> 4;
@@ -538,14 +544,18 @@ __device__ __forceinline__ void flush_group(WarpRing &w, int b0, int b1, unsigne
   if (v0 <= v1) {
     const int h = (v0 << 3) - (b0 >> 1);          // head half-words
     if (lane < h) d16[(b0 >> 1) + lane] = s16[(b0 >> 1) + lane];
-    uint4 *d = reinterpret_cast<uint4 *>(dst);
-#pragma unroll
-    for (int i = 0; i < (GRP * REC / 16 + 31) / 32; i++) {
-      const int k = v0 + lane + 32 * i;
-      if (k < v1) d[k] = w.stage[k];
-    }
     const int t0 = v1 << 3, tn = (b1 >> 1) - t0;  // tail half-words
     if (lane < tn) d16[t0 + lane] = s16[t0 + lane];
+    if (v1 > v0) {
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // staging writes -> async proxy
+      __syncwarp();
+      if (lane == 0) {
+        const unsigned sa = (unsigned)__cvta_generic_to_shared(w.stage + v0);
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n"
+                     ::"l"(dst + 16 * v0), "r"(sa), "r"(16 * (v1 - v0)) : "memory");
+        asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+      }
+    }
   } else {                                          // range inside one 16-byte unit
     const int n = (b1 - b0) >> 1;
     if (lane < n) d16[(b0 >> 1) + lane] = s16[(b0 >> 1) + lane];
@@ -638,6 +648,7 @@ __device__ void emit_band_whole(const TriParams &P, WarpRing &w, const RingRef &
     const unsigned ma = __ballot_sync(0xffffffffu, aa), mb = __ballot_sync(0xffffffffu, ab);
     const int ia = irun + __popc(ma & lt) + __popc(mb & lt);
     irun += __popc(ma) + __popc(mb);
+    stage_wait(lane);
     if (va || vb) {
       // state before the lane's first valid step: A_i, B_j; each triangle (A_i, c, B_j)
       // advances one ring onto its new point c
@@ -727,6 +738,7 @@ __device__ void emit_band(const TriParams &P, WarpRing &w, const BandRec &H, int
       const unsigned ma = __ballot_sync(0xffffffffu, aa), mb = __ballot_sync(0xffffffffu, ab);
       const int ia = irun + __popc(ma & lt) + __popc(mb & lt);
       irun += __popc(ma) + __popc(mb);
+      stage_wait(lane);
       if (va || vb) {
         uint32_t *d = reinterpret_cast<uint32_t *>(w.stage) + 25 * lane;
         uint32_t f[12];
@@ -835,6 +847,7 @@ __global__ void __launch_bounds__(EMIT_T, 8) k_emit(TriParams P, int64_t first, 
       cb ^= 1;
     } else emit_hole(P, w, (int)(g0 + u - nb), first, last, out, lane);
   }
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
 }
 
 TriParams make_params(lmm_ctx *c) {
