@@ -372,7 +372,8 @@ constexpr int MAXRA = 10;         // arc records cached per ring
 struct __align__(16) WarpRing {
   ArcRec arc[2][MAXRA];
   LoopRec le[2][MAXRE];   // loop entries (arc | fwd | N, phs, dph, cum); holes: arc_fwd, cum
-  float px[PMAX], py[PMAX], pz[PMAX];
+  float2 pxy[PMAX];
+  float pz[PMAX];
   uint4 stage[GRP * REC / 16];
 };
 
@@ -481,8 +482,8 @@ __device__ __forceinline__ f3 ring_point_formula(const WarpRing &w, int r, const
             R.oz + fmaf(A.az, sn, fmaf(A.bz, cs, A.oz)));
 }
 
-__device__ __forceinline__ void put_point(WarpRing &w, int k, f3 p) { w.px[k] = p.x; w.py[k] = p.y; w.pz[k] = p.z; }
-__device__ __forceinline__ f3 get_point(const WarpRing &w, int k) { return F3(w.px[k], w.py[k], w.pz[k]); }
+__device__ __forceinline__ void put_point(WarpRing &w, int k, f3 p) { w.pxy[k] = make_float2(p.x, p.y); w.pz[k] = p.z; }
+__device__ __forceinline__ f3 get_point(const WarpRing &w, int k) { const float2 q = w.pxy[k]; return F3(q.x, q.y, w.pz[k]); }
 
 // A-advances of band [base, ...) before triangle t
 __device__ __forceinline__ int merge_rank(const TriParams &P, int64_t base, int64_t t) {
@@ -497,11 +498,16 @@ __device__ __forceinline__ int merge_rank(const TriParams &P, int64_t base, int6
   return __ldg(&P.macc[w]) + __popc(below);
 }
 
+__device__ __forceinline__ float rsqrt_approx(float x) {
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
 __device__ __forceinline__ void tri_words(f3 a, f3 b, f3 c, uint32_t *f) {
   f3 u = f_sub(b, a), v = f_sub(c, a);
   float nx = u.y * v.z - u.z * v.y, ny = u.z * v.x - u.x * v.z, nz = u.x * v.y - u.y * v.x;
   float l2 = nx * nx + ny * ny + nz * nz;
-  float il = l2 > 0.0f ? rsqrtf(l2) : 0.0f;
+  float il = l2 > 0.0f ? rsqrt_approx(l2) : 0.0f;
   f[0] = __float_as_uint(nx * il); f[1] = __float_as_uint(ny * il); f[2] = __float_as_uint(nz * il);
   f[3] = __float_as_uint(a.x); f[4] = __float_as_uint(a.y); f[5] = __float_as_uint(a.z);
   f[6] = __float_as_uint(b.x); f[7] = __float_as_uint(b.y); f[8] = __float_as_uint(b.z);
@@ -542,10 +548,6 @@ __device__ __forceinline__ void flush_group(WarpRing &w, int b0, int b1, unsigne
   const uint16_t *s16 = reinterpret_cast<const uint16_t *>(w.stage);
   uint16_t *d16 = reinterpret_cast<uint16_t *>(dst);
   if (v0 <= v1) {
-    const int h = (v0 << 3) - (b0 >> 1);          // head half-words
-    if (lane < h) d16[(b0 >> 1) + lane] = s16[(b0 >> 1) + lane];
-    const int t0 = v1 << 3, tn = (b1 >> 1) - t0;  // tail half-words
-    if (lane < tn) d16[t0 + lane] = s16[t0 + lane];
     if (v1 > v0) {
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // staging writes -> async proxy
       __syncwarp();
@@ -556,6 +558,10 @@ __device__ __forceinline__ void flush_group(WarpRing &w, int b0, int b1, unsigne
         asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
       }
     }
+    const int h = (v0 << 3) - (b0 >> 1);          // head half-words
+    if (lane < h) d16[(b0 >> 1) + lane] = s16[(b0 >> 1) + lane];
+    const int t0 = v1 << 3, tn = (b1 >> 1) - t0;  // tail half-words
+    if (lane < tn) d16[t0 + lane] = s16[t0 + lane];
   } else {                                          // range inside one 16-byte unit
     const int n = (b1 - b0) >> 1;
     if (lane < n) d16[(b0 >> 1) + lane] = s16[(b0 >> 1) + lane];
@@ -589,12 +595,14 @@ __device__ void emit_band_whole(const TriParams &P, WarpRing &w, const RingRef &
   {
     const int cA = (lane >= 1 && lane < RA.cnt) ? w.le[0][lane].cum : 0x7fffffff;
     const int cB = lane < RB.cnt ? nA + w.le[1][lane].cum : 0x7fffffff;
+    int run = 0;   // entry starts (after ring A's first) below the current block
     for (int x = 0; x < nA + nB; x += 32) {
       const int k = x + lane;
-      const unsigned bits = ((cA >= x && cA < x + 32) ? 1u << (cA - x) : 0u) | ((cB >= x && cB < x + 32) ? 1u << (cB - x) : 0u);
+      const unsigned dA = (unsigned)(cA - x), dB = (unsigned)(cB - x);
+      const unsigned bits = (dA < 32u ? 1u << dA : 0u) | (dB < 32u ? 1u << dB : 0u);
       const unsigned M = __reduce_or_sync(0xffffffffu, bits);
-      const int ec = __popc(__ballot_sync(0xffffffffu, cA < x)) + __popc(__ballot_sync(0xffffffffu, cB < x)) +
-                     __popc(M & ((2u << lane) - 1u));
+      const int ec = run + __popc(M & ((2u << lane) - 1u));
+      run += __popc(M);
       if (k < nA + nB) {
         if (ec < RA.cnt) {
           const f3 p = ring_point_formula(w, 0, RA, ec, k);
