@@ -38,6 +38,14 @@ def _stale(obj: str, deps) -> bool:
 
 def build(verbose: bool = False, force: bool = False) -> str:
     os.makedirs(OUT_DIR, exist_ok=True)
+    # LMM_NVCC_EXTRA: extra nvcc flags for tuning experiments (a change forces a rebuild)
+    extra_all = os.environ.get("LMM_NVCC_EXTRA", "").split()
+    stamp = os.path.join(OUT_DIR, "flags.txt")
+    old = open(stamp).read() if os.path.exists(stamp) else ""
+    if old != " ".join(extra_all):
+        force = True
+        with open(stamp, "w") as f:
+            f.write(" ".join(extra_all))
     headers = [os.path.join(SRC, f) for f in os.listdir(SRC) if f.endswith((".h", ".cuh"))]
     headers.append(os.path.join(os.path.dirname(HERE), "include", "lmm.h"))
     objs = []
@@ -47,7 +55,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
         o = os.path.join(OUT_DIR, src.replace(".cu", ".o"))
         objs.append(o)
         if force or _stale(o, [s, *headers, __file__]):
-            cmd = [NVCC, *ARCH, *COMMON, *extra, "-c", s, "-o", o]
+            cmd = [NVCC, *ARCH, *COMMON, *extra, *extra_all, "-c", s, "-o", o]
             if verbose:
                 print(" ".join(cmd), flush=True)
             procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))

@@ -1128,14 +1128,38 @@ int launch_part(lmm_ctx *c, const MMParams &P) {
   return LMM_OK;
 }
 
-template <int G, int MAXS, int MAXJ, int MAXV, int MAXA, int MAXLE, int MAXH>
+// GA, GB, GC: lanes per node in parts A, B, C (32 = warp per node, 16 = two nodes per warp)
+template <int GA, int GB, int GC, int MAXS, int MAXJ, int MAXV, int MAXA, int MAXLE, int MAXH>
 int launch_bucket(lmm_ctx *c, MMParams P) {
   if (P.n_list <= 0) return LMM_OK;
   int rc;
-  if ((rc = launch_part<0, G, MAXS, MAXJ, MAXV, MAXA, MAXLE, MAXH>(c, P))) return rc;
-  if ((rc = launch_part<1, G, MAXS, MAXJ, MAXV, MAXA, MAXLE, MAXH>(c, P))) return rc;
-  return launch_part<2, G, MAXS, MAXJ, MAXV, MAXA, MAXLE, MAXH>(c, P);
+  if ((rc = launch_part<0, GA, MAXS, MAXJ, MAXV, MAXA, MAXLE, MAXH>(c, P))) return rc;
+  if ((rc = launch_part<1, GB, MAXS, MAXJ, MAXV, MAXA, MAXLE, MAXH>(c, P))) return rc;
+  return launch_part<2, GC, MAXS, MAXJ, MAXV, MAXA, MAXLE, MAXH>(c, P);
 }
+// lanes per node of each bucket's parts (tuning: -DLMM_B<b>_G<A|B|C>=16|32): degree <= 8 nodes
+// go two per warp (the paper's packing of combinable work into one warp), higher degrees one
+#ifndef LMM_B0_GA
+#define LMM_B0_GA 16
+#endif
+#ifndef LMM_B0_GB
+#define LMM_B0_GB 16
+#endif
+#ifndef LMM_B0_GC
+#define LMM_B0_GC 16
+#endif
+#ifndef LMM_B1_GA
+#define LMM_B1_GA 32
+#endif
+#ifndef LMM_B1_GB
+#define LMM_B1_GB 32
+#endif
+#ifndef LMM_B1_GC
+#define LMM_B1_GC 32
+#endif
+#define LMM_B0_G LMM_B0_GA, LMM_B0_GB, LMM_B0_GC
+#define LMM_B1_G LMM_B1_GA, LMM_B1_GB, LMM_B1_GC
+#define LMM_B2_G 32, 32, 32
 
 }  // namespace
 
@@ -1198,13 +1222,13 @@ int metamesh_run(lmm_ctx *c) {
     // bucket b occupies bucket_nodes[bucket_off[b] .. bucket_off[b+1])
     P.node_list = bn + c->bucket_off[0];
     P.n_list = (int)(c->bucket_off[1] - c->bucket_off[0]);
-    if ((rc = launch_bucket<32, LMM_B0_ARGS>(c, P))) return rc;
+    if ((rc = launch_bucket<LMM_B0_G, LMM_B0_ARGS>(c, P))) return rc;
     P.node_list = bn + c->bucket_off[1];
     P.n_list = (int)(c->bucket_off[2] - c->bucket_off[1]);
-    if ((rc = launch_bucket<32, LMM_B1_ARGS>(c, P))) return rc;
+    if ((rc = launch_bucket<LMM_B1_G, LMM_B1_ARGS>(c, P))) return rc;
     P.node_list = bn + c->bucket_off[2];
     P.n_list = (int)(c->bucket_off[3] - c->bucket_off[2]);
-    if ((rc = launch_bucket<32, LMM_B2_ARGS>(c, P))) return rc;
+    if ((rc = launch_bucket<LMM_B2_G, LMM_B2_ARGS>(c, P))) return rc;
   }
   return LMM_OK;
 }
