@@ -73,9 +73,9 @@ template <int MAXS, int MAXJ, int MAXV, int MAXA, int MAXLE, int MAXH>
 struct alignas(16) WS_A : WSCore<MAXS, MAXV> {
   // side k as broadcast pairs for the two-root junction test: (wx,wx,wy,wy), (wz,wz,-e,-e)
   float4 wp[MAXS][2];
-  float jx[MAXJ], jy[MAXJ], jz[MAXJ];
+  float4 jp[MAXJ];   // junction x, y, z; .w = vertex id once clustered (roots)
   uint32_t jabc[MAXJ];
-  int jlab[MAXJ], jcid[MAXJ];
+  int jlab[MAXJ];
 };
 
 constexpr int QL = 3;   // arc-interval midpoints queued per lane and round (part B)
@@ -494,11 +494,11 @@ __device__ void part_a(cg::thread_block_tile<G> &g, WS &ws, const MMParams &P, i
       if (fe) { status = fe; break; }
       uint32_t code = (uint32_t)a | ((uint32_t)b << 8) | ((uint32_t)c << 16);
       if (v0) {
-        ws.jx[p0] = y[0].x; ws.jy[p0] = y[0].y; ws.jz[p0] = y[0].z;
+        ws.jp[p0] = make_float4(y[0].x, y[0].y, y[0].z, 0.0f);
         ws.jabc[p0] = code | (fabsf(tau[0]) <= delta ? (1u << 25) : 0u);
       }
       if (v1) {
-        ws.jx[p1] = y[1].x; ws.jy[p1] = y[1].y; ws.jz[p1] = y[1].z;
+        ws.jp[p1] = make_float4(y[1].x, y[1].y, y[1].z, 0.0f);
         ws.jabc[p1] = code | (1u << 24) | (fabsf(tau[1]) <= delta ? (1u << 25) : 0u);
       }
       nj += __popc(m0) + __popc(m1);
@@ -508,39 +508,73 @@ __device__ void part_a(cg::thread_block_tile<G> &g, WS &ws, const MMParams &P, i
 
   PHASE_MARK(2);
   // ---- 3. clustering: connected components of "junctions within delta_c" -----------
-  // (label = lowest junction index of the component; junction coordinates travel by warp
-  //  shuffles, so the O(nj^2) proximity tests touch no shared memory)
+  // (label = lowest junction index of the component).  Up to MJ junctions: one pass builds
+  // each junction's proximity mask (coordinates broadcast from shared memory), the masks
+  // are closed under union in place (monotone; clusters are small, so 1-2 sweeps), and the
+  // component minimum is the lowest set bit.  More junctions: label propagation.
   if (status == 0 && nj > 0) {
-    #pragma unroll 1
-    for (int j = lane; j < nj; j += G) ws.jlab[j] = j;
-    g.sync();
-    for (;;) {
-      bool changed = false;
+    constexpr int MJ = sizeof(ws.wp) >= 64 * sizeof(unsigned long long) ? 64 : 32;
+    unsigned long long *msk = reinterpret_cast<unsigned long long *>(&ws.wp[0][0]);   // dead after step 2
+    const bool masks = nj <= MJ;
+    if (masks) {
       #pragma unroll 1
       for (int cj = 0; cj < nj; cj += G) {
         const int j = cj + lane;
-        const bool vj = j < nj;
-        const float yx = vj ? ws.jx[j] : 0.f, yy = vj ? ws.jy[j] : 0.f, yz = vj ? ws.jz[j] : 0.f;
-        int lj = vj ? ws.jlab[j] : 0x7fffffff;
+        const float4 pj = j < nj ? ws.jp[j] : make_float4(0.f, 0.f, 0.f, 0.f);
+        unsigned long long m = 0ull;
         #pragma unroll 1
-        for (int ck = 0; ck < nj; ck += G) {
-          const int k = ck + lane;
-          const float kx = k < nj ? ws.jx[k] : 0.f, ky = k < nj ? ws.jy[k] : 0.f, kz = k < nj ? ws.jz[k] : 0.f;
-          const int lk0 = k < nj ? ws.jlab[k] : 0x7fffffff;
-          const int kn = nj - ck < G ? nj - ck : G;
-          for (int t = 0; t < kn; t++) {
-            const float x = g.shfl(kx, t), y = g.shfl(ky, t), z = g.shfl(kz, t);
-            const int lk = g.shfl(lk0, t);
-            if (lk < lj && fabsf(yx - x) <= dc && fabsf(yy - y) <= dc && fabsf(yz - z) <= dc) lj = lk;
+        for (int k = 0; k < nj; k++) {
+          const float4 pk = ws.jp[k];
+          const bool cl = fabsf(pj.x - pk.x) <= dc && fabsf(pj.y - pk.y) <= dc && fabsf(pj.z - pk.z) <= dc;
+          m |= (unsigned long long)cl << k;
+        }
+        if (j < nj) msk[j] = m;
+      }
+      g.sync();
+      for (;;) {
+        bool changed = false;
+        #pragma unroll 1
+        for (int j = lane; j < nj; j += G) {
+          const unsigned long long R = msk[j];
+          unsigned long long nr = R, bits = R & ~(1ull << j);
+          while (bits) {
+            nr |= msk[__ffsll((long long)bits) - 1];
+            bits &= bits - 1;
           }
+          if (nr != R) { msk[j] = nr; changed = true; }
         }
         g.sync();
-        if (vj && lj != ws.jlab[j]) { ws.jlab[j] = lj; changed = true; }
-        g.sync();
+        if (!g.any(changed)) break;
       }
-      if (!g.any(changed)) break;
+      #pragma unroll 1
+      for (int j = lane; j < nj; j += G) ws.jlab[j] = __ffsll((long long)msk[j]) - 1;
+    } else {
+      #pragma unroll 1
+      for (int j = lane; j < nj; j += G) ws.jlab[j] = j;
+      g.sync();
+      for (;;) {
+        bool changed = false;
+        #pragma unroll 1
+        for (int cj = 0; cj < nj; cj += G) {
+          const int j = cj + lane;
+          const bool vj = j < nj;
+          const float4 pj = vj ? ws.jp[j] : make_float4(0.f, 0.f, 0.f, 0.f);
+          int lj = vj ? ws.jlab[j] : 0x7fffffff;
+          #pragma unroll 1
+          for (int k = 0; k < nj; k++) {
+            const float4 pk = ws.jp[k];
+            const int lk = ws.jlab[k];
+            if (lk < lj && fabsf(pj.x - pk.x) <= dc && fabsf(pj.y - pk.y) <= dc && fabsf(pj.z - pk.z) <= dc) lj = lk;
+          }
+          g.sync();
+          if (vj && lj != ws.jlab[j]) { ws.jlab[j] = lj; changed = true; }
+          g.sync();
+        }
+        if (!g.any(changed)) break;
+      }
     }
-    // component roots in index order -> vertex ids
+    g.sync();
+    // component roots in index order -> vertex ids (kept in the root's .w)
     #pragma unroll 1
     for (int base = 0; base < nj; base += G) {
       int j = base + lane;
@@ -548,8 +582,9 @@ __device__ void part_a(cg::thread_block_tile<G> &g, WS &ws, const MMParams &P, i
       unsigned rm = g.ballot(root);
       int id = nc + __popc(rm & ((1u << lane) - 1u));
       if (root && id < MAXV) {
-        ws.jcid[j] = id;
-        ws.vx[id] = ws.jx[j]; ws.vy[id] = ws.jy[j]; ws.vz[id] = ws.jz[j]; ws.vmask[id] = 0u;
+        const float4 q = ws.jp[j];
+        ws.jp[j].w = __int_as_float(id);
+        ws.vx[id] = q.x; ws.vy[id] = q.y; ws.vz[id] = q.z; ws.vmask[id] = 0u;
       }
       nc += __popc(rm);
     }
@@ -561,7 +596,7 @@ __device__ void part_a(cg::thread_block_tile<G> &g, WS &ws, const MMParams &P, i
         uint32_t code = ws.jabc[j];
         uint32_t bits = (1u << (code & 0xff)) | (1u << ((code >> 8) & 0xff)) | (1u << ((code >> 16) & 0xff));
         if (code & (1u << 25)) bits |= 1u;   // strut junction at tangent length ~0: on the sphere
-        atomicOr(&ws.vmask[ws.jcid[ws.jlab[j]]], bits);
+        atomicOr(&ws.vmask[__float_as_int(ws.jp[ws.jlab[j]].w)], bits);
       }
     }
   }
@@ -1079,8 +1114,18 @@ struct PartWS<1, G, MAXS, MAXJ, MAXV, MAXA, MAXLE, MAXH> { using T = WS_B<MAXS, 
 template <int G, int MAXS, int MAXJ, int MAXV, int MAXA, int MAXLE, int MAXH>
 struct PartWS<2, G, MAXS, MAXJ, MAXV, MAXA, MAXLE, MAXH> { using T = WS_C<MAXS, MAXJ, MAXV, MAXA, MAXLE, MAXH>; };
 
+#ifndef LMM_MM_MINB_A
+#define LMM_MM_MINB_A 8
+#endif
+#ifndef LMM_MM_MINB_B
+#define LMM_MM_MINB_B 1
+#endif
+#ifndef LMM_MM_MINB_C
+#define LMM_MM_MINB_C 1
+#endif
 template <int PART, int G, int MAXS, int MAXJ, int MAXV, int MAXA, int MAXLE, int MAXH>
-__global__ void __launch_bounds__(128) metamesh_kernel(MMParams P) {
+__global__ void __launch_bounds__(128, PART == 0 ? LMM_MM_MINB_A : (PART == 1 ? LMM_MM_MINB_B : LMM_MM_MINB_C))
+metamesh_kernel(MMParams P) {
   using WS = typename PartWS<PART, G, MAXS, MAXJ, MAXV, MAXA, MAXLE, MAXH>::T;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   auto block = cg::this_thread_block();
