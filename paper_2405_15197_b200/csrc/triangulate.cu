@@ -210,8 +210,8 @@ __global__ void k_band_merge(TriParams P) {
   const float a0 = A.phs;
   // rotation of ring B: its first point with the smallest angle relative to A's start
   int kB = 0;
+  float best = 0.0f;
   {
-    float best = 0.0f;
     for (int j = 0; j < nB; j++) {
       float r = wrap_rel(B.key(j), a0);
       if (j == 0 || r < best) { best = r; kB = j; }
@@ -219,29 +219,36 @@ __global__ void k_band_merge(TriParams P) {
     P.band[s].z = kB;
     rq[0] = make_float4(__int_as_float(nA), __int_as_float(nB), __int_as_float(kB), __int_as_float(LA.x | (LA.y << 16)));
   }
-  const float b0 = wrap_rel(B.key(kB), a0);
+  const float b0 = best;   // = wrap_rel(B.key(kB), a0)
   const int64_t base = P.strut_off[s];
-  const int64_t end = base + nA + nB;
+  const int n = nA + nB;
+  const int sb = (int)(base & 31);
+  uint32_t *mw = P.mbits + (base >> 5);
+  int *ma = P.macc + (base >> 5);
   int i = 0, j = 0;
+  int jb = 1 + kB >= nB ? 1 + kB - nB : 1 + kB;   // ring-B index of B's next point
   float an = (1 < nA) ? __fsub_rn(A.key(1), a0) : LMM_TWO_PI_F;
-  float bn = (1 < nB) ? wrap_rel(B.key((1 + kB) % nB), a0) : __fadd_rn(b0, LMM_TWO_PI_F);
+  float bn = (1 < nB) ? wrap_rel(B.key(jb), a0) : __fadd_rn(b0, LMM_TWO_PI_F);
   uint32_t word = 0;
-  for (int64_t t = base; t < end; t++) {
-    if ((t & 31) == 0) P.macc[t >> 5] = i;
-    bool advA = i < nA && (j == nB || an <= bn);
+  for (int q = 0; q < n; q++) {
+    const int bit = sb + q;
+    if ((bit & 31) == 0) ma[bit >> 5] = i;
+    const bool advA = i < nA && (j == nB || an <= bn);
     if (advA) {
-      word |= 1u << (t & 31);
+      word |= 1u << (bit & 31);
       i++;
       if (i < nA) an = (i + 1 < nA) ? __fsub_rn(A.key(i + 1), a0) : LMM_TWO_PI_F;
     } else {
       j++;
-      if (j < nB) bn = (j + 1 < nB) ? wrap_rel(B.key((j + 1 + kB) % nB), a0) : __fadd_rn(b0, LMM_TWO_PI_F);
+      if (++jb == nB) jb = 0;
+      if (j < nB) bn = (j + 1 < nB) ? wrap_rel(B.key(jb), a0) : __fadd_rn(b0, LMM_TWO_PI_F);
     }
-    if ((t & 31) == 31 || t + 1 == end) {
-      int64_t w = t >> 5;
-      bool full = (w << 5) >= base && (w << 5) + 31 < end;
-      if (full) P.mbits[w] = word;
-      else if (word) atomicOr(&P.mbits[w], word);
+    if ((bit & 31) == 31 || q + 1 == n) {
+      // a word is the band's alone when it starts at or after the band start and ends inside it
+      const int w = bit >> 5;
+      const bool own = (w << 5) >= sb && (w << 5) + 31 <= sb + n - 1;
+      if (own) mw[w] = word;
+      else if (word) atomicOr(&mw[w], word);
       word = 0;
     }
   }
