@@ -71,7 +71,9 @@ struct lmm_ctx {
   DevBuf stage[2];   // device staging for host output
   void *pinned[2] = {nullptr, nullptr};
   size_t pinned_bytes = 0;
-  cudaEvent_t stage_ev[2] = {nullptr, nullptr};
+  cudaEvent_t stage_ev[2] = {nullptr, nullptr};   // staging buffer b free again (copy done)
+  cudaEvent_t emit_ev[2] = {nullptr, nullptr};    // staging buffer b filled (emit done)
+  cudaStream_t copy_stream = nullptr;             // device -> host copies of host output
   // timing
   bool timing = false;
   double k_ms[LMM_K_NCLASSES] = {0};
