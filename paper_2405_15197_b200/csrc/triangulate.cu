@@ -533,14 +533,6 @@ __device__ __forceinline__ void put_second(uint32_t *d, const uint32_t *g) {
   d[24] = g[11] >> 16;
 }
 
-// one record through 2-byte stores (unaligned hole triangles)
-__device__ __forceinline__ void put_rec16(unsigned char *dst, const uint32_t *f) {
-  uint16_t *d = reinterpret_cast<uint16_t *>(dst);
-#pragma unroll
-  for (int i = 0; i < 12; i++) { d[2 * i] = (uint16_t)(f[i] & 0xffffu); d[2 * i + 1] = (uint16_t)(f[i] >> 16); }
-  d[24] = 0;
-}
-
 // staged group bytes [b0, b1) -> dst + [b0, b1), dst 16-byte aligned: 2-byte head up to the
 // first 16-byte boundary and 2-byte tail through the LSU, the 16-byte-aligned body as one
 // TMA bulk copy (cp.async.bulk.global.shared::cta) issued by lane 0 -- the body bypasses
@@ -802,21 +794,34 @@ __device__ void emit_hole(const TriParams &P, WarpRing &w, int g, int64_t first,
   }
   __syncwarp();
   const int mb = (int)(ta - hb), me = (int)(tb - hb);
-  for (int m0 = mb; m0 < me; m0 += WIN) {
-    const int m1 = m0 + WIN < me ? m0 + WIN : me;
+  for (int m0 = mb, m1; m0 < me; m0 = m1) {
+    m1 = m0 - (int)((hb + m0 - first) & 7) + WIN;   // windows end on the 8-triangle grid
+    m1 = m1 < me ? m1 : me;
     for (int k = lane; k <= m1 - m0; k += 32) {
       int idx = m0 + k;
       put_point(w, k, ring_point(w, 0, RH, idx >= M ? idx - M : idx));
     }
     __syncwarp();
-    for (int mm = m0; mm < m1; mm += 32) {
-      const int m = mm + lane;
-      if (m < m1) {
-        int k = m - m0;
+    // fan triangles (b_project, P_m, P_m+1) in aligned groups, two records per lane, leaving
+    // through the staging buffer like the band groups
+    for (int gq = m0 - (int)((hb + m0 - first) & 7); gq < m1; gq += GRP) {
+      const int qa = gq + 2 * lane, qb2 = qa + 1;
+      const int lo_q = gq > m0 ? gq : m0;
+      const int hi_q = gq + GRP < m1 ? gq + GRP : m1;
+      const bool va = qa >= lo_q && qa < hi_q, vb = qb2 >= lo_q && qb2 < hi_q;
+      stage_wait(lane);
+      uint32_t *d = reinterpret_cast<uint32_t *>(w.stage) + 25 * lane;   // records 2l, 2l+1
+      if (va) {
         uint32_t f[12];
-        tri_words(bp, get_point(w, k), get_point(w, k + 1), f);
-        put_rec16(out + (hb + m - first) * REC, f);
+        tri_words(bp, get_point(w, qa - m0), get_point(w, qa - m0 + 1), f);
+        put_first(d, f);
       }
+      if (vb) {
+        uint32_t f[12];
+        tri_words(bp, get_point(w, qb2 - m0), get_point(w, qb2 - m0 + 1), f);
+        put_second(d, f);
+      }
+      flush_group(w, (lo_q - gq) * REC, (hi_q - gq) * REC, out + (hb + gq - first) * REC, lane);
     }
     __syncwarp();
   }
