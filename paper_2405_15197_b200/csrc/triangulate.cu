@@ -167,21 +167,38 @@ __global__ void k_band_count(TriParams P) {
   P.band_cnt[s] = (int64_t)nA + nB;
 }
 
-// sequential cursor over a ring's stitch keys (point index increases; wraps once)
-struct KeyCursor {
+// Sequential cursor over a ring's stitch keys: key(idx) = phs_e + (idx - cum_e) * (dph_e / N_e)
+// of the last entry e with cum_e <= idx; past the last entry's end the
+// last entry is extrapolated.  Walked forward one point at a time (rem = points left in the
+// current entry), re-seeked only where a ring wraps.
+struct SeqKey {
   const LoopRec *le;
-  int cnt, e, cum, N;
+  int cnt, e, jl, rem;
   float phs, step;
-  __device__ void load(int ee) {
+  __device__ void enter(int ee, int j0) {
     e = ee;
-    LoopRec L = le[e];
-    cum = L.cum; N = le_N(L.arc_fwd); phs = L.phs;
-    step = __fdiv_rn(L.dph, (float)N);   // key_at's step, hoisted (same bits)
+    const LoopRec L = le[e];
+    const int N = le_N(L.arc_fwd);
+    phs = L.phs;
+    step = __fdiv_rn(L.dph, (float)N);   // same bits as dividing at every key
+    jl = j0;
+    rem = N - j0;
   }
-  __device__ float key(int idx) {
-    if (idx < cum) load(0);
-    while (idx >= cum + N && e + 1 < cnt) load(e + 1);
-    return __fadd_rn(phs, __fmul_rn((float)(idx - cum), step));
+  __device__ void seek(int idx) {
+    int ee = 0, cum = 0;
+    for (;;) {
+      const LoopRec L = le[ee];
+      const int N = le_N(L.arc_fwd);
+      cum = L.cum;
+      if (idx < cum + N || ee + 1 >= cnt) break;
+      ee++;
+    }
+    enter(ee, idx - cum);
+  }
+  __device__ float key() const { return __fadd_rn(phs, __fmul_rn((float)jl, step)); }
+  __device__ void next() {
+    jl++;
+    if (--rem == 0 && e + 1 < cnt) enter(e + 1, 0);
   }
 };
 
@@ -204,22 +221,24 @@ __global__ void k_band_merge(TriParams P) {
     rq[2] = make_float4(__uint_as_float((unsigned)(offB + e.y)), na.x, na.y, na.z);
     rq[3] = make_float4(nb.x, nb.y, nb.z, 0.0f);
   }
-  KeyCursor A, B;
-  A.le = P.loop + lbase(P.csr_off, e.x) + LA.x; A.cnt = LA.y; A.load(0);
-  B.le = P.loop + lbase(P.csr_off, e.y) + LB.x; B.cnt = LB.y; B.load(0);
-  const float a0 = A.phs;
+  SeqKey A, B;
+  A.le = P.loop + lbase(P.csr_off, e.x) + LA.x; A.cnt = LA.y;
+  B.le = P.loop + lbase(P.csr_off, e.y) + LB.x; B.cnt = LB.y;
+  A.enter(0, 0);
+  const float a0 = A.phs;     // ring A first entry phi
   // rotation of ring B: its first point with the smallest angle relative to A's start
   int kB = 0;
   float best = 0.0f;
-  {
-    for (int j = 0; j < nB; j++) {
-      float r = wrap_rel(B.key(j), a0);
-      if (j == 0 || r < best) { best = r; kB = j; }
-    }
-    P.band[s].z = kB;
-    rq[0] = make_float4(__int_as_float(nA), __int_as_float(nB), __int_as_float(kB), __int_as_float(LA.x | (LA.y << 16)));
+  B.enter(0, 0);
+  for (int j = 0; j < nB; j++, B.next()) {
+    const float r = wrap_rel(B.key(), a0);
+    if (j == 0 || r < best) { best = r; kB = j; }
   }
-  const float b0 = best;   // = wrap_rel(B.key(kB), a0)
+  P.band[s].z = kB;
+  rq[0] = make_float4(__int_as_float(nA), __int_as_float(nB), __int_as_float(kB), __int_as_float(LA.x | (LA.y << 16)));
+  const float b0 = best;   // = wrap_rel(key_B(kB), a0)
+  // merge: an = key_A(i + 1) - a0 (2 pi after the last point), bn = wrap(key_B(kB + j + 1)) (b0 +
+  // 2 pi after the last); triangle q advances ring A iff i < nA and (j == nB or an <= bn)
   const int64_t base = P.strut_off[s];
   const int n = nA + nB;
   const int sb = (int)(base & 31);
@@ -227,31 +246,36 @@ __global__ void k_band_merge(TriParams P) {
   int *ma = P.macc + (base >> 5);
   int i = 0, j = 0;
   int jb = 1 + kB >= nB ? 1 + kB - nB : 1 + kB;   // ring-B index of B's next point
-  float an = (1 < nA) ? __fsub_rn(A.key(1), a0) : LMM_TWO_PI_F;
-  float bn = (1 < nB) ? wrap_rel(B.key(jb), a0) : __fadd_rn(b0, LMM_TWO_PI_F);
-  uint32_t word = 0;
-  for (int q = 0; q < n; q++) {
-    const int bit = sb + q;
-    if ((bit & 31) == 0) ma[bit >> 5] = i;
-    const bool advA = i < nA && (j == nB || an <= bn);
-    if (advA) {
-      word |= 1u << (bit & 31);
-      i++;
-      if (i < nA) an = (i + 1 < nA) ? __fsub_rn(A.key(i + 1), a0) : LMM_TWO_PI_F;
-    } else {
-      j++;
-      if (++jb == nB) jb = 0;
-      if (j < nB) bn = (j + 1 < nB) ? wrap_rel(B.key(jb), a0) : __fadd_rn(b0, LMM_TWO_PI_F);
+  if (nA > 1) A.seek(1);
+  if (nB > 1) B.seek(jb);
+  float an = (1 < nA) ? __fsub_rn(A.key(), a0) : LMM_TWO_PI_F;
+  float bn = (1 < nB) ? wrap_rel(B.key(), a0) : __fadd_rn(b0, LMM_TWO_PI_F);
+  const int nw = (sb + n + 31) >> 5;
+  for (int w = 0; w < nw; w++) {
+    const int q0 = w == 0 ? 0 : 32 * w - sb;
+    const int q1 = 32 * (w + 1) - sb < n ? 32 * (w + 1) - sb : n;
+    if (w > 0) ma[w] = i;   // A-advances before the word's first bit
+    uint32_t word = 0;
+    for (int q = q0; q < q1; q++) {
+      if (i < nA && (j == nB || an <= bn)) {
+        word |= 1u << ((sb + q) & 31);
+        i++;
+        if (i < nA) {
+          if (i + 1 < nA) { A.next(); an = __fsub_rn(A.key(), a0); }
+          else an = LMM_TWO_PI_F;
+        }
+      } else {
+        j++;
+        if (++jb == nB) { jb = 0; B.enter(0, 0); } else if (j < nB) B.next();
+        if (j < nB) bn = (j + 1 < nB) ? wrap_rel(B.key(), a0) : __fadd_rn(b0, LMM_TWO_PI_F);
+      }
     }
-    if ((bit & 31) == 31 || q + 1 == n) {
-      // a word is the band's alone when it starts at or after the band start and ends inside it
-      const int w = bit >> 5;
-      const bool own = (w << 5) >= sb && (w << 5) + 31 <= sb + n - 1;
-      if (own) mw[w] = word;
-      else if (word) atomicOr(&mw[w], word);
-      word = 0;
-    }
+    // a word is the band's alone when it starts at or after the band start and ends inside it
+    const bool own = 32 * w >= sb && 32 * w + 31 <= sb + n - 1;
+    if (own) mw[w] = word;
+    else if (word) atomicOr(&mw[w], word);
   }
+  if (sb == 0) ma[0] = 0;
 }
 
 __global__ void k_node_nholes(const int4 *hdr, int64_t N, const uint8_t *mask, int *nh) {
