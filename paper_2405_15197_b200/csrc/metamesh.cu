@@ -82,6 +82,7 @@ constexpr int QL = 3;   // arc-interval midpoints queued per lane and round (par
 
 template <int MAXS, int MAXJ, int MAXV, int MAXA, int MAXLE, int MAXH>
 struct alignas(16) WS_B : WSCore<MAXS, MAXV> {
+  float4 wp[MAXS][2];   // side k as broadcast pairs (wx,wx,wy,wy), (wz,wz,-e,-e) for packed tests
   ArcRec arcs[MAXA];
   float atmid[MAXA];
   int adrop[MAXA];
@@ -635,6 +636,13 @@ __device__ void part_b(cg::thread_block_tile<G> &g, WS &ws, const MMParams &P, i
   load_sides<G>(g, ws, P.side, off, d);
   load_verts<G>(g, ws, vslab, nv);
   g.sync();
+  #pragma unroll 1
+  for (int k = 1 + lane; k <= d; k += G) {
+    const float4 q = ws.w4[k];
+    ws.wp[k][0] = make_float4(q.x, q.x, q.y, q.y);
+    ws.wp[k][1] = make_float4(q.z, q.z, -q.w, -q.w);
+  }
+  g.sync();
 #ifdef LMM_PHASE_TIMING
   long long ph_t = clock64();
 #define PHASE_MARK(k)                                                    \
@@ -763,15 +771,27 @@ __device__ void part_b(cg::thread_block_tile<G> &g, WS &ws, const MMParams &P, i
         PHASE_MARK(10);
         // (2) queued midpoints: end-circle points strictly exposed (h_m - 0 > -delta
         // rejects, as valid_sphere_pt), strut points within the tolerance (valid_strut_pt)
-        for (int qi = lane; qi < qtot; qi += G) {
-          const uint32_t m = qm[qi];
-          const bool sph = m >> 31;
-          const f3 y = F3(qx[qi], qy[qi], qz[qi]);
-          const float tau = __int_as_float(qt[qi]);
-          const float thr = sph ? -delta : delta;
-          bool ok = sph || !(tau < -delta);
-          for (int mm = 1; mm <= d; mm++) ok = ok && (((m >> mm) & 1u) || !(nd.hs(mm, y) - tau > thr));
-          qok[qi] = ok;
+        // two midpoints per lane in packed f32x2 operations: each lane of the pair rounds like
+        // the scalar hs(m, y) - tau (h - e as h + (-e), h - tau as h + (-tau))
+        for (int qi = lane; qi < qtot; qi += 2 * G) {
+          const int qj = qi + G < qtot ? qi + G : qi;
+          const uint32_t m0 = qm[qi], m1 = qm[qj];
+          const bool s0 = m0 >> 31, s1 = m1 >> 31;
+          const float t0 = __int_as_float(qt[qi]), t1 = __int_as_float(qt[qj]);
+          const float th0 = s0 ? -delta : delta, th1 = s1 ? -delta : delta;
+          bool ok0 = s0 || !(t0 < -delta), ok1 = s1 || !(t1 < -delta);
+          const float2 Yx = make_float2(qx[qi], qx[qj]), Yy = make_float2(qy[qi], qy[qj]), Yz = make_float2(qz[qi], qz[qj]);
+          const float2 nT = make_float2(-t0, -t1);
+          for (int mm = 1; mm <= d; mm++) {
+            const float4 p0 = ws.wp[mm][0], p1 = ws.wp[mm][1];
+            float2 h = add2(mul2(make_float2(p0.x, p0.y), Yx), mul2(make_float2(p0.z, p0.w), Yy));
+            h = add2(h, mul2(make_float2(p1.x, p1.y), Yz));
+            h = add2(add2(h, make_float2(p1.z, p1.w)), nT);
+            ok0 = ok0 && (((m0 >> mm) & 1u) || !(h.x > th0));
+            ok1 = ok1 && (((m1 >> mm) & 1u) || !(h.y > th1));
+          }
+          qok[qi] = ok0;
+          if (qj != qi) qok[qj] = ok1;
         }
         g.sync();
         PHASE_MARK(11);
@@ -1118,7 +1138,7 @@ struct PartWS<2, G, MAXS, MAXJ, MAXV, MAXA, MAXLE, MAXH> { using T = WS_C<MAXS, 
 #define LMM_MM_MINB_A 8
 #endif
 #ifndef LMM_MM_MINB_B
-#define LMM_MM_MINB_B 1
+#define LMM_MM_MINB_B 5
 #endif
 #ifndef LMM_MM_MINB_C
 #define LMM_MM_MINB_C 1
