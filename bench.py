@@ -431,6 +431,9 @@ def main():
         res["config"]["triangles_per_ce"] = {str(k): int(v) for k, v in per_ce.items()}
         res["config"]["metamesh"] = "built once before the timed region (multi-resolution reuse)"
         res["metamesh_struts_per_s"] = None
+    if one_gpu and world > 1:
+        res["config"]["note"] = (f"{world} ranks time-sharing cuda:0 over gloo (LMM_BENCH_ONE_GPU=1): a functional "
+                                 "check of the multi-rank path, not a scaling number")
     if args.config.startswith("stoch"):
         dh = [int(x) for x in st["degree_hist"]]
         res["config"]["degree_hist"] = {str(d): c for d, c in enumerate(dh) if c}
