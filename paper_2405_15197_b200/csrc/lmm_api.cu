@@ -105,14 +105,16 @@ LMM_API void lmm_destroy(lmm_ctx *c) {
   if (!c) return;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream); else cudaDeviceSynchronize();
-  if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
+  for (int i = 0; i < 2; i++)
+    if (c->copy_stream[i]) cudaStreamSynchronize(c->copy_stream[i]);
   free_all(c);
   for (int i = 0; i < 2; i++) {
     if (c->pinned[i]) cudaFreeHost(c->pinned[i]);
     if (c->stage_ev[i]) cudaEventDestroy(c->stage_ev[i]);
     if (c->emit_ev[i]) cudaEventDestroy(c->emit_ev[i]);
   }
-  if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+  for (int i = 0; i < 2; i++)
+    if (c->copy_stream[i]) cudaStreamDestroy(c->copy_stream[i]);
   resolve_timers(c);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   if (c->pinned_scalar) cudaFreeHost(c->pinned_scalar);
@@ -257,11 +259,11 @@ LMM_API int lmm_write_triangles(lmm_ctx *c, int64_t first, int64_t count, void *
   // the emission of chunk b + 1
   const int64_t CH = 1ll << 22;   // triangles per chunk (200 MiB)
   int rc;
-  if (!c->copy_stream) CUDA_TRY(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
   for (int i = 0; i < 2; i++) {
     if ((rc = dev_alloc(c->stage[i], (size_t)CH * 50))) return rc;
     if (!c->stage_ev[i]) CUDA_TRY(cudaEventCreateWithFlags(&c->stage_ev[i], cudaEventDisableTiming));
     if (!c->emit_ev[i]) CUDA_TRY(cudaEventCreateWithFlags(&c->emit_ev[i], cudaEventDisableTiming));
+    if (!c->copy_stream[i]) CUDA_TRY(cudaStreamCreateWithFlags(&c->copy_stream[i], cudaStreamNonBlocking));
   }
   unsigned char *dst = (unsigned char *)out;
   int b = 0;
@@ -271,12 +273,12 @@ LMM_API int lmm_write_triangles(lmm_ctx *c, int64_t first, int64_t count, void *
     if (used[b]) CUDA_TRY(cudaStreamWaitEvent(c->stream, c->stage_ev[b], 0));   // buffer b copied out
     if ((rc = triangulate_emit(c, first + t, n, c->stage[b].p, c->stream))) return rc;
     CUDA_TRY(cudaEventRecord(c->emit_ev[b], c->stream));
-    CUDA_TRY(cudaStreamWaitEvent(c->copy_stream, c->emit_ev[b], 0));
-    CUDA_TRY(cudaMemcpyAsync(dst + t * 50, c->stage[b].p, (size_t)n * 50, cudaMemcpyDeviceToHost, c->copy_stream));
-    CUDA_TRY(cudaEventRecord(c->stage_ev[b], c->copy_stream));
+    CUDA_TRY(cudaStreamWaitEvent(c->copy_stream[b], c->emit_ev[b], 0));
+    CUDA_TRY(cudaMemcpyAsync(dst + t * 50, c->stage[b].p, (size_t)n * 50, cudaMemcpyDeviceToHost, c->copy_stream[b]));
+    CUDA_TRY(cudaEventRecord(c->stage_ev[b], c->copy_stream[b]));
     used[b] = true;
   }
-  CUDA_TRY(cudaStreamSynchronize(c->copy_stream));
+  for (int i = 0; i < 2; i++) CUDA_TRY(cudaStreamSynchronize(c->copy_stream[i]));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
   return LMM_OK;
 }

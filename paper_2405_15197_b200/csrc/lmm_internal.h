@@ -73,7 +73,7 @@ struct lmm_ctx {
   size_t pinned_bytes = 0;
   cudaEvent_t stage_ev[2] = {nullptr, nullptr};   // staging buffer b free again (copy done)
   cudaEvent_t emit_ev[2] = {nullptr, nullptr};    // staging buffer b filled (emit done)
-  cudaStream_t copy_stream = nullptr;             // device -> host copies of host output
+  cudaStream_t copy_stream[2] = {nullptr, nullptr};   // device -> host copies of host output (one per staging buffer)
   // timing
   bool timing = false;
   double k_ms[LMM_K_NCLASSES] = {0};
