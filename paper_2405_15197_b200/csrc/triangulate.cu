@@ -382,7 +382,8 @@ __device__ __forceinline__ void put_rec(unsigned char *dst, f3 a, f3 b, f3 c) {
 // that intersect [first, first+count).  A band's ring data -- both rings' loop entries and
 // arc records -- sits in shared memory; every ring point is computed once, in parallel
 // (the entry of a point comes from a ballot/redux count of the entry starts below it).
-// Bands whose rings exceed PMAX points are walked in windows of WIN merge steps instead.
+// Bands whose rings exceed the point cache (pcap points) are walked in windows of pcap - 2
+// merge steps instead.
 // Triangles then go in groups of 64 whose output offset is 16-byte aligned: lane l
 // assembles records 2l and 2l+1 (100 bytes = 25 aligned words), its ring positions
 // following from ballot prefix-popcounts of the merge bits; the group leaves the per-warp
@@ -394,18 +395,26 @@ __device__ __forceinline__ void put_rec(unsigned char *dst, f3 a, f3 b, f3 c) {
 // and arc records (after its last group).  No registers are held across a band and no
 // block-level barriers are used.
 constexpr int EW = EMIT_T / 32;   // warps per CTA
-constexpr int PMAX = 160;         // ring points cached per band (both rings)
-constexpr int WIN = PMAX - 2;     // merge steps per window of a band with more points
+constexpr int PCAP_MIN = 160;     // ring points cached per band (both rings), runtime-sized
+constexpr int PCAP_MAX = 640;     //   from the mean band size (triangulate_emit)
 constexpr int GRP = 56;           // triangles per aligned group (2800 B; 28 lanes x 2 records)
 constexpr int MAXRE = 32;         // ring entries per ring (>= MAXLOOP of the meta-mesh)
 constexpr int MAXRA = 10;         // arc records cached per ring
 
+// per-warp shared memory: fixed part, then the point cache (pcap x float2, pcap x float)
 struct __align__(16) WarpRing {
   ArcRec arc[2][MAXRA];
   LoopRec le[2][MAXRE];   // loop entries (arc | fwd | N, phs, dph, cum); holes: arc_fwd, cum
-  float2 pxy[PMAX];
-  float pz[PMAX];
   uint4 stage[GRP * REC / 16];
+};
+__host__ __device__ constexpr int ring_bytes(int pcap) {
+  return (int)((sizeof(WarpRing) + (size_t)pcap * 12 + 15) / 16 * 16);
+}
+// the point cache of one warp: xy pairs and z, capacity cap (cap - 2 merge steps per window)
+struct Pts {
+  float2 *xy;
+  float *z;
+  int cap;
 };
 
 template <int BYTES>
@@ -513,8 +522,8 @@ __device__ __forceinline__ f3 ring_point_formula(const WarpRing &w, int r, const
             R.oz + fmaf(A.az, sn, fmaf(A.bz, cs, A.oz)));
 }
 
-__device__ __forceinline__ void put_point(WarpRing &w, int k, f3 p) { w.pxy[k] = make_float2(p.x, p.y); w.pz[k] = p.z; }
-__device__ __forceinline__ f3 get_point(const WarpRing &w, int k) { const float2 q = w.pxy[k]; return F3(q.x, q.y, w.pz[k]); }
+__device__ __forceinline__ void put_point(const Pts &pt, int k, f3 p) { pt.xy[k] = make_float2(p.x, p.y); pt.z[k] = p.z; }
+__device__ __forceinline__ f3 get_point(const Pts &pt, int k) { const float2 q = pt.xy[k]; return F3(q.x, q.y, pt.z[k]); }
 
 // A-advances of band [base, ...) before triangle t
 __device__ __forceinline__ int merge_rank(const TriParams &P, int64_t base, int64_t t) {
@@ -596,7 +605,7 @@ __device__ __forceinline__ void flush_group(WarpRing &w, int b0, int b1, unsigne
 // nA + 1 + j (j = 0..nB, B_j = ring-B point (j + kB) mod nB), so triangle positions need
 // no wrapping.  The band's merge-bit words are held one per lane.
 template <class Prefetch>
-__device__ void emit_band_whole(const TriParams &P, WarpRing &w, const RingRef &RA, const RingRef &RB,
+__device__ void emit_band_whole(const TriParams &P, WarpRing &w, const Pts &pt, const RingRef &RA, const RingRef &RB,
                                 int64_t base, int nA, int nB, int kB, int qb, int qe, int64_t first,
                                 unsigned char *out, int lane, Prefetch &prefetch) {
   const int oB = nA + 1;
@@ -629,14 +638,14 @@ __device__ void emit_band_whole(const TriParams &P, WarpRing &w, const RingRef &
       if (k < nA + nB) {
         if (ec < RA.cnt) {
           const f3 p = ring_point_formula(w, 0, RA, ec, k);
-          put_point(w, k, p);
-          if (k == 0) put_point(w, nA, p);
+          put_point(pt, k, p);
+          if (k == 0) put_point(pt, nA, p);
         } else {
           const int idx = k - nA;
           const f3 p = ring_point_formula(w, 1, RB, ec - RA.cnt, idx);
           const int jr = idx - kB + (idx < kB ? nB : 0);
-          put_point(w, oB + jr, p);
-          if (jr == 0) put_point(w, oB + nB, p);
+          put_point(pt, oB + jr, p);
+          if (jr == 0) put_point(pt, oB + nB, p);
         }
       }
     }
@@ -650,12 +659,12 @@ __device__ void emit_band_whole(const TriParams &P, WarpRing &w, const RingRef &
         const f3 p = F3(R.ox + q.x, R.oy + q.y, R.oz + q.z);
         const int idx = w.le[r][lane].cum;
         if (r == 0) {
-          put_point(w, idx, p);
-          if (idx == 0) put_point(w, nA, p);
+          put_point(pt, idx, p);
+          if (idx == 0) put_point(pt, nA, p);
         } else {
           const int jr = idx - kB + (idx < kB ? nB : 0);
-          put_point(w, oB + jr, p);
-          if (jr == 0) put_point(w, oB + nB, p);
+          put_point(pt, oB + jr, p);
+          if (jr == 0) put_point(pt, oB + nB, p);
         }
       }
     }
@@ -684,17 +693,17 @@ __device__ void emit_band_whole(const TriParams &P, WarpRing &w, const RingRef &
       // state before the lane's first valid step: A_i, B_j; each triangle (A_i, c, B_j)
       // advances one ring onto its new point c
       int i = ia, j = (va ? qa : qb2) - ia;
-      f3 pA = get_point(w, i), pB = get_point(w, oB + j);
+      f3 pA = get_point(pt, i), pB = get_point(pt, oB + j);
       uint32_t *d = reinterpret_cast<uint32_t *>(w.stage) + 25 * lane;   // records 2l, 2l+1
       if (va) {
-        const f3 c = get_point(w, aa ? i + 1 : oB + j + 1);
+        const f3 c = get_point(pt, aa ? i + 1 : oB + j + 1);
         uint32_t f[12];
         tri_words(pA, c, pB, f);
         put_first(d, f);
         if (aa) { pA = c; i++; } else { pB = c; j++; }
       }
       if (vb) {
-        const f3 c = get_point(w, ab ? i + 1 : oB + j + 1);
+        const f3 c = get_point(pt, ab ? i + 1 : oB + j + 1);
         uint32_t g[12];
         tri_words(pA, c, pB, g);
         put_second(d, g);
@@ -708,7 +717,7 @@ __device__ void emit_band_whole(const TriParams &P, WarpRing &w, const RingRef &
 }
 
 template <class Prefetch>
-__device__ void emit_band(const TriParams &P, WarpRing &w, const BandRec &H, int64_t base, int64_t first, int64_t last,
+__device__ void emit_band(const TriParams &P, WarpRing &w, const Pts &pt, const BandRec &H, int64_t base, int64_t first, int64_t last,
                           unsigned char *out, int lane, Prefetch prefetch) {
   const int nA = H.nA, nB = H.nB, kB = H.kB;
   const int64_t ta = base > first ? base : first;
@@ -723,14 +732,14 @@ __device__ void emit_band(const TriParams &P, WarpRing &w, const BandRec &H, int
   RB.ox = H.obx; RB.oy = H.oby; RB.oz = H.obz; RB.cnt = rec_cnt(H.lBc);
   const int qb = (int)(ta - base), qe = (int)(tb - base);
   prefetch(0);
-  if (nA + nB + 2 <= PMAX && RA.cnt <= MAXRA && RB.cnt <= MAXRA) {
-    emit_band_whole(P, w, RA, RB, base, nA, nB, kB, qb, qe, first, out, lane, prefetch);
+  if (nA + nB + 2 <= pt.cap && RA.cnt <= MAXRA && RB.cnt <= MAXRA) {
+    emit_band_whole(P, w, pt, RA, RB, base, nA, nB, kB, qb, qe, first, out, lane, prefetch);
     return;
   }
   // windowed: the ring data stays in use to the end, the next band's stages follow it
   const unsigned lt = (1u << lane) - 1u;
   for (int q0 = qb, q1; q0 < qe; q0 = q1) {
-    q1 = q0 - (int)((base + q0 - first) & 7) + WIN;   // windows end on the 8-triangle grid
+    q1 = q0 - (int)((base + q0 - first) & 7) + pt.cap - 2;   // windows end on the 8-triangle grid
     q1 = q1 < qe ? q1 : qe;
     int i0 = 0, i1 = 0;
     if (lane == 0) i0 = merge_rank(P, base, base + q0);
@@ -748,14 +757,14 @@ __device__ void emit_band(const TriParams &P, WarpRing &w, const BandRec &H, int
       idx = idx >= n ? idx - n : idx;
       idx = idx >= n ? idx - n : idx;
       f3 p = r ? ring_point(w, 1, RB, idx) : ring_point(w, 0, RA, idx);
-      put_point(w, k, p);
+      put_point(pt, k, p);
     }
     __syncwarp();
     // the record of step q is the triangle (A_i, A_i+1, B_j) or (A_i, B_j+1, B_j)
     auto tri = [&](int q, int i, bool advA, uint32_t *f) {
       const int pa = i - i0, pb = na + (q - i - j0);
       const int pc = advA ? pa + 1 : pb + 1;
-      tri_words(get_point(w, pa), get_point(w, pc), get_point(w, pb), f);
+      tri_words(get_point(pt, pa), get_point(pt, pc), get_point(pt, pb), f);
     };
     int irun = i0;
     for (int gq = q0 - (int)((base + q0 - first) & 7); gq < q1; gq += GRP) {
@@ -785,7 +794,7 @@ __device__ void emit_band(const TriParams &P, WarpRing &w, const BandRec &H, int
   prefetch(3);
 }
 
-__device__ void emit_hole(const TriParams &P, WarpRing &w, int g, int64_t first, int64_t last,
+__device__ void emit_hole(const TriParams &P, WarpRing &w, const Pts &pt, int g, int64_t first, int64_t last,
                           unsigned char *out, int lane) {
   const int64_t hb = P.n_tri_band + P.hole_off[g];
   const int M = P.hole_M[g];
@@ -819,11 +828,11 @@ __device__ void emit_hole(const TriParams &P, WarpRing &w, int g, int64_t first,
   __syncwarp();
   const int mb = (int)(ta - hb), me = (int)(tb - hb);
   for (int m0 = mb, m1; m0 < me; m0 = m1) {
-    m1 = m0 - (int)((hb + m0 - first) & 7) + WIN;   // windows end on the 8-triangle grid
+    m1 = m0 - (int)((hb + m0 - first) & 7) + pt.cap - 2;   // windows end on the 8-triangle grid
     m1 = m1 < me ? m1 : me;
     for (int k = lane; k <= m1 - m0; k += 32) {
       int idx = m0 + k;
-      put_point(w, k, ring_point(w, 0, RH, idx >= M ? idx - M : idx));
+      put_point(pt, k, ring_point(w, 0, RH, idx >= M ? idx - M : idx));
     }
     __syncwarp();
     // fan triangles (b_project, P_m, P_m+1) in aligned groups, two records per lane, leaving
@@ -837,12 +846,12 @@ __device__ void emit_hole(const TriParams &P, WarpRing &w, int g, int64_t first,
       uint32_t *d = reinterpret_cast<uint32_t *>(w.stage) + 25 * lane;   // records 2l, 2l+1
       if (va) {
         uint32_t f[12];
-        tri_words(bp, get_point(w, qa - m0), get_point(w, qa - m0 + 1), f);
+        tri_words(bp, get_point(pt, qa - m0), get_point(pt, qa - m0 + 1), f);
         put_first(d, f);
       }
       if (vb) {
         uint32_t f[12];
-        tri_words(bp, get_point(w, qb2 - m0), get_point(w, qb2 - m0 + 1), f);
+        tri_words(bp, get_point(pt, qb2 - m0), get_point(pt, qb2 - m0 + 1), f);
         put_second(d, f);
       }
       flush_group(w, (lo_q - gq) * REC, (hi_q - gq) * REC, out + (hb + gq - first) * REC, lane);
@@ -853,12 +862,17 @@ __device__ void emit_hole(const TriParams &P, WarpRing &w, int g, int64_t first,
 
 // units: bands [s0, s1) then holes [g0, g1) intersecting [first, last)
 __global__ void __launch_bounds__(EMIT_T, 8) k_emit(TriParams P, int64_t first, int64_t count, unsigned char *out,
-                                                 int64_t s0, int64_t s1, int64_t g0, int64_t g1) {
+                                                 int64_t s0, int64_t s1, int64_t g0, int64_t g1, int pcap) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ BandRec rec[EW][2];
   __shared__ long long rbase[EW][2];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  WarpRing &w = reinterpret_cast<WarpRing *>(smem)[warp];
+  unsigned char *wbase = smem + (size_t)warp * ring_bytes(pcap);
+  WarpRing &w = *reinterpret_cast<WarpRing *>(wbase);
+  Pts pt;
+  pt.xy = reinterpret_cast<float2 *>(wbase + sizeof(WarpRing));
+  pt.z = reinterpret_cast<float *>(pt.xy + pcap);
+  pt.cap = pcap;
   const int64_t last = first + count;
   const int64_t gw = (int64_t)blockIdx.x * EW + warp, nw = (int64_t)gridDim.x * EW;
   const int64_t nb = s1 - s0, nh = g1 - g0;
@@ -877,7 +891,7 @@ __global__ void __launch_bounds__(EMIT_T, 8) k_emit(TriParams P, int64_t first, 
     if (u < nb) {
       const bool more = u + nw < nb;
       BandRec &nx = rec[warp][cb ^ 1];
-      emit_band(P, w, rec[warp][cb], rbase[warp][cb], first, last, out, lane, [&](int stage) {
+      emit_band(P, w, pt, rec[warp][cb], rbase[warp][cb], first, last, out, lane, [&](int stage) {
         if (stage == 0) {
           if (more) fetch_rec(P, (int)(s0 + u + nw), nx, rbase[warp][cb ^ 1], lane);
           return;
@@ -889,7 +903,7 @@ __global__ void __launch_bounds__(EMIT_T, 8) k_emit(TriParams P, int64_t first, 
       });
       cp_async_wait_warp();
       cb ^= 1;
-    } else emit_hole(P, w, (int)(g0 + u - nb), first, last, out, lane);
+    } else emit_hole(P, w, pt, (int)(g0 + u - nb), first, last, out, lane);
   }
   if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
 }
@@ -986,14 +1000,25 @@ int triangulate_count(lmm_ctx *c) {
 int triangulate_emit(lmm_ctx *c, int64_t first, int64_t count, void *out_dev, cudaStream_t st) {
   if (count <= 0) return LMM_OK;
   TriParams P = make_params(c);
-  const size_t smem = sizeof(WarpRing) * EW;
+  // point cache sized to the bands of this triangulation: whole-band emission when a band's
+  // rings fit, at the occupancy the cache allows (160 points: 8 CTAs/SM)
+  int pcap = PCAP_MIN;
+  {
+    const int64_t live = c->S > 0 ? c->S : 1;
+    const double mean = (double)c->n_tri_band / (double)live;
+    while (pcap < PCAP_MAX && mean + 2.0 > pcap - 10) pcap += 160;
+  }
+  const size_t smem = (size_t)ring_bytes(pcap) * EW;
   static bool attr_set = false;
-  static int occ = 1;
+  static int occ_for[PCAP_MAX / 160 + 1] = {0};
   if (!attr_set) {
-    CUDA_TRY(cudaFuncSetAttribute(k_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CUDA_TRY(cudaFuncSetAttribute(k_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, ring_bytes(PCAP_MAX) * EW));
+    attr_set = true;
+  }
+  int &occ = occ_for[pcap / 160];
+  if (occ == 0) {
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_emit, EMIT_T, smem));
     if (occ < 1) occ = 1;
-    attr_set = true;
   }
   // bands and holes intersecting [first, last): the chunk map at the chunk holding
   // `first` bounds the first unit, the one of the chunk after `last - 1` the last unit
@@ -1023,7 +1048,7 @@ int triangulate_emit(lmm_ctx *c, int64_t first, int64_t count, void *out_dev, cu
   if (grid > need) grid = need;
   if (grid < 1) grid = 1;
   KTimer t(c, LMM_K_EMIT);
-  (c->n_launch++), k_emit<<<(unsigned)grid, EMIT_T, smem, st>>>(P, first, count, (unsigned char *)out_dev, s0, s1, g0, g1);
+  (c->n_launch++), k_emit<<<(unsigned)grid, EMIT_T, smem, st>>>(P, first, count, (unsigned char *)out_dev, s0, s1, g0, g1, pcap);
   CUDA_TRY(cudaGetLastError());
   return LMM_OK;
 }

@@ -34,13 +34,17 @@ def _lat(name):
         # configs[2] shape: skewed degrees 3..30, cones; configs[3] shape: a BCC spatial block
         "stochastic9": lambda: synth.stochastic(9, seed=7),
         "bccwin": lambda: synth.bcc_window(4, 3, 5, 3, 8),
+        # a strut ringed by 16 neighbours: its loop has 16 entries (> the emit pass's arc cache,
+        # so its band takes the windowed path)
+        "crown16": lambda: synth.star([[0, 0, 1]] + [[np.sin(0.7) * np.cos(t), np.sin(0.7) * np.sin(t), np.cos(0.7)]
+                                                     for t in np.linspace(0, 2 * np.pi, 16, endpoint=False)], 1.0, 0.05),
         # BASELINE.json configs[0]: 10x10x10 BCC, uniform radius, eps = 1e-3 r
         "bcc10": lambda: synth.bcc(10, 10, 10),
     }[name]()
 
 
 NAMES = ["single", "cone", "chain-bent", "star-bcc", "cubic3", "bcc3", "octet2", "octet2-graded", "bcc3-jitter",
-         "cubic4-graded-jitter", "voronoi", "stochastic9", "bccwin", "bcc10"]
+         "cubic4-graded-jitter", "voronoi", "stochastic9", "bccwin", "crown16", "bcc10"]
 
 
 @pytest.fixture(scope="module")
@@ -82,6 +86,17 @@ def _mesh_edges_ok(tris):
 @pytest.mark.parametrize("name", NAMES)
 @pytest.mark.parametrize("ce", [1e-2, 1e-3])
 def test_triangulation_parity(built, name, ce):
+    _triangulation_parity(built, name, ce)
+
+
+@pytest.mark.parametrize("name", ["octet2-graded", "stochastic9", "crown16", "chain-bent"])
+@pytest.mark.parametrize("ce", [3e-4, 1e-4])
+def test_triangulation_parity_fine(built, name, ce):
+    """Fine chord errors: long bands, the emit pass's larger point caches (and windows)."""
+    _triangulation_parity(built, name, ce)
+
+
+def _triangulation_parity(built, name, ce):
     lat, mm, orc, _ = built(name)
     assert mm.stats()["n_error_nodes"] == 0
     T = mm.triangulate(ce)
