@@ -46,8 +46,10 @@ static_assert(sizeof(ArcRec) == 48, "arc record is 48 bytes");
 struct LoopRec {
   uint32_t arc_fwd;
   float phs, dph;
-  int32_t cum;
+  int32_t cum;   // point offset in the ring (count pass, low 24 bits) | start vertex << 24 (meta-mesh)
 };
+__host__ __device__ inline int le_cum(int32_t c) { return c & 0xffffff; }
+__host__ __device__ inline int le_vid(int32_t c) { return (int)((uint32_t)c >> 24); }
 static_assert(sizeof(LoopRec) == 16, "loop record is 16 bytes");
 
 // hole entry: arc | fwd<<16, cum

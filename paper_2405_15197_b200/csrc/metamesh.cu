@@ -1044,10 +1044,11 @@ __device__ void part_c(cg::thread_block_tile<G> &g, WS &ws, const MMParams &P, i
         for (int i = 0; i < cnt; i++) {
           if (i > 0) ph = ph + ws.edp[slot[i - 1]];
           LoopRec &L = ws.le[pos + i];
+          const uint32_t aid = ws.arcs[slot[i] >> 1].ids;
           L.arc_fwd = (uint32_t)(slot[i] >> 1) | ((uint32_t)ws.efw[slot[i]] << 16);
           L.phs = ph;
           L.dph = ws.edp[slot[i]];
-          L.cum = 0;
+          L.cum = (int32_t)((ws.efw[slot[i]] ? (aid >> 16) & 0xffu : aid >> 24) << 24);   // start vertex
         }
       }
       nle += tot;

@@ -128,8 +128,11 @@ __device__ __forceinline__ int ring_counts(LoopRec *__restrict__ le, int cnt, co
   for (int i0 = 0; i0 < cnt; i0 += 4) {
     uint32_t af[4];
     float dt[4];
+    int vt[4];
 #pragma unroll
     for (int k = 0; k < 4; k++) af[k] = i0 + k < cnt ? (le[i0 + k].arc_fwd & 0x1ffffu) : 0u;
+#pragma unroll
+    for (int k = 0; k < 4; k++) vt[k] = i0 + k < cnt ? (le[i0 + k].cum & (int)0xff000000) : 0;
 #pragma unroll
     for (int k = 0; k < 4; k++) dt[k] = i0 + k < cnt ? __ldg(&arc[le_arc(af[k])].dt) : 0.0f;
 #pragma unroll
@@ -137,7 +140,7 @@ __device__ __forceinline__ int ring_counts(LoopRec *__restrict__ le, int cnt, co
       if (i0 + k < cnt) {
         int N = arc_N(dt[k], th0);
         le[i0 + k].arc_fwd = af[k] | ((uint32_t)N << 17);
-        le[i0 + k].cum = n;
+        le[i0 + k].cum = vt[k] | n;   // the start vertex stays in the top byte
         n += N;
       }
     }
@@ -189,7 +192,7 @@ struct SeqKey {
     for (;;) {
       const LoopRec L = le[ee];
       const int N = le_N(L.arc_fwd);
-      cum = L.cum;
+      cum = le_cum(L.cum);
       if (idx < cum + N || ee + 1 >= cnt) break;
       ee++;
     }
@@ -395,15 +398,16 @@ __device__ __forceinline__ void put_rec(unsigned char *dst, f3 a, f3 b, f3 c) {
 // and arc records (after its last group).  No registers are held across a band and no
 // block-level barriers are used.
 constexpr int EW = EMIT_T / 32;   // warps per CTA
-constexpr int PCAP_MIN = 160;     // ring points cached per band (both rings), runtime-sized
+constexpr int PCAP_MIN = 152;     // ring points cached per band (both rings), runtime-sized
 constexpr int PCAP_MAX = 640;     //   from the mean band size (triangulate_emit)
 constexpr int GRP = 56;           // triangles per aligned group (2800 B; 28 lanes x 2 records)
 constexpr int MAXRE = 32;         // ring entries per ring (>= MAXLOOP of the meta-mesh)
-constexpr int MAXRA = 10;         // arc records cached per ring
+constexpr int MAXRA = 8;          // arc records (and entry start vertices) cached per ring
 
 // per-warp shared memory: fixed part, then the point cache (pcap x float2, pcap x float)
 struct __align__(16) WarpRing {
   ArcRec arc[2][MAXRA];
+  float4 vq[2][MAXRA];    // start vertex of each cached entry (node-local)
   LoopRec le[2][MAXRE];   // loop entries (arc | fwd | N, phs, dph, cum); holes: arc_fwd, cum
   uint4 stage[GRP * REC / 16];
 };
@@ -456,6 +460,8 @@ __device__ __forceinline__ void fetch_arcs(const TriParams &P, WarpRing &w, cons
       cp_async<16>(reinterpret_cast<float4 *>(&w.arc[r][e]) + (k - 3 * e),
                    reinterpret_cast<const float4 *>(arcs + le_arc(w.le[r][e].arc_fwd)) + (k - 3 * e));
     }
+    if (lane < nq / 3)   // the entries' start vertices (ids from the loop entries)
+      cp_async<16>(&w.vq[r][lane], P.vert + 2 * (int64_t)(r ? h.pB : h.pA) + le_vid(w.le[r][lane].cum));
   }
 }
 
@@ -480,7 +486,7 @@ __device__ __forceinline__ ArcRec lds_arc(const ArcRec *p) {
 __device__ __forceinline__ f3 ring_point_e(const WarpRing &w, int r, const RingRef &R, int e, int idx) {
   const LoopRec L = w.le[r][e];
   const int N = le_N(L.arc_fwd), fwd = le_fwd(L.arc_fwd);
-  const int j = idx - L.cum;
+  const int j = idx - le_cum(L.cum);
   const int jj = fwd ? j : N - j;
   f3 p;
   if (jj == 0 || jj == N) {
@@ -502,7 +508,7 @@ __device__ __forceinline__ f3 ring_point_e(const WarpRing &w, int r, const RingR
 // point idx of ring r, its entry found by a scan of the entry starts (windowed bands, holes)
 __device__ __forceinline__ f3 ring_point(const WarpRing &w, int r, const RingRef &R, int idx) {
   int e = 0;
-  for (int k = 1; k < R.cnt; k++) e += (w.le[r][k].cum <= idx) ? 1 : 0;
+  for (int k = 1; k < R.cnt; k++) e += (le_cum(w.le[r][k].cum) <= idx) ? 1 : 0;
   return ring_point_e(w, r, R, e, idx);
 }
 
@@ -511,7 +517,7 @@ __device__ __forceinline__ f3 ring_point(const WarpRing &w, int r, const RingRef
 __device__ __forceinline__ f3 ring_point_formula(const WarpRing &w, int r, const RingRef &R, int e, int idx) {
   const LoopRec L = w.le[r][e];
   const int N = le_N(L.arc_fwd), fwd = le_fwd(L.arc_fwd);
-  const int j = idx - L.cum;
+  const int j = idx - le_cum(L.cum);
   const int jj = fwd ? j : N - j;
   const ArcRec A = lds_arc(&w.arc[r][e]);
   float t = A.t0 + (float)jj * __fdividef(A.dt, (float)N);
@@ -612,21 +618,13 @@ __device__ void emit_band_whole(const TriParams &P, WarpRing &w, const Pts &pt, 
   const int64_t w0 = base >> 5;
   const int nwd = (int)(((base + nA + nB - 1) >> 5) - w0 + 1);
   const uint32_t mword = lane < nwd ? __ldg(&P.mbits[w0 + lane]) : 0u;
-  // entry start vertices: loads issued before the formula pass, stored after it
+  // entry start vertices (prefetched with the arcs)
   float4 vq[2];
 #pragma unroll
-  for (int r = 0; r < 2; r++) {
-    const RingRef &R = r ? RB : RA;
-    vq[r] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (lane < R.cnt) {
-      const uint32_t ids = w.arc[r][lane].ids;
-      const int v = le_fwd(w.le[r][lane].arc_fwd) ? (ids >> 16) & 0xff : (ids >> 24);
-      vq[r] = __ldg(&R.vs[v]);
-    }
-  }
+  for (int r = 0; r < 2; r++) vq[r] = lane < (r ? RB.cnt : RA.cnt) ? w.vq[r][lane] : make_float4(0.f, 0.f, 0.f, 0.f);
   {
-    const int cA = (lane >= 1 && lane < RA.cnt) ? w.le[0][lane].cum : 0x7fffffff;
-    const int cB = lane < RB.cnt ? nA + w.le[1][lane].cum : 0x7fffffff;
+    const int cA = (lane >= 1 && lane < RA.cnt) ? le_cum(w.le[0][lane].cum) : 0x7fffffff;
+    const int cB = lane < RB.cnt ? nA + le_cum(w.le[1][lane].cum) : 0x7fffffff;
     int run = 0;   // entry starts (after ring A's first) below the current block
     for (int x = 0; x < nA + nB; x += 32) {
       const int k = x + lane;
@@ -657,7 +655,7 @@ __device__ void emit_band_whole(const TriParams &P, WarpRing &w, const Pts &pt, 
       if (lane < R.cnt) {
         const float4 q = vq[r];
         const f3 p = F3(R.ox + q.x, R.oy + q.y, R.oz + q.z);
-        const int idx = w.le[r][lane].cum;
+        const int idx = le_cum(w.le[r][lane].cum);
         if (r == 0) {
           put_point(pt, idx, p);
           if (idx == 0) put_point(pt, nA, p);
@@ -1006,7 +1004,7 @@ int triangulate_emit(lmm_ctx *c, int64_t first, int64_t count, void *out_dev, cu
   {
     const int64_t live = c->S > 0 ? c->S : 1;
     const double mean = (double)c->n_tri_band / (double)live;
-    while (pcap < PCAP_MAX && mean + 2.0 > pcap - 10) pcap += 160;
+    while (pcap < PCAP_MAX && mean + 2.0 > pcap - 4) pcap += 160;
   }
   const size_t smem = (size_t)ring_bytes(pcap) * EW;
   static bool attr_set = false;

@@ -146,7 +146,8 @@ def decode_node(bufs: dict, n: int) -> dict:
         l_int=np.stack([le[:, 0] & 0xFFFF, (le[:, 0] >> 16) & 1], 1).astype(np.int32),
         l_N=(le[:, 0] >> 17).astype(np.int32),
         l_f32=le[:, 1:3].copy().view(np.float32),
-        l_cum=le[:, 3].astype(np.int32),
+        l_cum=(le[:, 3] & 0xFFFFFF).astype(np.int32),
+        l_vid=(le[:, 3] >> 24).astype(np.int32),
         hole_off=hole_off,
         h_int=np.stack([he[:, 0] & 0xFFFF, (he[:, 0] >> 16) & 1], 1).astype(np.int32),
     )
