@@ -3,7 +3,8 @@ times (the meta-mesh of every node in one lmm_build_metamesh, the triangles emit
 device buffer in bench.py's 2^28-triangle chunks), CE = 1e-3:
   octet100 -- configs[1]: 100^3-cell graded octet truss, 24.12M struts (the headline bench);
   bcc250   -- configs[3]: one GPU's 250^3-cell block of the 1B-strut BCC lattice, 125M struts;
-  stoch290 -- configs[2]: stochastic lattice, degrees 3..30, 102M struts.
+  stoch290 -- configs[2]: stochastic lattice, degrees 3..30, 102M struts;
+  octet160 at CE = 1e-4 -- configs[4]'s fixed 98.6M-strut meta-mesh at its finest chord error.
 
 The oracle cannot meta-mesh 4M nodes in seconds, so it computes SAMPLED outputs one by
 one (orc_metamesh on a node subset; a band needs only its two end nodes):
@@ -24,18 +25,20 @@ from _parity import assert_node_parity, assert_triangles_close
 
 pytestmark = pytest.mark.gpu
 
-CE = 1e-3
 N_NODES_SAMPLE = 4000
 N_STRUTS_SAMPLE = 4000
 
 
-@pytest.fixture(scope="module", params=["octet100", "bcc250", "stoch290"])
+@pytest.fixture(scope="module", params=[("octet100", 1e-3), ("bcc250", 1e-3), ("stoch290", 1e-3), ("octet160", 1e-4)],
+                ids=["octet100", "bcc250", "stoch290", "octet160-ce1e-4"])
 def full(request):
     import torch
     from paper_2405_15197_b200 import MetaMesher
-    lat, _, _ = bench.make_config(request.param)
+    name, ce = request.param
+    lat, _, _ = bench.make_config(name)
+    lat.ce = ce
     mm = MetaMesher(0).load_lattice(lat).build()
-    T = mm.triangulate(CE)
+    T = mm.triangulate(ce)
     orc = oracle.Oracle.from_lattice(lat)
     out = torch.empty(bench.EMIT_CHUNK * bench.STL, dtype=torch.uint8, device="cuda")
     yield lat, mm, T, orc, out
@@ -129,7 +132,7 @@ def test_fullsize_sampled_bands_and_holes(full):
     hnodes = np.unique(rng.choice(bnd, 1000, replace=False))
     need = np.unique(np.concatenate([lat.ends[struts].ravel(), hnodes]))
     assert orc.metamesh(need) == 0
-    orc.triangulate(CE)                               # bands of struts with both ends done
+    orc.triangulate(lat.ce)                           # bands of struts with both ends done
     bn, _ = orc.band_info()
     orc._bn = bn                                      # strut_triangles() reuses it
     base, M, _ = orc.hole_info()

@@ -11,7 +11,7 @@ import pytest
 
 import oracle
 import synth
-from _parity import GEOM_TOL, assert_node_parity
+from _parity import GEOM_TOL, assert_node_parity, assert_triangles_close
 
 pytestmark = pytest.mark.gpu
 
@@ -160,6 +160,17 @@ def test_remesh_reuses_metamesh(built):
     counts = [mm.triangulate(ce) for ce in (1e-4, 1e-3, 1e-2, 5e-2)]
     assert all(a >= b for a, b in zip(counts, counts[1:]))
     assert counts[-1] == orc.triangulate(5e-2)
+
+
+def test_ce_sweep_on_one_metamesh_matches_oracle_each_time(built):
+    """BASELINE configs[4] in miniature: ONE meta-mesh re-triangulated at 1e-2, 1e-3, 1e-4 and
+    again at 1e-2 (state from the finer pass must not leak): every pass equals the oracle."""
+    lat, mm, orc, _ = built("octet2-graded")
+    r = float(lat.node_r.min())
+    for ce in (1e-2, 1e-3, 1e-4, 1e-2):
+        T = mm.triangulate(ce)
+        assert T == orc.triangulate(ce)
+        assert_triangles_close(mm.triangles(0, T), orc.write_triangles(), r, ce)
 
 
 def test_csr_offsets_are_the_degree_prefix_sum(built):
