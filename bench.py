@@ -230,7 +230,7 @@ def main():
     ap.add_argument("--ce-sweep", default="",
                     help="comma-separated chord errors: re-triangulate ONE meta-mesh (built before the timed "
                          "region) at each CE per step (configs[4], multi-resolution reuse)")
-    ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
