@@ -291,23 +291,6 @@ template <int G> __device__ __forceinline__ int first_err(cg::thread_block_tile<
   return g.shfl(err, __ffs(m) - 1);
 }
 
-__device__ __forceinline__ void unrank3(int t, int n, int *a, int *b, int *c) {
-  int A = 0;
-  for (;;) {
-    int cnt = (n - 1 - A) * (n - 2 - A) / 2;
-    if (t < cnt) break;
-    t -= cnt;
-    A++;
-  }
-  int B = A + 1;
-  for (;;) {
-    int cnt = n - 1 - B;
-    if (t < cnt) break;
-    t -= cnt;
-    B++;
-  }
-  *a = A; *b = B; *c = B + 1 + t;
-}
 
 // lexicographic pair t of {0..n-1} (a < b): row a from the quadratic's root, corrected
 // by one step for the rounding of the square root (arguments < 2^12: exact enough)
@@ -323,11 +306,6 @@ __device__ __forceinline__ void unrank2(int t, int n, int *a, int *b) {
 
 #define MAXQ 16
 #define MAXLOOP 32
-
-__device__ __forceinline__ int rank2(int a, int b, int n) {
-  // lexicographic index of pair (a < b) among the pairs of {0..n-1}
-  return a * (2 * n - a - 1) / 2 + (b - a - 1);
-}
 
 // side records between the parts: 5 float4 per CSR entry
 template <int G, class WS>
@@ -911,7 +889,7 @@ __device__ void part_c(cg::thread_block_tile<G> &g, WS &ws, const MMParams &P, i
   const float4 on = P.node[n];
   Node<WS> nd{ws, d, on.w};
   const float R = on.w;
-  const float delta = LMM_TOL_REL * R, dc = LMM_CTOL_REL * R;
+  const float dc = LMM_CTOL_REL * R;
   (void)dc;
   const int4 st = P.state[n];
   int status = st.x;

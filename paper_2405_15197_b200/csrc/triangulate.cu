@@ -71,10 +71,6 @@ struct TriParams {
 
 __device__ __forceinline__ int arc_N(float dt, float th0) { return (int)floorf(__fdiv_rn(dt, th0)) + 1; }
 
-__device__ __forceinline__ float key_at(float phs, float dph, int N, int j) {
-  // phs + j * (dph / N), each operation rounded
-  return __fadd_rn(phs, __fmul_rn((float)j, __fdiv_rn(dph, (float)N)));
-}
 
 __device__ __forceinline__ float wrap_rel(float b, float a0) {
   float r = __fsub_rn(b, a0);
@@ -360,26 +356,6 @@ __global__ void k_chunk_map_holes(TriParams P) {
 // ---------------------------------------------------------------------------------
 // emit pass
 // ---------------------------------------------------------------------------------
-__device__ __forceinline__ void put_rec(unsigned char *dst, f3 a, f3 b, f3 c) {
-  f3 u = f_sub(b, a), v = f_sub(c, a);
-  float nx = u.y * v.z - u.z * v.y, ny = u.z * v.x - u.x * v.z, nz = u.x * v.y - u.y * v.x;
-  float l2 = nx * nx + ny * ny + nz * nz;
-  float il = l2 > 0.0f ? rsqrtf(l2) : 0.0f;
-  float f[12] = {nx * il, ny * il, nz * il, a.x, a.y, a.z, b.x, b.y, b.z, c.x, c.y, c.z};
-  if ((((uintptr_t)dst) & 3) == 0) {
-    uint32_t *d32 = reinterpret_cast<uint32_t *>(dst);
-#pragma unroll
-    for (int i = 0; i < 12; i++) d32[i] = __float_as_uint(f[i]);
-    reinterpret_cast<uint16_t *>(dst)[24] = 0;
-  } else {
-    uint16_t *d16 = reinterpret_cast<uint16_t *>(dst);   // records are 2-byte aligned
-    d16[0] = (uint16_t)(__float_as_uint(f[0]) & 0xffffu);
-    uint32_t *d32 = reinterpret_cast<uint32_t *>(dst + 2);
-#pragma unroll
-    for (int i = 0; i < 11; i++) d32[i] = __funnelshift_r(__float_as_uint(f[i]), __float_as_uint(f[i + 1]), 16);
-    d32[11] = __float_as_uint(f[11]) >> 16;   // high half of f11 + attribute 0
-  }
-}
 
 // Warp-per-band emission.  Warps grid-stride over the strut bands (then the hole fans)
 // that intersect [first, first+count).  A band's ring data -- both rings' loop entries and
