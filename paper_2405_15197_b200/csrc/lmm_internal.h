@@ -57,6 +57,7 @@ struct lmm_ctx {
   DevBuf macc;       // int per merge word
   DevBuf cmap;       // int per emit chunk
   DevBuf brec;       // 64-byte emit record per strut band
+  DevBuf ring_n;     // int [2S] points per ring (CSR entry), count pass
   int64_t H = 0, n_tri = 0, n_tri_band = 0;
   bool tri_ok = false;
   // scratch

@@ -39,6 +39,7 @@ static_assert(sizeof(BandRec) == 64, "band record is 4 x 16 bytes");
 struct TriParams {
   const float4 *node;
   const int *csr_off;
+  const int2 *csr_ent;
   const int2 *ends;
   const int2 *strut_csr;
   const int4 *node_hdr;
@@ -144,25 +145,35 @@ __device__ __forceinline__ int ring_counts(LoopRec *__restrict__ le, int cnt, co
   return n;
 }
 
-__global__ void k_band_count(TriParams P) {
+// Eq. 11 counts of one ring (strut end) per thread.  Thread = CSR entry, so consecutive
+// threads work on the same node's loop and arc slabs (coalesced, cache-friendly reads).
+__global__ void k_ring_count(TriParams P, int64_t S2, int *ring_n) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= S2) return;
+  const int2 ent = P.csr_ent[i];
+  const int2 e = P.ends[ent.x];
+  const int n = ((unsigned)ent.y >> 31) ? e.y : e.x;   // the node this entry belongs to
+  int nr = 0;
+  if ((P.node_hdr[n].x & 0xff) == 0) {
+    const int off = P.csr_off[n];
+    const int2 L = P.loop_hdr[i];
+    nr = ring_counts(P.loop + lbase(P.csr_off, n) + L.x, L.y, P.arc + slab_base(off, n, SLAB_A_K, SLAB_A_K0), P.th0);
+  }
+  ring_n[i] = nr;
+}
+
+// band sizes from the two rings of each strut (0 when masked out or an end node failed)
+__global__ void k_band_count(TriParams P, const int *ring_n) {
   int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (s >= P.S) return;
-  int2 e = P.ends[s];
-  int2 ce = P.strut_csr[s];
-  int4 hA = P.node_hdr[e.x], hB = P.node_hdr[e.y];
-  int nA = 0, nB = 0, kB = 0;
-  const bool emit = !P.strut_mask || P.strut_mask[s];
-  if (emit && (hA.x & 0xff) == 0 && (hB.x & 0xff) == 0) {
-    int2 LA = P.loop_hdr[ce.x], LB = P.loop_hdr[ce.y];
-    LoopRec *la = P.loop + lbase(P.csr_off, e.x) + LA.x;
-    LoopRec *lb = P.loop + lbase(P.csr_off, e.y) + LB.x;
-    const ArcRec *aa = P.arc + abase(P.csr_off, e.x);
-    const ArcRec *ab = P.arc + abase(P.csr_off, e.y);
-    nA = ring_counts(la, LA.y, aa, P.th0);
-    nB = ring_counts(lb, LB.y, ab, P.th0);
+  int nA = 0, nB = 0;
+  if (!P.strut_mask || P.strut_mask[s]) {
+    const int2 ce = P.strut_csr[s];
+    nA = ring_n[ce.x];
+    nB = ring_n[ce.y];
     if (!(nA > 0 && nB > 0)) nA = nB = 0;   // the band rotation kB is found by k_band_merge
   }
-  P.band[s] = make_int4(nA, nB, kB, 0);
+  P.band[s] = make_int4(nA, nB, 0, 0);
   P.band_cnt[s] = (int64_t)nA + nB;
 }
 
@@ -886,6 +897,7 @@ TriParams make_params(lmm_ctx *c) {
   TriParams P;
   P.node = (const float4 *)c->node.p;
   P.csr_off = (const int *)c->csr_off.p;
+  P.csr_ent = (const int2 *)c->csr_ent.p;
   P.ends = (const int2 *)c->ends.p;
   P.strut_csr = (const int2 *)c->strut_csr.p;
   P.node_hdr = (const int4 *)c->node_hdr.p;
@@ -929,11 +941,15 @@ int triangulate_count(lmm_ctx *c) {
   if ((rc = dev_alloc(c->tmp64, sizeof(int64_t) * ((S > N ? S : N) + 2)))) return rc;
   if ((rc = dev_alloc(c->node_hole0, sizeof(int) * (N + 1)))) return rc;
   if ((rc = dev_alloc(c->node_hole0_64, sizeof(int64_t) * (N + 1)))) return rc;
+  if ((rc = dev_alloc(c->ring_n, sizeof(int) * (2 * S + 1)))) return rc;
   const int T = 256;
   TriParams P = make_params(c);
   {
     KTimer t(c, LMM_K_COUNT);
-    if (S) (c->n_launch++), k_band_count<<<(unsigned)((S + T - 1) / T), T, 0, c->stream>>>(P);
+    if (S) {
+      (c->n_launch++), k_ring_count<<<(unsigned)((2 * S + T - 1) / T), T, 0, c->stream>>>(P, 2 * S, (int *)c->ring_n.p);
+      (c->n_launch++), k_band_count<<<(unsigned)((S + T - 1) / T), T, 0, c->stream>>>(P, (const int *)c->ring_n.p);
+    }
     if (N) (c->n_launch++), k_node_nholes<<<(unsigned)((N + T - 1) / T), T, 0, c->stream>>>((const int4 *)c->node_hdr.p, N, c->has_node_mask ? (const uint8_t *)c->node_mask.p : nullptr, (int *)c->node_hole0.p);
     CUDA_TRY(cudaGetLastError());
   }
