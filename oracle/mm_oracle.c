@@ -1002,9 +1002,10 @@ static int hole_ring(const orc_lat *L, int64_t n, int h, d3 **pts, d3 *bp) {
     for (int j = 0; j < N; j++) P[p++] = arc_point64(M, E, N, M->he[i].fwd ? j : N - j);
   }
   /* Eq. 13: b = mean of contour vertices; b_project = (b-o)/|b-o| R + o.
-   * Reading: the direction is regularised by the contour's outward
+   * Reading (R7): the direction is regularised by the contour's outward
    * (Newell) normal nu, b_project = R nrm(b + R nu/|nu|) + o, which equals Eq. 13's
-   * direction for small holes and stays defined when b = o (free strut ends). */
+   * direction for small holes and stays defined when b = o (free strut ends); a contour
+   * without area (nu = 0) keeps Eq. 13's b - o. */
   d3 bsum = D3(0, 0, 0), nu = D3(0, 0, 0);
   for (int i = 0; i < tot; i++) {
     bsum = d_add(bsum, P[i]);
@@ -1012,7 +1013,10 @@ static int hole_ring(const orc_lat *L, int64_t n, int h, d3 **pts, d3 *bp) {
   }
   d3 bc = d_div(bsum, tot);
   double R = L->rad[n];
-  d3 dir = d_add(bc, d_scl(d_nrm(nu), R));
+  /* a two-point contour (a lune of two one-segment arcs) has no area: nu = 0 exactly, and
+   * Eq. 13's own direction b - o is used (reading R7) */
+  const int flat = nu.x == 0.0 && nu.y == 0.0 && nu.z == 0.0;
+  d3 dir = flat ? bc : d_add(bc, d_scl(d_nrm(nu), R));
   *bp = d_scl(d_nrm(dir), R);
   *pts = P;
   return tot;

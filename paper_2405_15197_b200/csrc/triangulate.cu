@@ -339,7 +339,8 @@ __global__ void k_hole_count(TriParams P) {
       }
     }
     float inv = 1.0f / (float)M;
-    float nl = rsqrtf(nx * nx + ny * ny + nz * nz);
+    const float n2 = nx * nx + ny * ny + nz * nz;
+    float nl = n2 > 0.0f ? rsqrtf(n2) : 0.0f;   // a contour without area keeps Eq. 13's b - o
     float dx = (p0.x + bx * inv) + R * nx * nl, dy = (p0.y + by * inv) + R * ny * nl, dz = (p0.z + bz * inv) + R * nz * nl;
     float dl = R * rsqrtf(dx * dx + dy * dy + dz * dz);
     P.hole_M[g] = M;

@@ -217,3 +217,38 @@ def test_virtual_ranks_union_equals_global_gpu(family):
     key = lambda a: np.unique(a.reshape(len(a), -1).view(np.uint32), axis=0)
     assert np.array_equal(key(got), key(ref))
     mm.close()
+
+
+def _random_lattice(seed):
+    """Seeded mixes of the generators: jittered, graded, stochastic, with radii spanning 2x."""
+    rng = np.random.default_rng(seed)
+    kind = seed % 4
+    if kind == 0:
+        lat = synth.stochastic(int(rng.integers(5, 9)), seed=seed, r_min=0.015, r_max=0.05)
+    elif kind == 1:
+        lat = synth.jitter(synth.graded_radii(synth.octet(3, 2, 2), 0.02, 0.05, axis=int(rng.integers(0, 3))), 0.04, seed)
+    elif kind == 2:
+        lat = synth.jitter(synth.graded_radii(synth.bcc(3, 3, 2), 0.03, 0.07, axis=2), 0.06, seed)
+    else:
+        lat = synth.jitter(synth.graded_radii(synth.cubic(4, 3, 3), 0.05, 0.11, axis=1), 0.05, seed)
+    return lat
+
+
+@pytest.mark.parametrize("seed", list(range(16)))
+def test_random_lattices_parity(seed):
+    """Stress: 16 seeded random lattices (all generator families, jitter, graded radii);
+    per node topology bit-exact and geometry within 1e-4 r_min, then the whole STL."""
+    from paper_2405_15197_b200 import MetaMesher, decode_node
+    lat = _random_lattice(seed)
+    mm = MetaMesher(0).load_lattice(lat).build()
+    orc = oracle.Oracle.from_lattice(lat)
+    orc.metamesh()
+    bufs = mm.buffers()
+    tol = GEOM_TOL * float(lat.node_r.min())
+    for n in range(lat.n_nodes):
+        assert_node_parity(decode_node(bufs, n), orc.node(n), tol, n)
+    ce = (2e-3, 5e-3, 1e-3, 3e-3)[seed % 4]
+    T = mm.triangulate(ce)
+    assert T == orc.triangulate(ce)
+    assert_triangles_close(mm.triangles(0, T), orc.write_triangles(), float(lat.node_r.min()), seed)
+    mm.close()
