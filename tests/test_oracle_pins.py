@@ -432,3 +432,19 @@ def test_fan_apex_on_nodal_sphere_and_hole_orientation(oracle_mod):
         t = o.node_hole_triangles(n)
         cen = (t[:, 1] + t[:, 2] + t[:, 3]) / 3 - lat.xyz[n]
         assert np.all(np.einsum("ij,ij->i", t[:, 0], cen) > 0)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_oracle_outputs_finite_on_random_lattices(oracle_mod, seed):
+    """Every triangle coordinate and normal is finite, every node representable, on seeded
+    random (jittered, graded, stochastic) lattices at several chord errors."""
+    rng = np.random.default_rng(100 + seed)
+    lat = [lambda: synth.stochastic(int(rng.integers(4, 7)), seed=seed, r_min=0.015, r_max=0.05),
+           lambda: synth.jitter(synth.graded_radii(synth.octet(2, 2, 2), 0.02, 0.05, 1), 0.05, seed),
+           lambda: synth.jitter(synth.graded_radii(synth.bcc(2, 2, 2), 0.03, 0.07, 0), 0.07, seed)][seed % 3]()
+    o = oracle_mod.Oracle.from_lattice(lat)
+    assert o.metamesh() == 0
+    for ce in (1e-2, 3e-3):
+        T = o.triangulate(ce)
+        tris = o.write_triangles()
+        assert len(tris) == T and np.isfinite(tris).all()
