@@ -86,7 +86,9 @@ __global__ void k_deg_hist(const int *off, int64_t N, unsigned long long *hist) 
   if (threadIdx.x < 33 && h[threadIdx.x]) atomicAdd(&hist[threadIdx.x], (unsigned long long)h[threadIdx.x]);
 }
 
-__device__ __forceinline__ int bucket_of(int d) { return d == 0 || d > LMM_MAXD ? -1 : (d <= 8 ? 0 : (d <= 16 ? 1 : 2)); }
+__host__ __device__ __forceinline__ int bucket_of(int d) {
+  return d == 0 || d > LMM_MAXD ? -1 : (d <= 8 ? 0 : (d <= 16 ? 1 : (d <= 23 ? 2 : 3)));
+}
 
 __global__ void k_bucket_fill(const int *off, int64_t N, const int *bucket_base, int *cursor, int *list) {
   int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -172,8 +174,8 @@ int degree_buckets(lmm_ctx *c) {
   unsigned long long *h = c->pinned_hist;
   CUDA_TRY(cudaMemcpyAsync(h, c->deg_hist.p, 33 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
-  int64_t cnt[LMM_NBUCKET] = {0, 0, 0};
-  for (int d = 1; d <= 31; d++) cnt[d <= 8 ? 0 : (d <= 16 ? 1 : 2)] += (int64_t)h[d];
+  int64_t cnt[LMM_NBUCKET] = {0};
+  for (int d = 1; d <= 31; d++) cnt[bucket_of(d)] += (int64_t)h[d];
   c->bucket_off[0] = 0;
   for (int b = 0; b < LMM_NBUCKET; b++) c->bucket_off[b + 1] = c->bucket_off[b] + cnt[b];
   int *base = (int *)(c->pinned_hist + 40);

@@ -27,10 +27,11 @@ extern "C" LMM_API int lmm_debug_phase_cycles(unsigned long long *out) {
 
 namespace {
 
-// per-bucket capacities <MAXS, MAXJ, MAXV, MAXA, MAXLE, MAXH> (degree 1-8, 9-16, 17-31)
+// per-bucket capacities <MAXS, MAXJ, MAXV, MAXA, MAXLE, MAXH> (degree 1-8, 9-16, 17-23, 24-31)
 #define LMM_B0_ARGS 9, 96, 18, 26, 52, 18
 #define LMM_B1_ARGS 17, 160, 34, 50, 100, 34
-#define LMM_B2_ARGS 32, 448, 64, 95, 190, 64
+#define LMM_B2_ARGS 24, 336, 48, 71, 142, 48
+#define LMM_B3_ARGS 32, 448, 64, 95, 190, 64
 
 struct MMParams {
   const float4 *node;
@@ -1204,6 +1205,7 @@ int launch_bucket(lmm_ctx *c, MMParams P) {
 #define LMM_B0_G LMM_B0_GA, LMM_B0_GB, LMM_B0_GC
 #define LMM_B1_G LMM_B1_GA, LMM_B1_GB, LMM_B1_GC
 #define LMM_B2_G 32, 32, 32
+#define LMM_B3_G 32, 32, 32
 
 }  // namespace
 
@@ -1218,7 +1220,10 @@ extern "C" LMM_API int lmm_debug_ws_bytes(int bucket, int part) {
     case 5: return (int)sizeof(WS_C<LMM_B1_ARGS>);
     case 6: return (int)sizeof(WS_A<LMM_B2_ARGS>);
     case 7: return (int)sizeof(WS_B<LMM_B2_ARGS>);
-    default: return (int)sizeof(WS_C<LMM_B2_ARGS>);
+    case 8: return (int)sizeof(WS_C<LMM_B2_ARGS>);
+    case 9: return (int)sizeof(WS_A<LMM_B3_ARGS>);
+    case 10: return (int)sizeof(WS_B<LMM_B3_ARGS>);
+    default: return (int)sizeof(WS_C<LMM_B3_ARGS>);
   }
 }
 #endif
@@ -1273,6 +1278,9 @@ int metamesh_run(lmm_ctx *c) {
     P.node_list = bn + c->bucket_off[2];
     P.n_list = (int)(c->bucket_off[3] - c->bucket_off[2]);
     if ((rc = launch_bucket<LMM_B2_G, LMM_B2_ARGS>(c, P))) return rc;
+    P.node_list = bn + c->bucket_off[3];
+    P.n_list = (int)(c->bucket_off[4] - c->bucket_off[3]);
+    if ((rc = launch_bucket<LMM_B3_G, LMM_B3_ARGS>(c, P))) return rc;
   }
   return LMM_OK;
 }
