@@ -27,9 +27,10 @@ extern "C" LMM_API int lmm_debug_phase_cycles(unsigned long long *out) {
 
 namespace {
 
-// per-bucket capacities <MAXS, MAXJ, MAXV, MAXA, MAXLE, MAXH> (degree 1-8, 9-16, 17-23, 24-31)
+// per-bucket capacities <MAXS, MAXJ, MAXV, MAXA, MAXLE, MAXH> (degree 1-8, 9-12, 13-16, 17-23, 24-31)
 #define LMM_B0_ARGS 9, 96, 18, 26, 52, 18
-#define LMM_B1_ARGS 17, 160, 34, 50, 100, 34
+#define LMM_B1_ARGS 13, 128, 26, 38, 76, 26
+#define LMM_B1b_ARGS 17, 160, 34, 50, 100, 34
 #define LMM_B2_ARGS 24, 336, 48, 71, 142, 48
 #define LMM_B3_ARGS 32, 448, 64, 95, 190, 64
 
@@ -1277,9 +1278,12 @@ int metamesh_run(lmm_ctx *c) {
     if ((rc = launch_bucket<LMM_B1_G, LMM_B1_ARGS>(c, P))) return rc;
     P.node_list = bn + c->bucket_off[2];
     P.n_list = (int)(c->bucket_off[3] - c->bucket_off[2]);
-    if ((rc = launch_bucket<LMM_B2_G, LMM_B2_ARGS>(c, P))) return rc;
+    if ((rc = launch_bucket<LMM_B1_G, LMM_B1b_ARGS>(c, P))) return rc;
     P.node_list = bn + c->bucket_off[3];
     P.n_list = (int)(c->bucket_off[4] - c->bucket_off[3]);
+    if ((rc = launch_bucket<LMM_B2_G, LMM_B2_ARGS>(c, P))) return rc;
+    P.node_list = bn + c->bucket_off[4];
+    P.n_list = (int)(c->bucket_off[5] - c->bucket_off[4]);
     if ((rc = launch_bucket<LMM_B3_G, LMM_B3_ARGS>(c, P))) return rc;
   }
   return LMM_OK;
