@@ -87,7 +87,7 @@ __global__ void k_deg_hist(const int *off, int64_t N, unsigned long long *hist) 
 }
 
 __host__ __device__ __forceinline__ int bucket_of(int d) {
-  return d == 0 || d > LMM_MAXD ? -1 : (d <= 8 ? 0 : (d <= 12 ? 1 : (d <= 16 ? 2 : (d <= 23 ? 3 : 4))));
+  return d == 0 || d > LMM_MAXD ? -1 : (d <= 4 ? 0 : (d <= 8 ? 1 : (d <= 12 ? 2 : (d <= 16 ? 3 : (d <= 23 ? 4 : 5)))));
 }
 
 __global__ void k_bucket_fill(const int *off, int64_t N, const int *bucket_base, int *cursor, int *list) {

@@ -7,7 +7,7 @@
 #include "../../include/lmm.h"
 #include "lmm_common.cuh"
 
-#define LMM_NBUCKET 5   // degree buckets 1..8, 9..12, 13..16, 17..23, 24..31 (0 and >31 handled apart)
+#define LMM_NBUCKET 6   // degree buckets 1..4, 5..8, 9..12, 13..16, 17..23, 24..31 (0, >31 apart)
 
 struct DevBuf {
   void *p = nullptr;

@@ -27,7 +27,8 @@ extern "C" LMM_API int lmm_debug_phase_cycles(unsigned long long *out) {
 
 namespace {
 
-// per-bucket capacities <MAXS, MAXJ, MAXV, MAXA, MAXLE, MAXH> (degree 1-8, 9-12, 13-16, 17-23, 24-31)
+// per-bucket capacities <MAXS, MAXJ, MAXV, MAXA, MAXLE, MAXH> (degree 1-4, 5-8, 9-12, 13-16, 17-23, 24-31)
+#define LMM_B00_ARGS 5, 24, 10, 14, 28, 10
 #define LMM_B0_ARGS 9, 96, 18, 26, 52, 18
 #define LMM_B1_ARGS 13, 128, 26, 38, 76, 26
 #define LMM_B1b_ARGS 17, 160, 34, 50, 100, 34
@@ -494,7 +495,8 @@ __device__ void part_a(cg::thread_block_tile<G> &g, WS &ws, const MMParams &P, i
   // are closed under union in place (monotone; clusters are small, so 1-2 sweeps), and the
   // component minimum is the lowest set bit.  More junctions: label propagation.
   if (status == 0 && nj > 0) {
-    constexpr int MJ = sizeof(ws.wp) >= 64 * sizeof(unsigned long long) ? 64 : 32;
+    constexpr int MJW = (int)(sizeof(ws.wp) / sizeof(unsigned long long));   // masks fit in ws.wp
+    constexpr int MJ = MJW >= 64 ? 64 : MJW;
     unsigned long long *msk = reinterpret_cast<unsigned long long *>(&ws.wp[0][0]);   // dead after step 2
     const bool masks = nj <= MJ;
     if (masks) {
@@ -1203,6 +1205,10 @@ int launch_bucket(lmm_ctx *c, MMParams P) {
 #ifndef LMM_B1_GC
 #define LMM_B1_GC 32
 #endif
+#ifndef LMM_B00_GN
+#define LMM_B00_GN 8
+#endif
+#define LMM_B00_G LMM_B00_GN, LMM_B00_GN, LMM_B00_GN
 #define LMM_B0_G LMM_B0_GA, LMM_B0_GB, LMM_B0_GC
 #define LMM_B1_G LMM_B1_GA, LMM_B1_GB, LMM_B1_GC
 #define LMM_B2_G 32, 32, 32
@@ -1270,20 +1276,21 @@ int metamesh_run(lmm_ctx *c) {
       CUDA_TRY(cudaGetLastError());
     }
     // bucket b occupies bucket_nodes[bucket_off[b] .. bucket_off[b+1])
-    P.node_list = bn + c->bucket_off[0];
-    P.n_list = (int)(c->bucket_off[1] - c->bucket_off[0]);
+    auto sel = [&](int b) {
+      P.node_list = bn + c->bucket_off[b];
+      P.n_list = (int)(c->bucket_off[b + 1] - c->bucket_off[b]);
+    };
+    sel(0);
+    if ((rc = launch_bucket<LMM_B00_G, LMM_B00_ARGS>(c, P))) return rc;
+    sel(1);
     if ((rc = launch_bucket<LMM_B0_G, LMM_B0_ARGS>(c, P))) return rc;
-    P.node_list = bn + c->bucket_off[1];
-    P.n_list = (int)(c->bucket_off[2] - c->bucket_off[1]);
+    sel(2);
     if ((rc = launch_bucket<LMM_B1_G, LMM_B1_ARGS>(c, P))) return rc;
-    P.node_list = bn + c->bucket_off[2];
-    P.n_list = (int)(c->bucket_off[3] - c->bucket_off[2]);
+    sel(3);
     if ((rc = launch_bucket<LMM_B1_G, LMM_B1b_ARGS>(c, P))) return rc;
-    P.node_list = bn + c->bucket_off[3];
-    P.n_list = (int)(c->bucket_off[4] - c->bucket_off[3]);
+    sel(4);
     if ((rc = launch_bucket<LMM_B2_G, LMM_B2_ARGS>(c, P))) return rc;
-    P.node_list = bn + c->bucket_off[4];
-    P.n_list = (int)(c->bucket_off[5] - c->bucket_off[4]);
+    sel(5);
     if ((rc = launch_bucket<LMM_B3_G, LMM_B3_ARGS>(c, P))) return rc;
   }
   return LMM_OK;
