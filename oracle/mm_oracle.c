@@ -46,7 +46,7 @@
 #endif
 
 #define ORC_MAXD 31          /* struts per node (sides 1..31, side 0 = sphere)   */
-#define ORC_MAXJ 512         /* valid junctions per node                          */
+#define ORC_MAXJ 512         /* valid junctions per node (storage)                */
 #define ORC_MAXC 256         /* vertex clusters per node                          */
 #define ORC_MAXA 512         /* arcs per node                                     */
 #define ORC_MAXQ 64          /* clusters on one conic                             */
@@ -516,7 +516,11 @@ static int node_metamesh(orc_lat *L, int64_t n) {
   float R = L->rad[n];
   float delta = TOL_REL * R, dc = CTOL_REL * R;
 
-  /* 1. junctions of every triple a<b<c of sides {0..d}, lexicographic order */
+  /* 1. junctions of every triple a<b<c of sides {0..d}, lexicographic order.  A node with
+   * more valid junctions than the capacity of its degree class (reading R13:
+   * degree 1-4: 24, 5-8: 96, 9-12: 192, 13-16: 240, 17-23: 336, 24-31: 448) is flagged
+   * JCAP -- the fixed per-node workspace of the model. */
+  const int maxj = d <= 4 ? 24 : d <= 8 ? 96 : d <= 12 ? 192 : d <= 16 ? 240 : d <= 23 ? 336 : 448;
   junc_t *J = (junc_t *)malloc(sizeof(junc_t) * ORC_MAXJ);
   int nj = 0;
   for (int a = 0; a <= d; a++)
@@ -529,7 +533,7 @@ static int node_metamesh(orc_lat *L, int64_t n) {
           int ok = a == 0 ? valid_sphere_junction(S, d, excl, y[r], delta)
                           : valid_strut_pt(S, d, excl, y[r], tau[r], delta);
           if (!ok) continue;
-          if (nj >= ORC_MAXJ) { free(J); M->status = ORC_E_JCAP; return M->status; }
+          if (nj >= maxj) { free(J); M->status = ORC_E_JCAP; return M->status; }
           int ks[3] = {a, b, c};
           for (int q = 0; q < 3; q++)
             if (ks[q] > 0 && tau[r] > 0.45f * (S[ks[q]].L * S[ks[q]].c)) { free(J); M->status = ORC_E_SHORT; return M->status; }

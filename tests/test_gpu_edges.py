@@ -125,3 +125,16 @@ def test_errors_are_loud():
     with pytest.raises(LmmError):                       # device output must be 16-byte aligned
         mm.write(0, 2, dev[1:])
     mm.close()
+
+
+@pytest.mark.parametrize("k", [8, 11, 12, 16])
+def test_umbrella_vertex_capacity_like_the_oracle(k):
+    """k struts on a cone around an axis meet in ONE k-valent vertex (C(k, 3) junctions at a
+    point): representable up to the junction capacity of the degree class (R13),
+    flagged JCAP beyond it -- identically by kernel and oracle."""
+    d = [[np.sin(1.0) * np.cos(t), np.sin(1.0) * np.sin(t), np.cos(1.0)] for t in np.linspace(0, 2 * np.pi, k, endpoint=False)]
+    lat = synth.star(d, 1.0, 0.05)
+    mm, orc, T = _full_parity(lat)
+    st = mm.stats()
+    assert st["n_error_nodes"] == (1 if k >= 12 else 0)
+    mm.close()
