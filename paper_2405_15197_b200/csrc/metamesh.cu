@@ -92,6 +92,7 @@ struct alignas(16) WS_B : WSCore<MAXS, MAXV> {
   int adrop[MAXA];
   // active side pairs, each with the mask of the clusters holding both sides
   unsigned long long pmask[MAXS * (MAXS - 1) / 2];
+  unsigned long long sclu[MAXS];   // per side: the clusters whose tie set holds it
   int plist[MAXS * (MAXS - 1) / 2];
   // queued interval midpoints
   float qx[32 * QL], qy[32 * QL], qz[32 * QL];
@@ -647,7 +648,15 @@ __device__ void part_b(cg::thread_block_tile<G> &g, WS &ws, const MMParams &P, i
     #pragma unroll 1
     for (int q = lane; q < nc; q += G) um |= ws.vmask[q];
     um = cg::reduce(g, um, cg::bit_or<uint32_t>());
-    // one lane per side pair: the clusters whose tie set holds both sides (nc <= MAXV <= 64)
+    // one lane per side pair: the clusters whose tie set holds both sides (nc <= MAXV <= 64),
+    // the intersection of the two sides' cluster sets
+    #pragma unroll 1
+    for (int k = lane; k < ns; k += G) {
+      unsigned long long m = 0ull;
+      for (int q = 0; q < nc; q++) m |= (unsigned long long)((ws.vmask[q] >> k) & 1u) << q;
+      ws.sclu[k] = m;
+    }
+    g.sync();
     int nact = 0;
     {
       #pragma unroll 1
@@ -659,7 +668,7 @@ __device__ void part_b(cg::thread_block_tile<G> &g, WS &ws, const MMParams &P, i
           int a, b;
           unrank2(p, ns, &a, &b);
           const uint32_t pb = (1u << a) | (1u << b);
-          for (int q = 0; q < nc; q++) cm |= (unsigned long long)((ws.vmask[q] & pb) == pb) << q;
+          cm = ws.sclu[a] & ws.sclu[b];
           const uint32_t strut_bits = a == 0 ? (1u << b) : pb;
           act = cm != 0ull || (um & strut_bits) == 0;
         }
@@ -857,22 +866,17 @@ __device__ void part_b(cg::thread_block_tile<G> &g, WS &ws, const MMParams &P, i
   }
   g.sync();
 
-  // every junction vertex must carry an arc
+  // every junction vertex must carry an arc (vertex ids < MAXV <= 64: one bit each)
   if (status == 0) {
-    int e = 0;
+    unsigned long long used = 0ull;
     #pragma unroll 1
-    for (int q0 = 0; q0 < nc; q0 += G) {
-      int q = q0 + lane;
-      if (q < nc) {
-        bool used = false;
-        for (int i = 0; i < na && !used; i++) {
-          uint32_t ids = ws.arcs[i].ids;
-          used = (int)((ids >> 16) & 0xff) == q || (int)(ids >> 24) == q;
-        }
-        if (!used) e = LMM_NODE_UNREF;
-      }
+    for (int i = lane; i < na; i += G) {
+      const uint32_t ids = ws.arcs[i].ids;
+      used |= (1ull << ((ids >> 16) & 0xff)) | (1ull << (ids >> 24));
     }
-    if (g.any(e != 0)) status = LMM_NODE_UNREF;
+    used = cg::reduce(g, used, cg::bit_or<unsigned long long>());
+    const unsigned long long need = nc >= 64 ? ~0ull : (1ull << nc) - 1ull;
+    if ((used & need) != need) status = LMM_NODE_UNREF;
   }
 
   // seam vertices and arcs to their slabs, state for part C
