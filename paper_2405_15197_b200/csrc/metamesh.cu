@@ -1045,7 +1045,13 @@ __device__ void part_c(cg::thread_block_tile<G> &g, WS &ws, const MMParams &P, i
 
   PHASE_MARK(6);
   // ---- 6. hole contours: cap arcs chained around the exposed sphere (lane 0) --------
+  bool anycap = false;   // nodes without cap arcs (the sphere fully covered) have no holes
   if (status == 0 && d > 0) {
+    #pragma unroll 1
+    for (int i = lane; i < na; i += G) anycap = anycap || (ws.arcs[i].ids & 0xff) == 0;
+    anycap = g.any(anycap);
+  }
+  if (status == 0 && d > 0 && anycap) {
     int st = 0;
     if (lane == 0) {
       uint64_t used = 0;   // MAXA <= 64 tracked per word below
