@@ -252,3 +252,24 @@ def test_random_lattices_parity(seed):
     assert T == orc.triangulate(ce)
     assert_triangles_close(mm.triangles(0, T), orc.write_triangles(), float(lat.node_r.min()), seed)
     mm.close()
+
+
+@pytest.mark.parametrize("seed", list(range(6)))
+def test_medium_random_lattices_parity(seed):
+    """Stress at medium size (10-40k struts): every node of a stochastic / jittered graded
+    lattice bit-exact in topology, and the whole STL within tolerance."""
+    from paper_2405_15197_b200 import MetaMesher, decode_node
+    lat = [lambda: synth.stochastic(16 + seed, seed=1000 + seed, r_min=0.015, r_max=0.05),
+           lambda: synth.jitter(synth.graded_radii(synth.octet(7, 6, 6), 0.02, 0.06, seed % 3), 0.05, 1000 + seed),
+           lambda: synth.jitter(synth.graded_radii(synth.bcc(12, 10, 9), 0.03, 0.07, seed % 3), 0.08, 1000 + seed)][seed % 3]()
+    mm = MetaMesher(0).load_lattice(lat).build()
+    orc = oracle.Oracle.from_lattice(lat)
+    assert orc.metamesh() == mm.stats()["n_error_nodes"]
+    bufs = mm.buffers()
+    tol = GEOM_TOL * float(lat.node_r.min())
+    for n in range(lat.n_nodes):
+        assert_node_parity(decode_node(bufs, n), orc.node(n), tol, n)
+    T = mm.triangulate(2e-3)
+    assert T == orc.triangulate(2e-3)
+    assert_triangles_close(mm.triangles(0, T), orc.write_triangles(), float(lat.node_r.min()), seed)
+    mm.close()
