@@ -56,22 +56,23 @@ __global__ void k_fill(const int2 *e32, int64_t S, const int *off, int *cursor, 
   ent[p1] = make_int2((int)s, (int)((unsigned)e.x | 0x80000000u));
 }
 
-// ascending strut id within each node (deterministic local side numbering)
-__global__ void k_sort_segments(const int *off, int64_t N, int2 *ent, int2 *strut_csr) {
-  int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (n >= N) return;
-  int b = off[n], e = off[n + 1];
-  for (int i = b + 1; i < e; i++) {
-    int2 x = ent[i];
-    int j = i;
-    while (j > b && ent[j - 1].x > x.x) { ent[j] = ent[j - 1]; j--; }
-    ent[j] = x;
-  }
-  for (int i = b; i < e; i++) {
-    int2 x = ent[i];
-    if ((unsigned)x.y >> 31) strut_csr[x.x].y = i;
-    else strut_csr[x.x].x = i;
-  }
+// ascending strut id within each node (deterministic local side numbering): every entry is
+// placed at its rank among its node's entries (thread per entry; the segment is read from
+// L1), and the strut's CSR positions are recorded on the way
+__global__ void k_rank_segments(const int *off, const int2 *e32, int64_t S2, const int2 *in, int2 *out, int2 *strut_csr) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= S2) return;
+  const int2 x = in[i];
+  const bool endB = ((unsigned)x.y >> 31) != 0;
+  const int2 e = e32[x.x];
+  const int n = endB ? e.y : e.x;
+  const int b = off[n], en = off[n + 1];
+  int rank = 0;
+  for (int j = b; j < en; j++) rank += __ldg(&in[j].x) < x.x ? 1 : 0;
+  const int p = b + rank;
+  out[p] = x;
+  if (endB) strut_csr[x.x].y = p;
+  else strut_csr[x.x].x = p;
 }
 
 __global__ void k_deg_hist(const int *off, int64_t N, unsigned long long *hist) {
@@ -150,7 +151,15 @@ int lattice_build(lmm_ctx *c, const float *xyz, const int64_t *ends, const float
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaMemsetAsync(deg, 0, sizeof(int) * N, c->stream));
   if (S) (c->n_launch++), k_fill<<<(unsigned)((S + T - 1) / T), T, 0, c->stream>>>((const int2 *)c->ends.p, S, (const int *)c->csr_off.p, deg, (int2 *)c->csr_ent.p);
-  if (N) (c->n_launch++), k_sort_segments<<<(unsigned)((N + T - 1) / T), T, 0, c->stream>>>((const int *)c->csr_off.p, N, (int2 *)c->csr_ent.p, (int2 *)c->strut_csr.p);
+  if (S) {
+    if ((rc = dev_alloc(c->csr_tmp, sizeof(int2) * (2 * S + 1)))) return rc;
+    (c->n_launch++), k_rank_segments<<<(unsigned)((2 * S + T - 1) / T), T, 0, c->stream>>>(
+        (const int *)c->csr_off.p, (const int2 *)c->ends.p, 2 * S, (const int2 *)c->csr_ent.p, (int2 *)c->csr_tmp.p,
+        (int2 *)c->strut_csr.p);
+    DevBuf t = c->csr_ent;   // the ranked copy becomes the CSR
+    c->csr_ent = c->csr_tmp;
+    c->csr_tmp = t;
+  }
   CUDA_TRY(cudaGetLastError());
   return LMM_OK;
 }

@@ -94,7 +94,7 @@ LMM_API int lmm_create(lmm_ctx **out, int device, void *stream) {
 }
 
 static void free_all(lmm_ctx *c) {
-  DevBuf *bufs[] = {&c->node, &c->ends, &c->csr_off, &c->csr_ent, &c->strut_csr, &c->deg_hist, &c->bucket_nodes,
+  DevBuf *bufs[] = {&c->node, &c->ends, &c->csr_off, &c->csr_ent, &c->csr_tmp, &c->strut_csr, &c->deg_hist, &c->bucket_nodes,
                     &c->bucket_cnt, &c->node_hdr, &c->vert, &c->arc, &c->loop_hdr, &c->loop, &c->hole_hdr,
                     &c->hole_ent, &c->band, &c->strut_off, &c->node_hole0, &c->node_hole0_64, &c->hole_M,
                     &c->hole_off, &c->hole_bp, &c->hole_node, &c->node_mask, &c->strut_mask, &c->mbits, &c->macc, &c->cmap, &c->brec, &c->ring_n, &c->tmp64, &c->scratch, &c->mm_side, &c->mm_state, &c->tri3, &c->scan_tmp, &c->stage[0], &c->stage[1]};

@@ -25,6 +25,7 @@ struct lmm_ctx {
   DevBuf csr_off;    // int    [N+1]
   DevBuf csr_ent;    // int2   [2S] strut, far | end<<31
   DevBuf strut_csr;  // int2   [S]  CSR entry of the strut at i0 and at i1
+  DevBuf csr_tmp;    // int2   [2S] CSR fill before ranking (swapped with csr_ent)
   DevBuf deg_hist;   // unsigned long long [33]
   DevBuf bucket_nodes;   // int [N]
   DevBuf bucket_cnt;     // int [LMM_NBUCKET + 2]
