@@ -265,19 +265,21 @@ __global__ void k_band_merge(TriParams P) {
     const int q0 = w == 0 ? 0 : 32 * w - sb;
     const int q1 = 32 * (w + 1) - sb < n ? 32 * (w + 1) - sb : n;
     if (w > 0) ma[w] = i;   // A-advances before the word's first bit
-    uint32_t word = 0;
-    for (int q = q0; q < q1; q++) {
-      if (i < nA && (j == nB || an <= bn)) {
-        word |= 1u << ((sb + q) & 31);
+    // an / bn become +inf once their ring is exhausted, so "i < nA && (j == nB || an <= bn)"
+    // is just "an <= bn" (both exhausted only after the last step)
+    uint32_t word = 0, bit = 1u << ((sb + q0) & 31);
+    for (int q = q0; q < q1; q++, bit <<= 1) {
+      if (an <= bn) {
+        word |= bit;
         i++;
-        if (i < nA) {
-          if (i + 1 < nA) { A.next(); an = __fsub_rn(A.key(), a0); }
-          else an = LMM_TWO_PI_F;
-        }
+        if (i + 1 < nA) { A.next(); an = __fsub_rn(A.key(), a0); }
+        else an = i < nA ? LMM_TWO_PI_F : __int_as_float(0x7f800000);
       } else {
         j++;
-        if (++jb == nB) { jb = 0; B.enter(0, 0); } else if (j < nB) B.next();
-        if (j < nB) bn = (j + 1 < nB) ? wrap_rel(B.key(), a0) : __fadd_rn(b0, LMM_TWO_PI_F);
+        if (j + 1 < nB) {
+          if (++jb == nB) { jb = 0; B.enter(0, 0); } else B.next();
+          bn = wrap_rel(B.key(), a0);
+        } else bn = j < nB ? __fadd_rn(b0, LMM_TWO_PI_F) : __int_as_float(0x7f800000);
       }
     }
     // a word is the band's alone when it starts at or after the band start and ends inside it
