@@ -183,7 +183,8 @@ __global__ void k_band_count(TriParams P, const int *ring_n) {
 // current entry), re-seeked only where a ring wraps.
 struct SeqKey {
   const LoopRec *le;
-  int cnt, e, jl, rem;
+  int cnt, e, rem;
+  float fj;      // index within the entry as a float (exact: < 2^24)
   float phs, step;
   __device__ void enter(int ee, int j0) {
     e = ee;
@@ -191,7 +192,7 @@ struct SeqKey {
     const int N = le_N(L.arc_fwd);
     phs = L.phs;
     step = __fdiv_rn(L.dph, (float)N);   // same bits as dividing at every key
-    jl = j0;
+    fj = (float)j0;
     rem = N - j0;
   }
   __device__ void seek(int idx) {
@@ -205,9 +206,9 @@ struct SeqKey {
     }
     enter(ee, idx - cum);
   }
-  __device__ float key() const { return __fadd_rn(phs, __fmul_rn((float)jl, step)); }
+  __device__ float key() const { return __fadd_rn(phs, __fmul_rn(fj, step)); }
   __device__ void next() {
-    jl++;
+    fj += 1.0f;
     if (--rem == 0 && e + 1 < cnt) enter(e + 1, 0);
   }
 };
@@ -238,11 +239,11 @@ __global__ void k_band_merge(TriParams P) {
   const float a0 = A.phs;     // ring A first entry phi
   // rotation of ring B: its first point with the smallest angle relative to A's start
   int kB = 0;
-  float best = 0.0f;
+  float best = __int_as_float(0x7f800000);   // first index of the minimum (strict <)
   B.enter(0, 0);
   for (int j = 0; j < nB; j++, B.next()) {
     const float r = wrap_rel(B.key(), a0);
-    if (j == 0 || r < best) { best = r; kB = j; }
+    if (r < best) { best = r; kB = j; }
   }
   P.band[s].z = kB;
   rq[0] = make_float4(__int_as_float(nA), __int_as_float(nB), __int_as_float(kB), __int_as_float(LA.x | (LA.y << 16)));
