@@ -85,6 +85,9 @@ LMM_API void lmm_destroy(lmm_ctx *ctx);
  *           nodal spheres (Sec. 4.1), so every strut end at a node must carry
  *           that node's sphere radius (else LMM_E_RADIUS); radii > 0.
  *   where : LMM_HOST or LMM_DEVICE for all three arrays.
+ * Sizes: n_nodes < 2^31 - 2, 2 n_struts < 2^31 - 2 and 6 n_struts + 2 n_nodes < 2^32 (one
+ * context holds up to ~700M struts; device memory is the binding limit well before that),
+ * else LMM_E_ARG.
  * Builds the device CSR (node -> incident struts, ascending strut id). */
 LMM_API int lmm_load_lattice(lmm_ctx *ctx, const float *xyz, int64_t n_nodes,
                              const int64_t *ends, const float *r_end, int64_t n_struts,

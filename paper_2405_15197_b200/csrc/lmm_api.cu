@@ -131,6 +131,8 @@ LMM_API int lmm_sync(lmm_ctx *c) {
 LMM_API int lmm_load_lattice(lmm_ctx *c, const float *xyz, int64_t n_nodes, const int64_t *ends, const float *r_end,
                              int64_t n_struts, int where) {
   if (!c || n_nodes < 0 || n_struts < 0 || n_nodes >= (1ll << 31) - 2 || 2 * n_struts >= (1ll << 31) - 2) return LMM_E_ARG;
+  // per-band emit records address a node's arc slab as 3 off + 2 n in 32 bits
+  if (3 * (2 * n_struts) + 2 * n_nodes >= (1ll << 32)) return LMM_E_ARG;
   if ((n_nodes && !xyz) || (n_struts && (!ends || !r_end))) return LMM_E_ARG;
   if (where != LMM_HOST && where != LMM_DEVICE) return LMM_E_ARG;
   CUDA_TRY(cudaSetDevice(c->device));
