@@ -206,16 +206,16 @@ template <class WS> struct Node {
     if (sphere) { t0 = 0.0f; t1 = 0.0f; }
     const float2 Yx = make_float2(y0.x, y1.x), Yy = make_float2(y0.y, y1.y), Yz = make_float2(y0.z, y1.z);
     const float2 nT = make_float2(-t0, -t1);
-    for (int m = 1; m <= d; m++) {
+    uint32_t v0 = 0u, v1 = 0u, mb = 2u;   // sides violated by each root (bit m)
+    for (int m = 1; m <= d; m++, mb <<= 1) {
       const float4 p0 = w.wp[m][0], p1 = w.wp[m][1];
-      const bool ex = (excl >> m) & 1u;
       float2 h = add2(mul2(make_float2(p0.x, p0.y), Yx), mul2(make_float2(p0.z, p0.w), Yy));
       h = add2(h, mul2(make_float2(p1.x, p1.y), Yz));
       h = add2(add2(h, make_float2(p1.z, p1.w)), nT);
-      k0 = k0 && (ex || !(h.x > delta));
-      k1 = k1 && (ex || !(h.y > delta));
+      v0 |= h.x > delta ? mb : 0u;
+      v1 |= h.y > delta ? mb : 0u;
     }
-    *ok0 = k0; *ok1 = k1;
+    *ok0 = k0 && !(v0 & ~excl); *ok1 = k1 && !(v1 & ~excl);
   }
   // end-circle (cap) point: strictly exposed
   __device__ bool valid_sphere_pt(uint32_t excl, f3 y, float delta) const {
@@ -774,14 +774,17 @@ __device__ void part_b(cg::thread_block_tile<G> &g, WS &ws, const MMParams &P, i
           bool ok0 = s0 || !(t0 < -delta), ok1 = s1 || !(t1 < -delta);
           const float2 Yx = make_float2(qx[qi], qx[qj]), Yy = make_float2(qy[qi], qy[qj]), Yz = make_float2(qz[qi], qz[qj]);
           const float2 nT = make_float2(-t0, -t1);
-          for (int mm = 1; mm <= d; mm++) {
+          uint32_t v0 = 0u, v1 = 0u, mb = 2u;   // sides violated at each midpoint (bit mm)
+          for (int mm = 1; mm <= d; mm++, mb <<= 1) {
             const float4 p0 = ws.wp[mm][0], p1 = ws.wp[mm][1];
             float2 h = add2(mul2(make_float2(p0.x, p0.y), Yx), mul2(make_float2(p0.z, p0.w), Yy));
             h = add2(h, mul2(make_float2(p1.x, p1.y), Yz));
             h = add2(add2(h, make_float2(p1.z, p1.w)), nT);
-            ok0 = ok0 && (((m0 >> mm) & 1u) || !(h.x > th0));
-            ok1 = ok1 && (((m1 >> mm) & 1u) || !(h.y > th1));
+            v0 |= h.x > th0 ? mb : 0u;
+            v1 |= h.y > th1 ? mb : 0u;
           }
+          ok0 = ok0 && !(v0 & ~m0 & 0x7fffffffu);
+          ok1 = ok1 && !(v1 & ~m1 & 0x7fffffffu);
           qok[qi] = ok0;
           if (qj != qi) qok[qj] = ok1;
         }
