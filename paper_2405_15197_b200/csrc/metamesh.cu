@@ -77,6 +77,7 @@ template <int MAXS, int MAXJ, int MAXV, int MAXA, int MAXLE, int MAXH>
 struct alignas(16) WS_A : WSCore<MAXS, MAXV> {
   // side k as broadcast pairs for the two-root junction test: (wx,wx,wy,wy), (wz,wz,-e,-e)
   float4 wp[MAXS][2];
+  float lim[MAXS];   // 0.45 L c of each strut side (SHORT limit); +inf for the sphere
   float4 jp[MAXJ];   // junction x, y, z; .w = vertex id once clustered (roots)
   uint32_t jabc[MAXJ];
   int jlab[MAXJ];
@@ -387,6 +388,7 @@ __device__ void part_a(cg::thread_block_tile<G> &g, WS &ws, const MMParams &P, i
   // ---- 1. sides -------------------------------------------------------------------
   if (lane == 0) {
     ws.w4[0] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+    ws.lim[0] = __int_as_float(0x7f800000);   // the sphere side never limits
   }
   int err = 0;
   #pragma unroll 1
@@ -415,6 +417,7 @@ __device__ void part_a(cg::thread_block_tile<G> &g, WS &ws, const MMParams &P, i
           ws.wp[k][1] = make_float4(wv.z, wv.z, -ek, -ek);
           ws.ux[k] = u.x; ws.uy[k] = u.y; ws.uz[k] = u.z;
           ws.s[k] = s; ws.c[k] = c; ws.L[k] = Ln;
+          ws.lim[k] = 0.45f * (Ln * c);
           ws.sign[k] = endbit ? -1 : 1;
           // strut frame from p[i1] - p[i0]
           f3 Da = endbit ? f_sub(po, pfar) : f_sub(pfar, po);
@@ -456,15 +459,10 @@ __device__ void part_a(cg::thread_block_tile<G> &g, WS &ws, const MMParams &P, i
           const uint32_t excl = (1u << a) | (1u << b) | (1u << c);
           v0 = v1 = true;
           nd.valid_junction_pair(a == 0, excl, y[0], tau[0], y[1], tau[1], delta, &v0, &v1);
-          const int ks[3] = {a, b, c};
-          for (int q = 0; q < 3; q++) {
-            if (ks[q] > 0) {
-              const float lim = 0.45f * (ws.L[ks[q]] * ws.c[ks[q]]);
-              if (tau[0] > lim) sh0 = true;
-              if (tau[1] > lim) sh1 = true;
-            }
-          }
-          sh0 = sh0 && v0; sh1 = sh1 && v1;
+          // strut too short: tau above 0.45 L c of any strut side of the triple
+          const float lm = fminf(fminf(ws.lim[a], ws.lim[b]), ws.lim[c]);
+          sh0 = v0 && tau[0] > lm;
+          sh1 = v1 && tau[1] > lm;
         }
       }
       unsigned m0 = g.ballot(v0), m1 = g.ballot(v1);
