@@ -152,17 +152,20 @@ template <class WS> struct Node {
     return ((q.x * y.x + q.y * y.y) + q.z * y.z) - q.w;
   }
 
-  // triple junction (oracle junction32)
-  __device__ bool junction(int a, int b, int c, f3 *y, float *tau) const {
+  // triple junction (oracle junction32), without branches: the three
+  // rejection tests become a flag and the divisors of rejected lanes are replaced by 1 (their
+  // roots are never used), so the group stays converged; accepted lanes compute exactly the
+  // specification's operations
+  __device__ bool junction_bf(int a, int b, int c, f3 *y, float *tau) const {
     f3 Wa = W(a), Wb = W(b), Wc = W(c);
-    float Ea = E(a), Eb = E(b), Ec = E(c);
-    if (a == 0) { Wa = F3(0.0f, 0.0f, 0.0f); Ea = 0.0f; }
+    float Ea = E(a), Eb = E(b), Ec = E(c);   // side 0 (the sphere) has W = 0, E = 0
     f3 n1 = f_sub(Wa, Wb), n2 = f_sub(Wa, Wc);
     float q1 = Ea - Eb, q2 = Ea - Ec;
     f3 m = f_cross(n1, n2);
     float mm = f_dot(m, m);
     float nn1 = f_dot(n1, n1), nn2 = f_dot(n2, n2);
-    if (!(mm > (1e-8f * nn1) * nn2)) return false;
+    bool ok = mm > (1e-8f * nn1) * nn2;
+    mm = ok ? mm : 1.0f;
     f3 c1 = f_cross(n2, m), c2 = f_cross(m, n1);
     float imm = 1.0f / mm;
     f3 y0 = F3((q1 * c1.x + q2 * c2.x) * imm, (q1 * c1.y + q2 * c2.y) * imm, (q1 * c1.z + q2 * c2.z) * imm);
@@ -171,11 +174,13 @@ template <class WS> struct Node {
     float tau0 = f_dot(Wa, y0) - Ea;
     float tau1 = f_dot(Wa, mh);
     float A = 1.0f - tau1 * tau1;
-    if (!(A > 1e-6f)) return false;
+    ok = ok && A > 1e-6f;
+    A = ok ? A : 1.0f;
     float Bp = f_dot(y0, mh) - tau0 * tau1;
     float C = (f_dot(y0, y0) - R * R) - tau0 * tau0;
     float disc = Bp * Bp - A * C;
-    if (disc < 0.0f) return false;
+    ok = ok && !(disc < 0.0f);
+    disc = ok ? disc : 0.0f;
     float sq = sqrtf(disc);
     float iA = 1.0f / A;
     float l0 = (-Bp - sq) * iA, l1 = (-Bp + sq) * iA;
@@ -183,7 +188,7 @@ template <class WS> struct Node {
     tau[0] = tau0 + l0 * tau1;
     y[1] = f_add(y0, f_scl(mh, l1));
     tau[1] = tau0 + l1 * tau1;
-    return true;
+    return ok;
   }
 
   // branch-free over the sides (same boolean as the early-exit form)
@@ -452,18 +457,18 @@ __device__ void part_a(cg::thread_block_tile<G> &g, WS &ws, const MMParams &P, i
       f3 y[2];
       float tau[2];
       bool sh0 = false, sh1 = false;
-      if (t < ntri) {
-        const uint32_t code = __ldg(&t3[t]);
+      {
+        // every lane of the group runs the same straight-line solve and side loop
+        const uint32_t code = __ldg(&t3[t < ntri ? t : ntri - 1]);
         a = code & 0xff; b = (code >> 8) & 0xff; c = code >> 16;
-        if (nd.junction(a, b, c, y, tau)) {
-          const uint32_t excl = (1u << a) | (1u << b) | (1u << c);
-          v0 = v1 = true;
-          nd.valid_junction_pair(a == 0, excl, y[0], tau[0], y[1], tau[1], delta, &v0, &v1);
-          // strut too short: tau above 0.45 L c of any strut side of the triple
-          const float lm = fminf(fminf(ws.lim[a], ws.lim[b]), ws.lim[c]);
-          sh0 = v0 && tau[0] > lm;
-          sh1 = v1 && tau[1] > lm;
-        }
+        const bool solved = nd.junction_bf(a, b, c, y, tau) && t < ntri;
+        const uint32_t excl = (1u << a) | (1u << b) | (1u << c);
+        v0 = v1 = solved;
+        nd.valid_junction_pair(a == 0, excl, y[0], tau[0], y[1], tau[1], delta, &v0, &v1);
+        // strut too short: tau above 0.45 L c of any strut side of the triple
+        const float lm = fminf(fminf(ws.lim[a], ws.lim[b]), ws.lim[c]);
+        sh0 = v0 && tau[0] > lm;
+        sh1 = v1 && tau[1] > lm;
       }
       unsigned m0 = g.ballot(v0), m1 = g.ballot(v1);
       unsigned lt = (1u << lane) - 1u;
