@@ -513,7 +513,8 @@ __device__ void part_a(cg::thread_block_tile<G> &g, WS &ws, const MMParams &P, i
         #pragma unroll 1
         for (int k = 0; k < nj; k++) {
           const float4 pk = ws.jp[k];
-          const bool cl = fabsf(pj.x - pk.x) <= dc && fabsf(pj.y - pk.y) <= dc && fabsf(pj.z - pk.z) <= dc;
+          const float dm = fmaxf(fmaxf(fabsf(pj.x - pk.x), fabsf(pj.y - pk.y)), fabsf(pj.z - pk.z));
+          const bool cl = dm <= dc;   // max-norm distance (exact: max and abs do not round)
           m |= (unsigned long long)cl << k;
         }
         if (j < nj) msk[j] = m;
