@@ -51,6 +51,7 @@ struct MMParams {
   int2 *hole_hdr;
   HoleEnt *hole_ent;
   const uint32_t *tri3;   // lexicographic triples a | b << 8 | c << 16 of n sides at C(n,4)
+  const uint32_t *pair2;  // lexicographic pairs a | b << 8 of n sides at C(n,3)
   float4 *side;    // [2S][5] side records between the parts (csr entry order)
   int4 *state;     // [N] status, clusters, vertices, arcs between the parts
 };
@@ -303,17 +304,6 @@ template <int G> __device__ __forceinline__ int first_err(cg::thread_block_tile<
 }
 
 
-// lexicographic pair t of {0..n-1} (a < b): row a from the quadratic's root, corrected
-// by one step for the rounding of the square root (arguments < 2^12: exact enough)
-__device__ __forceinline__ void unrank2(int t, int n, int *a, int *b) {
-  const float m = (float)(2 * n - 1);
-  int A = (int)floorf(0.5f * (m - sqrtf(m * m - 8.0f * (float)t)));
-  A = A < 0 ? 0 : (A > n - 2 ? n - 2 : A);
-  if ((A + 1) * (2 * n - A - 2) / 2 <= t) A++;
-  else if (A * (2 * n - A - 1) / 2 > t) A--;
-  *a = A;
-  *b = t - A * (2 * n - A - 1) / 2 + A + 1;
-}
 
 #define MAXQ 16
 #define MAXLOOP 32
@@ -669,8 +659,8 @@ __device__ void part_b(cg::thread_block_tile<G> &g, WS &ws, const MMParams &P, i
         bool act = false;
         unsigned long long cm = 0ull;
         if (p < npair) {
-          int a, b;
-          unrank2(p, ns, &a, &b);
+          const uint32_t pc = __ldg(&P.pair2[ns * (ns - 1) * (ns - 2) / 6 + p]);
+          const int a = pc & 0xff, b = pc >> 8;
           const uint32_t pb = (1u << a) | (1u << b);
           cm = ws.sclu[a] & ws.sclu[b];
           const uint32_t strut_bits = a == 0 ? (1u << b) : pb;
@@ -704,7 +694,8 @@ __device__ void part_b(cg::thread_block_tile<G> &g, WS &ws, const MMParams &P, i
         bool conic_ok = true;
         if (k < nact) {
           p = ws.plist[k];
-          unrank2(p, ns, &a, &b);
+          const uint32_t pc = __ldg(&P.pair2[ns * (ns - 1) * (ns - 2) / 6 + p]);
+          a = pc & 0xff; b = pc >> 8;
           cmk = ws.pmask[k];
           nq = __popcll(cmk);
           if (a == 0) nd.circle(b, &o, &av, &bv);
@@ -739,7 +730,7 @@ __device__ void part_b(cg::thread_block_tile<G> &g, WS &ws, const MMParams &P, i
             if (nq == 0) { ms = 0.0f; mc = 1.0f; t0 = 0.0f; dt = LMM_TWO_PI_F; vs = ve = -1; }
             else if (nq == 1) { ms = -us[0]; mc = -uc[0]; t0 = tq[0]; dt = LMM_TWO_PI_F; vs = ve = Q[0]; }
             else {
-              int j = (i + 1) % nq;
+              int j = i + 1 == nq ? 0 : i + 1;
               dt = j == 0 ? (tq[0] + LMM_TWO_PI_F) - tq[nq - 1] : tq[j] - tq[i];
               if (!(dt > 0.0f)) { e = LMM_NODE_CHAIN; break; }
               float sx = us[i] + us[j], sc = uc[i] + uc[j];
@@ -1271,17 +1262,26 @@ int metamesh_run(lmm_ctx *c) {
     if ((rc0 = dev_alloc(c->mm_side, sizeof(float4) * 5 * (2 * c->S + 1)))) return rc0;
     if ((rc0 = dev_alloc(c->mm_state, sizeof(int4) * (c->N + 1)))) return rc0;
   }
-  if (!c->tri3.p) {   // triple table for up to LMM_MAXD + 1 sides
+  // lexicographic triple and pair tables for up to LMM_MAXD + 1 sides: triples of n sides at
+  // C(n,4), then (at PAIR0) pairs of n sides at C(n,3)
+  constexpr int NS = LMM_MAXD + 1;
+  constexpr int PAIR0 = NS * (NS - 1) * (NS - 2) * (NS - 3) / 24 + NS * (NS - 1) * (NS - 2) / 6;
+  if (!c->tri3.p) {
     std::vector<uint32_t> t3;
-    for (int n = 3; n <= LMM_MAXD + 1; n++)
+    for (int n = 3; n <= NS; n++)
       for (int a = 0; a < n; a++)
         for (int b = a + 1; b < n; b++)
           for (int cc = b + 1; cc < n; cc++) t3.push_back((uint32_t)a | ((uint32_t)b << 8) | ((uint32_t)cc << 16));
+    t3.resize(PAIR0, 0u);
+    for (int n = 2; n <= NS; n++)
+      for (int a = 0; a < n; a++)
+        for (int b = a + 1; b < n; b++) t3.push_back((uint32_t)a | ((uint32_t)b << 8));
     int rc0;
     if ((rc0 = dev_alloc(c->tri3, sizeof(uint32_t) * t3.size()))) return rc0;
     CUDA_TRY(cudaMemcpy(c->tri3.p, t3.data(), sizeof(uint32_t) * t3.size(), cudaMemcpyHostToDevice));
   }
   P.tri3 = (const uint32_t *)c->tri3.p;
+  P.pair2 = (const uint32_t *)c->tri3.p + PAIR0;
   P.side = (float4 *)c->mm_side.p;
   P.state = (int4 *)c->mm_state.p;
   const int *bn = (const int *)c->bucket_nodes.p;
