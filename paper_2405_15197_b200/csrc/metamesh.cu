@@ -789,7 +789,7 @@ __device__ void part_b(cg::thread_block_tile<G> &g, WS &ws, const MMParams &P, i
         for (int i = 0; i < nint && !e; i++) {
           const bool ok = i < QL ? qok[qbase + i] != 0 : okv[i];
           if (!ok) continue;
-          vsv[cnt] = vsv[i]; vev[cnt] = vev[i]; t0v[cnt] = t0v[i]; dtv[cnt] = dtv[i]; tmv[cnt] = tmv[i];
+          if (cnt != i) { vsv[cnt] = vsv[i]; vev[cnt] = vev[i]; t0v[cnt] = t0v[i]; dtv[cnt] = dtv[i]; tmv[cnt] = tmv[i]; }
           if (vsv[cnt] < 0) closed = 1;
           cnt++;
         }
