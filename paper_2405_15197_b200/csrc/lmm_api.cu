@@ -97,23 +97,25 @@ static void free_all(lmm_ctx *c) {
   DevBuf *bufs[] = {&c->node, &c->ends, &c->csr_off, &c->csr_ent, &c->csr_tmp, &c->strut_csr, &c->deg_hist, &c->bucket_nodes,
                     &c->bucket_cnt, &c->node_hdr, &c->vert, &c->arc, &c->loop_hdr, &c->loop, &c->hole_hdr,
                     &c->hole_ent, &c->band, &c->strut_off, &c->node_hole0, &c->node_hole0_64, &c->hole_M,
-                    &c->hole_off, &c->hole_bp, &c->hole_node, &c->node_mask, &c->strut_mask, &c->mbits, &c->macc, &c->cmap, &c->brec, &c->ring_n, &c->tmp64, &c->scratch, &c->mm_side, &c->mm_state, &c->tri3, &c->scan_tmp, &c->stage[0], &c->stage[1]};
+                    &c->hole_off, &c->hole_bp, &c->hole_node, &c->node_mask, &c->strut_mask, &c->mbits, &c->macc, &c->cmap, &c->brec, &c->ring_n, &c->tmp64, &c->scratch, &c->mm_side, &c->mm_state, &c->tri3, &c->scan_tmp};
   for (DevBuf *b : bufs) dev_free(*b);
+  for (int i = 0; i < LMM_NSTAGE; i++) dev_free(c->stage[i]);
 }
 
 LMM_API void lmm_destroy(lmm_ctx *c) {
   if (!c) return;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream); else cudaDeviceSynchronize();
-  for (int i = 0; i < 2; i++)
+  for (int i = 0; i < LMM_NSTAGE; i++)
     if (c->copy_stream[i]) cudaStreamSynchronize(c->copy_stream[i]);
   free_all(c);
-  for (int i = 0; i < 2; i++) {
+  for (int i = 0; i < 2; i++)
     if (c->pinned[i]) cudaFreeHost(c->pinned[i]);
+  for (int i = 0; i < LMM_NSTAGE; i++) {
     if (c->stage_ev[i]) cudaEventDestroy(c->stage_ev[i]);
     if (c->emit_ev[i]) cudaEventDestroy(c->emit_ev[i]);
   }
-  for (int i = 0; i < 2; i++)
+  for (int i = 0; i < LMM_NSTAGE; i++)
     if (c->copy_stream[i]) cudaStreamDestroy(c->copy_stream[i]);
   resolve_timers(c);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
@@ -259,9 +261,12 @@ LMM_API int lmm_write_triangles(lmm_ctx *c, int64_t first, int64_t count, void *
   // host destination: emit chunks into two device staging buffers on the context stream
   // and DMA each to the caller's memory on a copy stream, so the copy of chunk b overlaps
   // the emission of chunk b + 1
-  const int64_t CH = 1ll << 22;   // triangles per chunk (200 MiB)
+#ifndef LMM_STAGE_LOG2
+#define LMM_STAGE_LOG2 22
+#endif
+  const int64_t CH = 1ll << LMM_STAGE_LOG2;   // triangles per chunk (2^22: 200 MiB)
   int rc;
-  for (int i = 0; i < 2; i++) {
+  for (int i = 0; i < LMM_NSTAGE; i++) {
     if ((rc = dev_alloc(c->stage[i], (size_t)CH * 50))) return rc;
     if (!c->stage_ev[i]) CUDA_TRY(cudaEventCreateWithFlags(&c->stage_ev[i], cudaEventDisableTiming));
     if (!c->emit_ev[i]) CUDA_TRY(cudaEventCreateWithFlags(&c->emit_ev[i], cudaEventDisableTiming));
@@ -269,8 +274,8 @@ LMM_API int lmm_write_triangles(lmm_ctx *c, int64_t first, int64_t count, void *
   }
   unsigned char *dst = (unsigned char *)out;
   int b = 0;
-  bool used[2] = {false, false};
-  for (int64_t t = 0; t < count; t += CH, b ^= 1) {
+  bool used[LMM_NSTAGE] = {};
+  for (int64_t t = 0; t < count; t += CH, b = b + 1 == LMM_NSTAGE ? 0 : b + 1) {
     int64_t n = count - t < CH ? count - t : CH;
     if (used[b]) CUDA_TRY(cudaStreamWaitEvent(c->stream, c->stage_ev[b], 0));   // buffer b copied out
     if ((rc = triangulate_emit(c, first + t, n, c->stage[b].p, c->stream))) return rc;
@@ -280,7 +285,7 @@ LMM_API int lmm_write_triangles(lmm_ctx *c, int64_t first, int64_t count, void *
     CUDA_TRY(cudaEventRecord(c->stage_ev[b], c->copy_stream[b]));
     used[b] = true;
   }
-  for (int i = 0; i < 2; i++) CUDA_TRY(cudaStreamSynchronize(c->copy_stream[i]));
+  for (int i = 0; i < LMM_NSTAGE; i++) CUDA_TRY(cudaStreamSynchronize(c->copy_stream[i]));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
   return LMM_OK;
 }

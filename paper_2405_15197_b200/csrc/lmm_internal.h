@@ -70,12 +70,15 @@ struct lmm_ctx {
   DevBuf scan_tmp;   // scan tile sums (all recursion levels)
   int64_t *pinned_scalar = nullptr;   // pinned host words for scan totals / flags
   unsigned long long *pinned_hist = nullptr;   // pinned degree histogram + bucket bases
-  DevBuf stage[2];   // device staging for host output
+#ifndef LMM_NSTAGE
+#define LMM_NSTAGE 3      // device staging buffers (and copy streams) of host output
+#endif
+  DevBuf stage[LMM_NSTAGE];   // device staging for host output
   void *pinned[2] = {nullptr, nullptr};
   size_t pinned_bytes = 0;
-  cudaEvent_t stage_ev[2] = {nullptr, nullptr};   // staging buffer b free again (copy done)
-  cudaEvent_t emit_ev[2] = {nullptr, nullptr};    // staging buffer b filled (emit done)
-  cudaStream_t copy_stream[2] = {nullptr, nullptr};   // device -> host copies of host output (one per staging buffer)
+  cudaEvent_t stage_ev[LMM_NSTAGE] = {};   // staging buffer b free again (copy done)
+  cudaEvent_t emit_ev[LMM_NSTAGE] = {};    // staging buffer b filled (emit done)
+  cudaStream_t copy_stream[LMM_NSTAGE] = {};   // device -> host copies of host output (one per staging buffer)
   // timing
   bool timing = false;
   double k_ms[LMM_K_NCLASSES] = {0};
