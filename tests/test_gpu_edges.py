@@ -138,3 +138,24 @@ def test_umbrella_vertex_capacity_like_the_oracle(k):
     st = mm.stats()
     assert st["n_error_nodes"] == (1 if k >= 12 else 0)
     mm.close()
+
+
+def test_index_region_worked_example():
+    """PAPER.md Sec. 4.3.2: an index region [0, 5, 15, 32, 47, ...] is the exclusive prefix sum of
+    per-item counts 5, 10, 17, 15.  Four hub nodes of degree 5, 10, 17 and 15 (ids 0-3, leaves
+    after them) must give exactly those CSR offsets from the device scan."""
+    from paper_2405_15197_b200 import MetaMesher, lmm_buffer
+    from paper_2405_15197_b200 import binding as B
+    degs = [5, 10, 17, 15]
+    xyz, ends = [], []
+    hubs = [np.array([4.0 * i, 0.0, 0.0]) for i in range(4)]
+    xyz.extend(hubs)
+    for h, dg in enumerate(degs):
+        for u in _fib_dirs(dg):
+            ends.append((h, len(xyz)))
+            xyz.append(hubs[h] + u)
+    lat = synth.Lattice(np.array(xyz, np.float32), np.array(ends, np.int64), np.full(len(xyz), 0.05, np.float32))
+    mm = MetaMesher(0).load_lattice(lat)
+    off = lmm_buffer(mm.h, B.LMM_BUF_CSR_OFF, np.int32)
+    assert off[:5].tolist() == [0, 5, 15, 32, 47]
+    mm.close()
