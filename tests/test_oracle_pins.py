@@ -448,3 +448,35 @@ def test_oracle_outputs_finite_on_random_lattices(oracle_mod, seed):
         T = o.triangulate(ce)
         tris = o.write_triangles()
         assert len(tris) == T and np.isfinite(tris).all()
+
+
+@pytest.mark.parametrize("ce", [0.05, 5e-3])
+def test_emitted_arc_chords_within_chord_error(oracle_mod, ce):
+    """Chord conformance of the subdivided meta-mesh arcs (Eq. 11-12): a chord spanning
+    parameter step dt/N of an arc o + a sin t + b cos t deviates from the arc by at most
+    (1 - cos(step/2)) |A| with |A| the largest semi-axis (the arc is an affine image of a circle),
+    i.e. by at most CE times the semi-axis; checked by dense sampling of every segment of every
+    arc of a graded, jittered octet lattice."""
+    lat = synth.jitter(synth.graded_radii(synth.octet(2, 2, 2), 0.03, 0.06), 0.04, 5)
+    o = oracle_mod.Oracle.from_lattice(lat)
+    assert o.metamesh() == 0
+    th = oracle_mod.theta0(ce)
+    worst = 0.0
+    for n in range(lat.n_nodes):
+        for rec in o.node(n)["a_f64"]:
+            t0, dt = rec[0], rec[1]
+            oo, a, b = rec[2:5], rec[5:8], rec[8:11]
+            N = oracle_mod.subdiv_count(np.float32(dt), th)
+            semi = max(np.linalg.norm(a), np.linalg.norm(b))
+            step = dt / N
+            ts = t0 + step * np.arange(N + 1)
+            P = oo + np.outer(np.sin(ts), a) + np.outer(np.cos(ts), b)
+            for i in range(N):
+                u = np.linspace(0.0, 1.0, 33)[1:-1]
+                curve = oo + np.outer(np.sin(ts[i] + u * step), a) + np.outer(np.cos(ts[i] + u * step), b)
+                seg = P[i + 1] - P[i]
+                w = curve - P[i]
+                lam = np.clip(w @ seg / max(seg @ seg, 1e-300), 0.0, 1.0)
+                dev = np.linalg.norm(w - np.outer(lam, seg), axis=1).max()
+                worst = max(worst, dev / (ce * semi))
+    assert 0.5 < worst <= 1.0 + 1e-6   # tight: some segment comes close to the bound
