@@ -2,17 +2,21 @@
 // (Sec. 5: Eq. 11 subdivision counts, Eq. 12 uniform parameters, strut bands
 // "by connecting these vertices", Eq. 13 hole fans, Algorithm 1).
 //
-// Count pass (one thread per strut / per node): N per arc from the chord error, loop
-// point counts, the band rotation, hole sizes and fan centres; device scans give the
-// output offsets; then every band's stitch merge is run once and stored as one bit per
-// triangle (advance ring A / ring B) with a per-32-triangle prefix count, and a map from
-// output chunk to its first band/hole.
+// Count pass: Eq. 11 N per arc and the point offsets of every ring (one thread per strut
+// end, a node's rings on consecutive threads), band sizes per strut, hole sizes and fan
+// centres per node; device scans give the output offsets; then every band's rotation and
+// stitch merge is run once (one thread per strut, forward key cursors) and stored as one bit
+// per triangle (advance ring A / ring B) with a per-32-triangle prefix count, together with
+// the band's 64-byte emit record; a map from 1024-triangle output chunks to their first
+// band/hole bounds any requested range.
 //
-// Emit pass: output-centric persistent CTAs, each owning 1024-triangle chunks of the
-// global order.  A thread takes 4 consecutive triangles: its ring positions come from
-// the merge bits in O(1), it walks both rings with incremental cursors and computes one
-// new Eq. 12 point per triangle.  The 50-byte STL records are assembled in shared
-// memory and leave with one TMA bulk store (cp.async.bulk.global.shared::cta) per chunk.
+// Emit pass: warps grid-stride over the bands (then the hole fans) of the requested range.
+// A band is fetched as its record, then its loop entries, arcs and start vertices (cp.async
+// stages overlapped with the previous band); its ring points are computed once into a
+// shared-memory cache sized per triangulation; lanes assemble pairs of 50-byte STL records
+// (ring positions from ballot prefix-popcounts of the merge bits) in a per-warp staging
+// buffer, which leaves as one TMA bulk copy (cp.async.bulk.global.shared::cta) per
+// 56-triangle group on the 16-byte output grid.
 //
 // Decision arithmetic (N, stitch keys, band rotation, merge) is binary32 with the
 // operation order of DESIGN.md Sec. 4.5 written with explicit round-to-nearest
