@@ -1,6 +1,9 @@
 // metamesh.cu -- per-node meta-mesh kernel (Sec. 4.1, 4.3.1, Eq. 7-9).
 //
-// One lane group (a warp) owns one lattice node.  Lanes map to the node's struts for
+// One lane group (8, 16 or 32 lanes by degree bucket: four, two or one node per warp) owns
+// one lattice node; three part kernels (A: sides, junctions, vertex clusters; B: arcs;
+// C: loops, holes, slab write) hand the node over through side records.  Lanes map to the
+// node's struts for
 // the per-side set-up, to (side, side, side) triples for the junction solve, to side
 // pairs for the arc walk (Eq. 7 ellipse + interval tests, Eq. 8-9 read as
 // the half-space tests at interval midpoints) and to struts for loop assembly; warp
