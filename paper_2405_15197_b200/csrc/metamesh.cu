@@ -137,6 +137,17 @@ __device__ __forceinline__ float2 add2(float2 a, float2 b) {
   asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2u(a)), "l"(f2u(b)));
   return u2f(r);
 }
+// h_m at two points at once, each lane rounded like the scalar spec ((w.x y.x + w.y y.y) +
+// w.z y.z) + (-e) + (-tau): the three products packed, the two sums of products scalar --
+// ptxas contracts an add.rn.f32x2 of a mul.rn.f32x2 result into FFMA2 even under -fmad=false
+// (scalar add.rn is never contracted), so packed adds only take operands that are not products.
+// tests/test_abi.py checks the meta-mesh SASS for FFMA2.
+__device__ __forceinline__ float2 side_h2(float4 p0, float4 p1, float2 Yx, float2 Yy, float2 Yz, float2 nT) {
+  const float2 a = mul2(make_float2(p0.x, p0.y), Yx), b = mul2(make_float2(p0.z, p0.w), Yy);
+  const float2 c = mul2(make_float2(p1.x, p1.y), Yz);
+  const float2 h = make_float2(__fadd_rn(__fadd_rn(a.x, b.x), c.x), __fadd_rn(__fadd_rn(a.y, b.y), c.y));
+  return add2(add2(h, make_float2(p1.z, p1.w)), nT);
+}
 
 template <class WS> struct Node {
   WS &w;
@@ -219,9 +230,7 @@ template <class WS> struct Node {
     uint32_t v0 = 0u, v1 = 0u, mb = 2u;   // sides violated by each root (bit m)
     for (int m = 1; m <= d; m++, mb <<= 1) {
       const float4 p0 = w.wp[m][0], p1 = w.wp[m][1];
-      float2 h = add2(mul2(make_float2(p0.x, p0.y), Yx), mul2(make_float2(p0.z, p0.w), Yy));
-      h = add2(h, mul2(make_float2(p1.x, p1.y), Yz));
-      h = add2(add2(h, make_float2(p1.z, p1.w)), nT);
+      const float2 h = side_h2(p0, p1, Yx, Yy, Yz, nT);
       v0 |= h.x > delta ? mb : 0u;
       v1 |= h.y > delta ? mb : 0u;
     }
@@ -775,9 +784,7 @@ __device__ void part_b(cg::thread_block_tile<G> &g, WS &ws, const MMParams &P, i
           uint32_t v0 = 0u, v1 = 0u, mb = 2u;   // sides violated at each midpoint (bit mm)
           for (int mm = 1; mm <= d; mm++, mb <<= 1) {
             const float4 p0 = ws.wp[mm][0], p1 = ws.wp[mm][1];
-            float2 h = add2(mul2(make_float2(p0.x, p0.y), Yx), mul2(make_float2(p0.z, p0.w), Yy));
-            h = add2(h, mul2(make_float2(p1.x, p1.y), Yz));
-            h = add2(add2(h, make_float2(p1.z, p1.w)), nT);
+            const float2 h = side_h2(p0, p1, Yx, Yy, Yz, nT);
             v0 |= h.x > th0 ? mb : 0u;
             v1 |= h.y > th1 ? mb : 0u;
           }

@@ -43,6 +43,22 @@ def test_library_is_sm100a_code(lib):
     assert "sm_100a" in out
 
 
+def test_metamesh_kernels_have_no_fused_multiply_adds(lib):
+    """The meta-mesh decisions follow the binary32 specification op by op:
+    no product may be fused into an add.  Scalar code is compiled -fmad=false; packed f32x2
+    sums of products would be contracted to FFMA2 by ptxas regardless, so the SASS must hold
+    none (FFMA from the correctly rounded division / square-root sequences is fine)."""
+    sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", lib], capture_output=True, text=True, check=True).stdout
+    fused, fn = [], "?"
+    for line in sass.splitlines():
+        if "Function :" in line:
+            fn = line.split("Function :")[1].strip()
+        elif "metamesh_kernel" in fn and re.search(r"\bFFMA2\b", line):
+            fused.append((fn, line.strip()))
+    assert "metamesh_kernel" in sass
+    assert not fused, fused[:3]
+
+
 def test_no_gpu_means_loud_failure(lib):
     import torch
     if torch.cuda.is_available():
