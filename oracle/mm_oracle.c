@@ -300,7 +300,11 @@ static void build_sides64(const orc_lat *L, int64_t n, side64 *S) {
   }
 }
 
-static inline float h32(const side32 *S, int k, f3 y) { return k == 0 ? 0.0f : f_dot(S[k].w, y) - S[k].e; }
+/* side function h_k(y) = w_k . y - e_k: the dot product as two fused
+ * multiply-adds, fma(w.z, y.z, fma(w.y, y.y, w.x y.x)) - e (C99 fmaf: one rounding each) */
+static inline float h32(const side32 *S, int k, f3 y) {
+  return k == 0 ? 0.0f : fmaf(S[k].w.z, y.z, fmaf(S[k].w.y, y.y, S[k].w.x * y.x)) - S[k].e;
+}
 
 /* ------------------------------------------------------------------------- */
 /* triple junctions: points where h_a = h_b = h_c = sqrt(|y|^2 - R^2)         */

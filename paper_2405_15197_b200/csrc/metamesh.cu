@@ -137,15 +137,19 @@ __device__ __forceinline__ float2 add2(float2 a, float2 b) {
   asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2u(a)), "l"(f2u(b)));
   return u2f(r);
 }
-// h_m at two points at once, each lane rounded like the scalar spec ((w.x y.x + w.y y.y) +
-// w.z y.z) + (-e) + (-tau): the three products packed, the two sums of products scalar --
-// ptxas contracts an add.rn.f32x2 of a mul.rn.f32x2 result into FFMA2 even under -fmad=false
-// (scalar add.rn is never contracted), so packed adds only take operands that are not products.
-// tests/test_abi.py checks the meta-mesh SASS for FFMA2.
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(f2u(a)), "l"(f2u(b)), "l"(f2u(c)));
+  return u2f(r);
+}
+// h_m at two points at once, each lane rounded like the scalar hs(m, y) - tau: the product, two
+// explicit fused multiply-adds, then + (-e) and + (-tau).  (Never write a packed add of a packed
+// product: ptxas contracts add.rn.f32x2 of a mul.rn.f32x2 result into FFMA2 even under
+// -fmad=false; tests/test_abi.py checks that every FFMA2 of the meta-mesh is one of these.)
 __device__ __forceinline__ float2 side_h2(float4 p0, float4 p1, float2 Yx, float2 Yy, float2 Yz, float2 nT) {
-  const float2 a = mul2(make_float2(p0.x, p0.y), Yx), b = mul2(make_float2(p0.z, p0.w), Yy);
-  const float2 c = mul2(make_float2(p1.x, p1.y), Yz);
-  const float2 h = make_float2(__fadd_rn(__fadd_rn(a.x, b.x), c.x), __fadd_rn(__fadd_rn(a.y, b.y), c.y));
+  float2 h = mul2(make_float2(p0.x, p0.y), Yx);
+  h = fma2(make_float2(p0.z, p0.w), Yy, h);
+  h = fma2(make_float2(p1.x, p1.y), Yz, h);
   return add2(add2(h, make_float2(p1.z, p1.w)), nT);
 }
 
@@ -161,10 +165,10 @@ template <class WS> struct Node {
   __device__ f3 E2(int k) const { return F3(w.e2x[k], w.e2y[k], w.e2z[k]); }
   __device__ f3 V(int q) const { return F3(w.vx[q], w.vy[q], w.vz[q]); }
   __device__ float h(int k, f3 y) const { return k == 0 ? 0.0f : hs(k, y); }
-  // strut side k >= 1: (w.x y.x + w.y y.y) + w.z y.z - e, as f_dot
+  // strut side k >= 1: fma(w.z, y.z, fma(w.y, y.y, w.x y.x)) - e
   __device__ float hs(int k, f3 y) const {
     const float4 q = w.w4[k];
-    return ((q.x * y.x + q.y * y.y) + q.z * y.z) - q.w;
+    return __fsub_rn(__fmaf_rn(q.z, y.z, __fmaf_rn(q.y, y.y, __fmul_rn(q.x, y.x))), q.w);
   }
 
   // triple junction (oracle junction32), without branches: the three

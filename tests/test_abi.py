@@ -43,20 +43,60 @@ def test_library_is_sm100a_code(lib):
     assert "sm_100a" in out
 
 
-def test_metamesh_kernels_have_no_fused_multiply_adds(lib):
+def _packed_adds_of_products(ptx):
+    """Packed adds (add/sub .f32x2) fed -- through any chain of bit moves -- by a packed
+    product (mul .f32x2): the pattern ptxas contracts into FFMA2 even under -fmad=false."""
+    bad = []
+    for body in re.split(r"\.(?:entry|func)\s", ptx)[1:]:
+        name = body.split("(", 1)[0].strip()
+        ins = []
+        for line in body.splitlines():
+            line = line.strip()
+            m = re.match(r"(?:@!?%\w+\s+)?([a-z][\w.]*)\s+(.*);", line)
+            if not m or line.startswith("//"):
+                continue
+            op, args = m.group(1), m.group(2)
+            if op.startswith(("st.", "bra", "ret", "bar", "setp", "atom", "red.")):
+                continue
+            dst, _, src = args.partition(",") if not args.startswith("{") else args.partition("},")
+            ins.append((op, set(re.findall(r"%\w+", dst)), set(re.findall(r"%\w+", src))))
+        taint, changed = set(), True
+        while changed:                                  # fixed point (loops carry values back)
+            changed = False
+            for op, d, sr in ins:
+                if re.match(r"mul(\.rn)?\.f32x2", op):
+                    new = d - taint
+                elif op.startswith(("fma", "add", "sub", "mul", "div", "sqrt", "rcp")) or ".f32" in op:
+                    new = set()                         # arithmetic consumes the product
+                else:
+                    new = d - taint if sr & taint else set()
+                if new:
+                    taint |= new
+                    changed = True
+        bad += [(name, op) for op, d, sr in ins if re.match(r"(add|sub)(\.rn)?\.f32x2", op) and sr & taint]
+    return bad
+
+
+def test_metamesh_has_no_contractible_packed_multiply_add(lib):
     """The meta-mesh decisions follow the binary32 specification op by op:
-    no product may be fused into an add.  Scalar code is compiled -fmad=false; packed f32x2
-    sums of products would be contracted to FFMA2 by ptxas regardless, so the SASS must hold
-    none (FFMA from the correctly rounded division / square-root sequences is fine)."""
-    sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", lib], capture_output=True, text=True, check=True).stdout
-    fused, fn = [], "?"
-    for line in sass.splitlines():
-        if "Function :" in line:
-            fn = line.split("Function :")[1].strip()
-        elif "metamesh_kernel" in fn and re.search(r"\bFFMA2\b", line):
-            fused.append((fn, line.strip()))
-    assert "metamesh_kernel" in sass
-    assert not fused, fused[:3]
+    scalar code is compiled -fmad=false, but ptxas contracts a packed add of a packed product
+    into FFMA2 regardless.  The PTX of metamesh.cu (same flags) must hold no such pair -- the
+    side function's fused multiply-adds are written as explicit fma.rn.f32x2 (Sec. 4.4)."""
+    import tempfile
+    from paper_2405_15197_b200 import build as b
+    with tempfile.TemporaryDirectory() as td:
+        out = os.path.join(td, "mm.ptx")
+        subprocess.run([b.NVCC, "-gencode", "arch=compute_100a,code=compute_100a", "-O3", "-std=c++17",
+                        "--expt-relaxed-constexpr", *b.SOURCES["metamesh.cu"], "-ptx",
+                        os.path.join(b.SRC, "metamesh.cu"), "-o", out], check=True, capture_output=True)
+        ptx = open(out).read()
+    assert re.search(r"mul\.rn\.f32x2", ptx) and re.search(r"fma\.rn\.f32x2", ptx)
+    # the checker itself must see the hazard: a packed add of a packed product
+    probe = ".entry probe(\n\tmul.rn.f32x2 %rd1, %rd2, %rd3;\n\tmov.b64 {%r1, %r2}, %rd1;\n" \
+            "\tmov.b64 %rd4, {%r1, %r2};\n\tadd.rn.f32x2 %rd5, %rd4, %rd6;\n"
+    assert _packed_adds_of_products(probe)
+    bad = _packed_adds_of_products(ptx)
+    assert not bad, bad[:3]
 
 
 def test_no_gpu_means_loud_failure(lib):
