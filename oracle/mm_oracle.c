@@ -75,9 +75,11 @@ static inline f3 f_sub(f3 a, f3 b) { return F3(a.x - b.x, a.y - b.y, a.z - b.z);
 static inline f3 f_add(f3 a, f3 b) { return F3(a.x + b.x, a.y + b.y, a.z + b.z); }
 static inline f3 f_scl(f3 a, float s) { return F3(a.x * s, a.y * s, a.z * s); }
 static inline f3 f_div(f3 a, float s) { return F3(a.x / s, a.y / s, a.z / s); }
-static inline float f_dot(f3 a, f3 b) { return (a.x * b.x + a.y * b.y) + a.z * b.z; }
+/* dot and cross products with explicit fused multiply-adds (C99 fmaf, one
+ * rounding each): dot = fma(a.z, b.z, fma(a.y, b.y, a.x b.x)), cross.x = fma(a.y, b.z, -(a.z b.y)) */
+static inline float f_dot(f3 a, f3 b) { return fmaf(a.z, b.z, fmaf(a.y, b.y, a.x * b.x)); }
 static inline f3 f_cross(f3 a, f3 b) {
-  return F3(a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x);
+  return F3(fmaf(a.y, b.z, -(a.z * b.y)), fmaf(a.z, b.x, -(a.x * b.z)), fmaf(a.x, b.y, -(a.y * b.x)));
 }
 static inline f3 f_nrm(f3 a) { return f_div(a, sqrtf(f_dot(a, a))); }
 
@@ -300,11 +302,8 @@ static void build_sides64(const orc_lat *L, int64_t n, side64 *S) {
   }
 }
 
-/* side function h_k(y) = w_k . y - e_k: the dot product as two fused
- * multiply-adds, fma(w.z, y.z, fma(w.y, y.y, w.x y.x)) - e (C99 fmaf: one rounding each) */
-static inline float h32(const side32 *S, int k, f3 y) {
-  return k == 0 ? 0.0f : fmaf(S[k].w.z, y.z, fmaf(S[k].w.y, y.y, S[k].w.x * y.x)) - S[k].e;
-}
+/* side function h_k(y) = w_k . y - e_k, the dot product as in Sec. 4.1 */
+static inline float h32(const side32 *S, int k, f3 y) { return k == 0 ? 0.0f : f_dot(S[k].w, y) - S[k].e; }
 
 /* ------------------------------------------------------------------------- */
 /* triple junctions: points where h_a = h_b = h_c = sqrt(|y|^2 - R^2)         */

@@ -67,9 +67,11 @@ __device__ __forceinline__ f3 f_sub(f3 a, f3 b) { return F3(a.x - b.x, a.y - b.y
 __device__ __forceinline__ f3 f_add(f3 a, f3 b) { return F3(a.x + b.x, a.y + b.y, a.z + b.z); }
 __device__ __forceinline__ f3 f_scl(f3 a, float s) { return F3(a.x * s, a.y * s, a.z * s); }
 __device__ __forceinline__ f3 f_div(f3 a, float s) { return F3(a.x / s, a.y / s, a.z / s); }
-__device__ __forceinline__ float f_dot(f3 a, f3 b) { return (a.x * b.x + a.y * b.y) + a.z * b.z; }
+// dot and cross products with explicit fused multiply-adds
+__device__ __forceinline__ float f_dot(f3 a, f3 b) { return __fmaf_rn(a.z, b.z, __fmaf_rn(a.y, b.y, __fmul_rn(a.x, b.x))); }
 __device__ __forceinline__ f3 f_cross(f3 a, f3 b) {
-  return F3(a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x);
+  return F3(__fmaf_rn(a.y, b.z, -__fmul_rn(a.z, b.y)), __fmaf_rn(a.z, b.x, -__fmul_rn(a.x, b.z)),
+            __fmaf_rn(a.x, b.y, -__fmul_rn(a.y, b.x)));
 }
 __device__ __forceinline__ f3 f_nrm(f3 a) { return f_div(a, sqrtf(f_dot(a, a))); }
 

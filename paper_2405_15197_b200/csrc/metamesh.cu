@@ -168,7 +168,7 @@ template <class WS> struct Node {
   // strut side k >= 1: fma(w.z, y.z, fma(w.y, y.y, w.x y.x)) - e
   __device__ float hs(int k, f3 y) const {
     const float4 q = w.w4[k];
-    return __fsub_rn(__fmaf_rn(q.z, y.z, __fmaf_rn(q.y, y.y, __fmul_rn(q.x, y.x))), q.w);
+    return __fsub_rn(f_dot(F3(q.x, q.y, q.z), y), q.w);
   }
 
   // triple junction (oracle junction32), without branches: the three
