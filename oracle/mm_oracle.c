@@ -323,23 +323,24 @@ static int junction32(const side32 *S, float R, int a, int b, int c, f3 *y, floa
   if (!(mm > (1e-8f * nn1) * nn2)) return 0;
   f3 c1 = f_cross(n2, m), c2 = f_cross(m, n1);
   float imm = 1.0f / mm;
-  f3 y0 = F3((q1 * c1.x + q2 * c2.x) * imm, (q1 * c1.y + q2 * c2.y) * imm, (q1 * c1.z + q2 * c2.z) * imm);
+  /* the fused multiply-adds of the junction solve */
+  f3 y0 = F3(fmaf(q2, c2.x, q1 * c1.x) * imm, fmaf(q2, c2.y, q1 * c1.y) * imm, fmaf(q2, c2.z, q1 * c1.z) * imm);
   float iml = 1.0f / sqrtf(mm);
   f3 mh = f_scl(m, iml);
   float tau0 = f_dot(Wa, y0) - Ea;
   float tau1 = f_dot(Wa, mh);
-  float A = 1.0f - tau1 * tau1;
+  float A = fmaf(-tau1, tau1, 1.0f);
   if (!(A > 1e-6f)) return 0;
-  float Bp = f_dot(y0, mh) - tau0 * tau1;
-  float C = (f_dot(y0, y0) - R * R) - tau0 * tau0;
-  float disc = Bp * Bp - A * C;
+  float Bp = fmaf(-tau0, tau1, f_dot(y0, mh));
+  float C = fmaf(-tau0, tau0, fmaf(-R, R, f_dot(y0, y0)));
+  float disc = fmaf(Bp, Bp, -(A * C));
   if (disc < 0.0f) return 0;
   float sq = sqrtf(disc);
   float iA = 1.0f / A;
   float lam[2] = {(-Bp - sq) * iA, (-Bp + sq) * iA};
   for (int r = 0; r < 2; r++) {
-    y[r] = f_add(y0, f_scl(mh, lam[r]));
-    tau[r] = tau0 + lam[r] * tau1;
+    y[r] = F3(fmaf(mh.x, lam[r], y0.x), fmaf(mh.y, lam[r], y0.y), fmaf(mh.z, lam[r], y0.z));
+    tau[r] = fmaf(lam[r], tau1, tau0);
   }
   return 2;
 }

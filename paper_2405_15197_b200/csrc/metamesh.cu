@@ -187,26 +187,27 @@ template <class WS> struct Node {
     mm = ok ? mm : 1.0f;
     f3 c1 = f_cross(n2, m), c2 = f_cross(m, n1);
     float imm = 1.0f / mm;
-    f3 y0 = F3((q1 * c1.x + q2 * c2.x) * imm, (q1 * c1.y + q2 * c2.y) * imm, (q1 * c1.z + q2 * c2.z) * imm);
+    f3 y0 = F3(__fmaf_rn(q2, c2.x, __fmul_rn(q1, c1.x)) * imm, __fmaf_rn(q2, c2.y, __fmul_rn(q1, c1.y)) * imm,
+               __fmaf_rn(q2, c2.z, __fmul_rn(q1, c1.z)) * imm);
     float iml = 1.0f / sqrtf(mm);
     f3 mh = f_scl(m, iml);
     float tau0 = f_dot(Wa, y0) - Ea;
     float tau1 = f_dot(Wa, mh);
-    float A = 1.0f - tau1 * tau1;
+    float A = __fmaf_rn(-tau1, tau1, 1.0f);
     ok = ok && A > 1e-6f;
     A = ok ? A : 1.0f;
-    float Bp = f_dot(y0, mh) - tau0 * tau1;
-    float C = (f_dot(y0, y0) - R * R) - tau0 * tau0;
-    float disc = Bp * Bp - A * C;
+    float Bp = __fmaf_rn(-tau0, tau1, f_dot(y0, mh));
+    float C = __fmaf_rn(-tau0, tau0, __fmaf_rn(-R, R, f_dot(y0, y0)));
+    float disc = __fmaf_rn(Bp, Bp, -__fmul_rn(A, C));
     ok = ok && !(disc < 0.0f);
     disc = ok ? disc : 0.0f;
     float sq = sqrtf(disc);
     float iA = 1.0f / A;
     float l0 = (-Bp - sq) * iA, l1 = (-Bp + sq) * iA;
-    y[0] = f_add(y0, f_scl(mh, l0));
-    tau[0] = tau0 + l0 * tau1;
-    y[1] = f_add(y0, f_scl(mh, l1));
-    tau[1] = tau0 + l1 * tau1;
+    y[0] = F3(__fmaf_rn(mh.x, l0, y0.x), __fmaf_rn(mh.y, l0, y0.y), __fmaf_rn(mh.z, l0, y0.z));
+    tau[0] = __fmaf_rn(l0, tau1, tau0);
+    y[1] = F3(__fmaf_rn(mh.x, l1, y0.x), __fmaf_rn(mh.y, l1, y0.y), __fmaf_rn(mh.z, l1, y0.z));
+    tau[1] = __fmaf_rn(l1, tau1, tau0);
     return ok;
   }
 
