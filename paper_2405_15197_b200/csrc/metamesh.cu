@@ -145,7 +145,7 @@ __device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
 // h_m at two points at once, each lane rounded like the scalar hs(m, y) - tau: the product, two
 // explicit fused multiply-adds, then + (-e) and + (-tau).  (Never write a packed add of a packed
 // product: ptxas contracts add.rn.f32x2 of a mul.rn.f32x2 result into FFMA2 even under
-// -fmad=false; tests/test_abi.py checks that every FFMA2 of the meta-mesh is one of these.)
+// -fmad=false; tests/test_abi.py checks the PTX for such pairs.)
 __device__ __forceinline__ float2 side_h2(float4 p0, float4 p1, float2 Yx, float2 Yy, float2 Yz, float2 nT) {
   float2 h = mul2(make_float2(p0.x, p0.y), Yx);
   h = fma2(make_float2(p0.z, p0.w), Yy, h);
