@@ -516,15 +516,19 @@ __device__ void part_a(cg::thread_block_tile<G> &g, WS &ws, const MMParams &P, i
       for (int cj = 0; cj < nj; cj += G) {
         const int j = cj + lane;
         const float4 pj = j < nj ? ws.jp[j] : make_float4(0.f, 0.f, 0.f, 0.f);
-        unsigned long long m = 0ull;
-        #pragma unroll 1
-        for (int k = 0; k < nj; k++) {
+        // max-norm distance (exact: max and abs do not round); bits shifted in from the top
+        // junction down, as two 32-bit halves
+        auto near = [&](int k) -> uint32_t {
           const float4 pk = ws.jp[k];
           const float dm = fmaxf(fmaxf(fabsf(pj.x - pk.x), fabsf(pj.y - pk.y)), fabsf(pj.z - pk.z));
-          const bool cl = dm <= dc;   // max-norm distance (exact: max and abs do not round)
-          m |= (unsigned long long)cl << k;
-        }
-        if (j < nj) msk[j] = m;
+          return dm <= dc ? 1u : 0u;
+        };
+        uint32_t hi = 0u, lo = 0u;
+        #pragma unroll 4
+        for (int k = nj - 1; k >= 32; k--) hi = (hi << 1) | near(k);
+        #pragma unroll 4
+        for (int k = (nj < 32 ? nj : 32) - 1; k >= 0; k--) lo = (lo << 1) | near(k);
+        if (j < nj) msk[j] = ((unsigned long long)hi << 32) | lo;
       }
       g.sync();
       for (;;) {
