@@ -17,7 +17,8 @@
  * exist, loop order, subdivision counts N, band stitching) is taken in IEEE
  * binary32 -- the paper's precision (Sec. 4.2.1: "each parameter occupies
  * a 4-byte floating-point number in GPU") -- with the operation order written
- * below (compile with -ffp-contract=off: no fused multiply-add, no reassociation).
+ * below (compile with -ffp-contract=off: no implicit fused multiply-add, no reassociation;
+ * the explicit fmaf() calls are the specification's).
  * GEOMETRY (vertex positions, ellipse parameters, triangle coordinates) is then
  * recomputed in binary64 for the topology so decided.  DESIGN.md "Readings" lists
  * every place where the paper is silent or garbled and the reading taken here.

@@ -3,7 +3,8 @@
     python -m paper_2405_15197_b200.build        # or __graft_entry__.build()
 
 metamesh.cu is compiled with -fmad=false: its binary32 topology decisions follow the
-fixed-order specification of DESIGN.md Sec. 4 (no contracted multiply-adds).
+fixed-order specification of DESIGN.md Sec. 4 (no implicitly contracted multiply-adds; the
+specification's own FMAs are written explicitly).
 """
 from __future__ import annotations
 
