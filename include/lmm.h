@@ -149,8 +149,14 @@ enum {
   LMM_BUF_HOLE_M = 11,      /* int32 [H]: triangles per hole (global hole order)      */
   LMM_BUF_HOLE_OFF = 12,    /* int64 [H+1] triangle offsets of the holes (after bands)*/
   LMM_BUF_HOLE_BP = 13,     /* float32x4 [H]: fan centre b_project (node-local), node */
-  LMM_BUF_NODE_HOLE0 = 14,  /* int32 [N+1]: global index of each node's first hole     */
-  LMM_BUF_COUNT = 15
+  LMM_BUF_NODE_HOLE0 = 14,  /* int64 [N+1]: global index of each node's first hole     */
+  LMM_BUF_SLAB_KEY = 15,    /* int32x2 [N]: slab key (off, n) of each node: its slabs   */
+                            /*   start at K off + K0 n (K, K0 per slab above); nodes of */
+                            /*   the spill kernel have virtual keys (>= (2S, N)) into   */
+                            /*   the overflow reserve behind the regular slots          */
+  LMM_BUF_VMASK_HI = 16,    /* uint32 [2 ovf_off + 2 ovf_n]: tie-mask bits 32..63 of the */
+                            /*   overflow vertex slots (slab index - (4S + 2N))          */
+  LMM_BUF_COUNT = 17
 };
 LMM_API int lmm_buffer_size(lmm_ctx *ctx, int id, int64_t *bytes);
 LMM_API int lmm_copy_buffer(lmm_ctx *ctx, int id, int64_t offset, int64_t bytes, void *dst);

@@ -18,10 +18,23 @@
  * binary32 -- the paper's precision (Sec. 4.2.1: "each parameter occupies
  * a 4-byte floating-point number in GPU") -- with the operation order written
  * below (compile with -ffp-contract=off: no implicit fused multiply-add, no reassociation;
- * the explicit fmaf() calls are the specification's).
+ * the explicit FMA() calls are the specification's, DESIGN.md Sec. 4 and reading R11).
  * GEOMETRY (vertex positions, ellipse parameters, triangle coordinates) is then
  * recomputed in binary64 for the topology so decided.  DESIGN.md "Readings" lists
  * every place where the paper is silent or garbled and the reading taken here.
+ *
+ * Built twice from this one source:
+ *   liborc.so    -- the oracle: decisions in binary32 (real = float, atan2p polynomial);
+ *   liborc64.so  -- -DORC_REAL64: the SAME algorithm with every decision in binary64
+ *                   (real = double, libm atan2), optionally with a seeded relative jitter
+ *                   of the side parameters.  It pins the binary32 decision specification:
+ *                   tests/test_oracle_pins.py requires identical topology on every node
+ *                   whose binary64 topology is stable under the jitter.
+ *
+ * Storage.  No capacity of the GPU kernels appears here: junctions, vertex clusters,
+ * arcs and conic vertices are held in growable heap arrays.  The one limit is the tie
+ * mask of a vertex, one 64-bit word over the sides (sphere + up to 63 struts): a node of
+ * degree > 63 is ORC_E_DEGREE (reading R13).
  *
  * Model.  At a node with centre o and sphere radius R, each
  * incident strut k is a cone (cylinder when radii agree) tangent to the nodal
@@ -46,17 +59,33 @@
 #define M_PI 3.14159265358979323846
 #endif
 
-#define ORC_MAXD 31          /* struts per node (sides 1..31, side 0 = sphere)   */
-#define ORC_MAXJ 512         /* valid junctions per node (storage)                */
-#define ORC_MAXC 256         /* vertex clusters per node                          */
-#define ORC_MAXA 512         /* arcs per node                                     */
-#define ORC_MAXQ 64          /* clusters on one conic                             */
+#define ORC_MAXD 63          /* struts per node: sides 0..63 in one 64-bit tie mask */
 
-#define TOL_REL 1e-4f        /* delta   = TOL_REL * R : tie tolerance              */
-#define CTOL_REL 1e-3f       /* delta_c = CTOL_REL * R : vertex clustering radius  */
+#ifdef ORC_REAL64
+typedef double real;
+#define FMA fma
+#define SQRT sqrt
+#define FABS fabs
+#define FLOOR floor
+#define ATAN2P(y, x) atan2((y), (x))
+#else
+typedef float real;
+#define FMA fmaf
+#define SQRT sqrtf
+#define FABS fabsf
+#define FLOOR floorf
+#define ATAN2P(y, x) orc_atan2p((y), (x))
+#endif
+typedef uint64_t smask;      /* bit k = side k */
+#define BIT(k) ((smask)1 << (k))
+
+#define TOL_REL ((real)1e-4f)    /* delta   = TOL_REL * R : tie tolerance              */
+#define CTOL_REL ((real)1e-3f)   /* delta_c = CTOL_REL * R : vertex clustering radius  */
+#define PI_R ((real)3.14159265358979324f)
+#define TWO_PI_R ((real)6.28318530717958648f)
+#define HALF_PI_F 1.57079632679489662f
 #define PI_F 3.14159265358979324f
 #define TWO_PI_F 6.28318530717958648f
-#define HALF_PI_F 1.57079632679489662f
 
 enum {
   ORC_OK = 0, ORC_E_DEGREE = 1, ORC_E_STRUT = 2, ORC_E_JCAP = 3, ORC_E_CCAP = 4,
@@ -64,25 +93,27 @@ enum {
   ORC_E_ANGLE = 9, ORC_E_EMPTY = 10, ORC_E_HOLE = 11, ORC_E_SHORT = 12,
   ORC_E_QCAP = 13
 };
+/* ORC_E_JCAP / CCAP / ACAP / QCAP are never produced (no storage capacities); the codes
+ * stay reserved so that the status numbering matches include/lmm.h. */
 
 /* ------------------------------------------------------------------------- */
-/* binary32 vector arithmetic, operation order fixed                          */
+/* decision arithmetic (binary32, or binary64 in liborc64), operation order fixed */
 /* ------------------------------------------------------------------------- */
-typedef struct { float x, y, z; } f3;
+typedef struct { real x, y, z; } f3;
 typedef struct { double x, y, z; } d3;
 
-static inline f3 F3(float x, float y, float z) { f3 r = {x, y, z}; return r; }
+static inline f3 F3(real x, real y, real z) { f3 r = {x, y, z}; return r; }
 static inline f3 f_sub(f3 a, f3 b) { return F3(a.x - b.x, a.y - b.y, a.z - b.z); }
 static inline f3 f_add(f3 a, f3 b) { return F3(a.x + b.x, a.y + b.y, a.z + b.z); }
-static inline f3 f_scl(f3 a, float s) { return F3(a.x * s, a.y * s, a.z * s); }
-static inline f3 f_div(f3 a, float s) { return F3(a.x / s, a.y / s, a.z / s); }
+static inline f3 f_scl(f3 a, real s) { return F3(a.x * s, a.y * s, a.z * s); }
+static inline f3 f_div(f3 a, real s) { return F3(a.x / s, a.y / s, a.z / s); }
 /* dot and cross products with explicit fused multiply-adds (C99 fmaf, one
  * rounding each): dot = fma(a.z, b.z, fma(a.y, b.y, a.x b.x)), cross.x = fma(a.y, b.z, -(a.z b.y)) */
-static inline float f_dot(f3 a, f3 b) { return fmaf(a.z, b.z, fmaf(a.y, b.y, a.x * b.x)); }
+static inline real f_dot(f3 a, f3 b) { return FMA(a.z, b.z, FMA(a.y, b.y, a.x * b.x)); }
 static inline f3 f_cross(f3 a, f3 b) {
-  return F3(fmaf(a.y, b.z, -(a.z * b.y)), fmaf(a.z, b.x, -(a.x * b.z)), fmaf(a.x, b.y, -(a.y * b.x)));
+  return F3(FMA(a.y, b.z, -(a.z * b.y)), FMA(a.z, b.x, -(a.x * b.z)), FMA(a.x, b.y, -(a.y * b.x)));
 }
-static inline f3 f_nrm(f3 a) { return f_div(a, sqrtf(f_dot(a, a))); }
+static inline f3 f_nrm(f3 a) { return f_div(a, SQRT(f_dot(a, a))); }
 
 static inline d3 D3(double x, double y, double z) { d3 r = {x, y, z}; return r; }
 static inline d3 d_sub(d3 a, d3 b) { return D3(a.x - b.x, a.y - b.y, a.z - b.z); }
@@ -99,7 +130,8 @@ static inline d3 d_of(f3 a) { return D3(a.x, a.y, a.z); }
 /* Four-quadrant arc tangent in binary32 using only + - * / (so that both the
  * oracle and the kernel evaluate it bit-identically).  Cephes-style reduction
  * to [-tan(pi/8), tan(pi/8)] and its degree-9 odd polynomial; |err| ~ 1e-7 rad
- * (pinned against libm atan2 in tests/test_oracle_pins.py). */
+ * (pinned against libm atan2 in tests/test_oracle_pins.py).  The binary64 build
+ * decides with libm atan2 instead. */
 float orc_atan2p(float y, float x) {
   float ax = fabsf(x), ay = fabsf(y);
   float mx = ax > ay ? ax : ay;
@@ -117,28 +149,40 @@ float orc_atan2p(float y, float x) {
   return a;
 }
 
+/* growable heap array: ensure room for n+1 elements of size sz */
+static int grow(void **p, int *cap, int n, size_t sz) {
+  if (n < *cap) return 1;
+  int nc = *cap ? 2 * *cap : 64;
+  while (nc <= n) nc *= 2;
+  void *q = realloc(*p, sz * (size_t)nc);
+  if (!q) return 0;
+  *p = q;
+  *cap = nc;
+  return 1;
+}
+
 /* ------------------------------------------------------------------------- */
 /* lattice + CSR                                                              */
 /* ------------------------------------------------------------------------- */
 typedef struct {
   int32_t lo, hi, vs, ve;     /* sides (lo<hi, 0 = sphere), start/end vertex      */
-  float t0, dt;               /* binary32 parameter range on the conic (t0, t0+dt) */
-  float tmid;                 /* binary32 tangent length at the interval midpoint      */
-  f3 o, a, b;                 /* binary32 conic v(t) = a sin t + b cos t + o     */
+  real t0, dt;                /* decision parameter range on the conic (t0, t0+dt) */
+  real tmid;                  /* tangent length at the interval midpoint           */
+  f3 o, a, b;                 /* decision conic v(t) = a sin t + b cos t + o      */
   d3 o64, a64, b64;           /* binary64 conic                                  */
   double t064, dt64;          /* binary64 parameter range                        */
 } arc_t;
 
 typedef struct {
-  uint32_t mask;              /* sides tied at this vertex (bit k = side k)       */
+  smask mask;                 /* sides tied at this vertex (bit k = side k)       */
   int32_t kind;               /* 0: junction cluster, 1: seam of a closed arc     */
   int32_t ja, jb, jc, jr;     /* representative triple and root (kind 0)          */
   int32_t seam_arc;           /* arc owning the seam (kind 1)                     */
-  f3 y;                       /* binary32 position, node-local                    */
+  f3 y;                       /* decision position, node-local                    */
   d3 y64;                     /* binary64 position, node-local                    */
 } vert_t;
 
-typedef struct { int32_t arc, fwd; float phs, dph; } loop_t;
+typedef struct { int32_t arc, fwd; real phs, dph; } loop_t;
 typedef struct { int32_t arc, fwd; } hole_t;
 
 typedef struct {
@@ -160,7 +204,7 @@ typedef struct orc_lat {
   int64_t *csr_strut;         /* [2S] incident struts, ascending per node */
   node_mm *mm;                /* [n_nodes] */
   /* triangulation */
-  double ce; float th0;
+  double ce; real th0;
   int64_t *band_n;            /* [S][3]: nA, nB, kB (rotation) */
   int64_t *strut_tri_off;     /* [S+1] */
   int64_t *hole_base;         /* [n_nodes+1] global hole index of node's first hole */
@@ -169,6 +213,9 @@ typedef struct orc_lat {
   d3 *hole_bp;                /* [n_holes] projected centre, node-local */
   int64_t n_tri;
   int32_t tri_ready;
+  /* binary64 build only: relative jitter of the side parameters (0 = none) */
+  double jitter;
+  uint64_t jitter_seed;
 } orc_lat;
 
 static void node_free(node_mm *m) {
@@ -180,9 +227,9 @@ orc_lat *orc_create(const float *xyz, const float *rad, int64_t n_nodes,
                     const int64_t *ends, int64_t n_struts) {
   orc_lat *L = (orc_lat *)calloc(1, sizeof(orc_lat));
   L->n_nodes = n_nodes; L->n_struts = n_struts;
-  L->xyz = (float *)malloc(sizeof(float) * 3 * (size_t)n_nodes);
-  L->rad = (float *)malloc(sizeof(float) * (size_t)n_nodes);
-  L->ends = (int64_t *)malloc(sizeof(int64_t) * 2 * (size_t)n_struts);
+  L->xyz = (float *)malloc(sizeof(float) * 3 * (size_t)n_nodes + 4);
+  L->rad = (float *)malloc(sizeof(float) * (size_t)n_nodes + 4);
+  L->ends = (int64_t *)malloc(sizeof(int64_t) * 2 * (size_t)n_struts + 8);
   memcpy(L->xyz, xyz, sizeof(float) * 3 * (size_t)n_nodes);
   memcpy(L->rad, rad, sizeof(float) * (size_t)n_nodes);
   memcpy(L->ends, ends, sizeof(int64_t) * 2 * (size_t)n_struts);
@@ -192,14 +239,14 @@ orc_lat *orc_create(const float *xyz, const float *rad, int64_t n_nodes,
   for (int64_t s = 0; s < n_struts; s++) { L->csr_off[ends[2 * s] + 1]++; L->csr_off[ends[2 * s + 1] + 1]++; }
   for (int64_t n = 0; n < n_nodes; n++) L->csr_off[n + 1] += L->csr_off[n];
   L->csr_strut = (int64_t *)malloc(sizeof(int64_t) * 2 * (size_t)n_struts + 8);
-  int64_t *fill = (int64_t *)calloc((size_t)n_nodes, sizeof(int64_t));
+  int64_t *fill = (int64_t *)calloc((size_t)n_nodes + 1, sizeof(int64_t));
   for (int64_t s = 0; s < n_struts; s++)
     for (int e = 0; e < 2; e++) {
       int64_t n = ends[2 * s + e];
       L->csr_strut[L->csr_off[n] + fill[n]++] = s;
     }
   free(fill);
-  L->mm = (node_mm *)calloc((size_t)n_nodes, sizeof(node_mm));
+  L->mm = (node_mm *)calloc((size_t)n_nodes + 1, sizeof(node_mm));
   return L;
 }
 
@@ -212,6 +259,22 @@ void orc_destroy(orc_lat *L) {
   free(L);
 }
 
+/* binary64 build: seeded relative jitter of every side parameter (w, e, u, s), eps = 0 off */
+void orc_set_jitter(orc_lat *L, double eps, uint64_t seed) { L->jitter = eps; L->jitter_seed = seed; }
+
+#ifdef ORC_REAL64
+static double jit(const orc_lat *L, int64_t n, int k, int comp) {
+  /* splitmix64 of (seed, node, side, component) -> uniform in [-1, 1) */
+  uint64_t z = L->jitter_seed * 0x9E3779B97F4A7C15ull + (uint64_t)n * 0xBF58476D1CE4E5B9ull +
+               (uint64_t)(k * 16 + comp) * 0x94D049BB133111EBull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  z ^= z >> 31;
+  return (double)(z >> 11) * (2.0 / 9007199254740992.0) - 1.0;
+}
+
+#endif
+
 static inline f3 node_pos(const orc_lat *L, int64_t n) {
   return F3(L->xyz[3 * n], L->xyz[3 * n + 1], L->xyz[3 * n + 2]);
 }
@@ -220,8 +283,8 @@ static inline f3 node_pos(const orc_lat *L, int64_t n) {
 /* sides of a node                                                            */
 /* ------------------------------------------------------------------------- */
 typedef struct {
-  f3 w; float e;        /* h(y) = w.y - e                                   */
-  f3 u; float s, c, L;  /* direction, sin/cos of cone half-angle, length     */
+  f3 w; real e;         /* h(y) = w.y - e                                   */
+  f3 u; real s, c, L;   /* direction, sin/cos of cone half-angle, length     */
   f3 as, e1, e2;        /* strut canonical frame (axis i0->i1)              */
   int64_t strut; int sign;
 } side32;
@@ -234,7 +297,7 @@ typedef struct { d3 w; double e; d3 u; double s, c, L; d3 as, e1, e2; } side64;
 static void strut_frame32(const orc_lat *L, int64_t s, f3 *as, f3 *e1, f3 *e2) {
   f3 D = f_sub(node_pos(L, L->ends[2 * s + 1]), node_pos(L, L->ends[2 * s]));
   *as = f_nrm(D);
-  float ax = fabsf(as->x), ay = fabsf(as->y), az = fabsf(as->z);
+  real ax = FABS(as->x), ay = FABS(as->y), az = FABS(as->z);
   f3 ref = (ax <= ay && ax <= az) ? F3(1, 0, 0) : (ay <= az ? F3(0, 1, 0) : F3(0, 0, 1));
   *e1 = f_nrm(f_cross(*as, ref));
   *e2 = f_cross(*as, *e1);
@@ -242,10 +305,10 @@ static void strut_frame32(const orc_lat *L, int64_t s, f3 *as, f3 *e1, f3 *e2) {
 
 static void strut_frame64(const orc_lat *L, int64_t s, d3 *as, d3 *e1, d3 *e2) {
   f3 as32, e132, e232;
-  strut_frame32(L, s, &as32, &e132, &e232);   /* reference axis choice as in binary32 */
+  strut_frame32(L, s, &as32, &e132, &e232);   /* reference axis choice as decided */
   d3 D = d_sub(d_of(node_pos(L, L->ends[2 * s + 1])), d_of(node_pos(L, L->ends[2 * s])));
   *as = d_nrm(D);
-  float ax = fabsf(as32.x), ay = fabsf(as32.y), az = fabsf(as32.z);
+  real ax = FABS(as32.x), ay = FABS(as32.y), az = FABS(as32.z);
   d3 ref = (ax <= ay && ax <= az) ? D3(1, 0, 0) : (ay <= az ? D3(0, 1, 0) : D3(0, 0, 1));
   *e1 = d_nrm(d_cross(*as, ref));
   *e2 = d_cross(*as, *e1);
@@ -259,25 +322,34 @@ static int build_sides32(const orc_lat *L, int64_t n, side32 *S, int *d_out) {
   *d_out = (int)d;
   if (d > ORC_MAXD) return ORC_E_DEGREE;
   f3 o = node_pos(L, n);
-  float R = L->rad[n];
+  real R = L->rad[n];
   memset(&S[0], 0, sizeof(side32));
   for (int k = 1; k <= d; k++) {
     int64_t s = L->csr_strut[b + k - 1];
     int64_t far = L->ends[2 * s] == n ? L->ends[2 * s + 1] : L->ends[2 * s];
     side32 *q = &S[k];
     f3 D = f_sub(node_pos(L, far), o);
-    float Ln = sqrtf(f_dot(D, D));
-    if (!(Ln > 0.0f)) return ORC_E_STRUT;
+    real Ln = SQRT(f_dot(D, D));
+    if (!(Ln > 0)) return ORC_E_STRUT;
     q->u = f_div(D, Ln);
-    q->s = (R - L->rad[far]) / Ln;
-    if (!(fabsf(q->s) < 0.9f)) return ORC_E_STRUT;
-    q->c = sqrtf(1.0f - q->s * q->s);
+    q->s = (R - (real)L->rad[far]) / Ln;
+    if (!(FABS(q->s) < (real)0.9f)) return ORC_E_STRUT;
+    q->c = SQRT(1 - q->s * q->s);
     q->w = f_div(q->u, q->c);
     q->e = (R * q->s) / q->c;
     q->L = Ln;
     q->strut = s;
     q->sign = (L->ends[2 * s] == n) ? 1 : -1;
     strut_frame32(L, s, &q->as, &q->e1, &q->e2);
+#ifdef ORC_REAL64
+    if (L->jitter != 0.0) {
+      const double j = L->jitter;
+      q->w.x *= 1 + j * jit(L, n, k, 0); q->w.y *= 1 + j * jit(L, n, k, 1); q->w.z *= 1 + j * jit(L, n, k, 2);
+      q->e += j * R * jit(L, n, k, 3);
+      q->u.x *= 1 + j * jit(L, n, k, 4); q->u.y *= 1 + j * jit(L, n, k, 5); q->u.z *= 1 + j * jit(L, n, k, 6);
+      q->s += j * jit(L, n, k, 7);
+    }
+#endif
   }
   return ORC_OK;
 }
@@ -304,7 +376,7 @@ static void build_sides64(const orc_lat *L, int64_t n, side64 *S) {
 }
 
 /* side function h_k(y) = w_k . y - e_k, the dot product as in Sec. 4.1 */
-static inline float h32(const side32 *S, int k, f3 y) { return k == 0 ? 0.0f : f_dot(S[k].w, y) - S[k].e; }
+static inline real h32(const side32 *S, int k, f3 y) { return k == 0 ? 0 : f_dot(S[k].w, y) - S[k].e; }
 
 /* ------------------------------------------------------------------------- */
 /* triple junctions: points where h_a = h_b = h_c = sqrt(|y|^2 - R^2)         */
@@ -312,36 +384,36 @@ static inline float h32(const side32 *S, int k, f3 y) { return k == 0 ? 0.0f : f
 /* The line {h_a = h_b = h_c} is y = y0 + lam*mh (two plane equations
  * n1.y = q1, n2.y = q2 with n1 = w_a - w_b, n2 = w_a - w_c); substituting into
  * |y|^2 - R^2 = tau^2, tau = h_a(y), gives A lam^2 + 2 B' lam + C = 0. */
-static int junction32(const side32 *S, float R, int a, int b, int c, f3 *y, float *tau) {
+static int junction32(const side32 *S, real R, int a, int b, int c, f3 *y, real *tau) {
   f3 Wa = S[a].w, Wb = S[b].w, Wc = S[c].w;
-  float Ea = S[a].e, Eb = S[b].e, Ec = S[c].e;
-  if (a == 0) { Wa = F3(0, 0, 0); Ea = 0.0f; }
+  real Ea = S[a].e, Eb = S[b].e, Ec = S[c].e;
+  if (a == 0) { Wa = F3(0, 0, 0); Ea = 0; }
   f3 n1 = f_sub(Wa, Wb), n2 = f_sub(Wa, Wc);
-  float q1 = Ea - Eb, q2 = Ea - Ec;
+  real q1 = Ea - Eb, q2 = Ea - Ec;
   f3 m = f_cross(n1, n2);
-  float mm = f_dot(m, m);
-  float nn1 = f_dot(n1, n1), nn2 = f_dot(n2, n2);
-  if (!(mm > (1e-8f * nn1) * nn2)) return 0;
+  real mm = f_dot(m, m);
+  real nn1 = f_dot(n1, n1), nn2 = f_dot(n2, n2);
+  if (!(mm > ((real)1e-8f * nn1) * nn2)) return 0;
   f3 c1 = f_cross(n2, m), c2 = f_cross(m, n1);
-  float imm = 1.0f / mm;
+  real imm = 1 / mm;
   /* the fused multiply-adds of the junction solve */
-  f3 y0 = F3(fmaf(q2, c2.x, q1 * c1.x) * imm, fmaf(q2, c2.y, q1 * c1.y) * imm, fmaf(q2, c2.z, q1 * c1.z) * imm);
-  float iml = 1.0f / sqrtf(mm);
+  f3 y0 = F3(FMA(q2, c2.x, q1 * c1.x) * imm, FMA(q2, c2.y, q1 * c1.y) * imm, FMA(q2, c2.z, q1 * c1.z) * imm);
+  real iml = 1 / SQRT(mm);
   f3 mh = f_scl(m, iml);
-  float tau0 = f_dot(Wa, y0) - Ea;
-  float tau1 = f_dot(Wa, mh);
-  float A = fmaf(-tau1, tau1, 1.0f);
-  if (!(A > 1e-6f)) return 0;
-  float Bp = fmaf(-tau0, tau1, f_dot(y0, mh));
-  float C = fmaf(-tau0, tau0, fmaf(-R, R, f_dot(y0, y0)));
-  float disc = fmaf(Bp, Bp, -(A * C));
-  if (disc < 0.0f) return 0;
-  float sq = sqrtf(disc);
-  float iA = 1.0f / A;
-  float lam[2] = {(-Bp - sq) * iA, (-Bp + sq) * iA};
+  real tau0 = f_dot(Wa, y0) - Ea;
+  real tau1 = f_dot(Wa, mh);
+  real A = FMA(-tau1, tau1, (real)1);
+  if (!(A > (real)1e-6f)) return 0;
+  real Bp = FMA(-tau0, tau1, f_dot(y0, mh));
+  real C = FMA(-tau0, tau0, FMA(-R, R, f_dot(y0, y0)));
+  real disc = FMA(Bp, Bp, -(A * C));
+  if (disc < 0) return 0;
+  real sq = SQRT(disc);
+  real iA = 1 / A;
+  real lam[2] = {(-Bp - sq) * iA, (-Bp + sq) * iA};
   for (int r = 0; r < 2; r++) {
-    y[r] = F3(fmaf(mh.x, lam[r], y0.x), fmaf(mh.y, lam[r], y0.y), fmaf(mh.z, lam[r], y0.z));
-    tau[r] = fmaf(lam[r], tau1, tau0);
+    y[r] = F3(FMA(mh.x, lam[r], y0.x), FMA(mh.y, lam[r], y0.y), FMA(mh.z, lam[r], y0.z));
+    tau[r] = FMA(lam[r], tau1, tau0);
   }
   return 2;
 }
@@ -374,36 +446,36 @@ static void junction64(const side64 *S, double R, int a, int b, int c, int root,
  * coordinates v_i^0 = 0, d = -u_a (from v^1 towards v^0), r_i^0 = R,
  * Rot(d', alpha) d = cos(alpha) d + sin(alpha) (d' x d) with alpha = -beta.
  * Returns 0 when the section is not a bounded ellipse. */
-static int ellipse32(const side32 *S, float R, int a, int b, f3 *o, f3 *av, f3 *bv) {
+static int ellipse32(const side32 *S, real R, int a, int b, f3 *o, f3 *av, f3 *bv) {
   const side32 *A = &S[a];
   f3 N = f_sub(A->w, S[b].w);
-  float inl = 1.0f / sqrtf(f_dot(N, N));
+  real inl = 1 / SQRT(f_dot(N, N));
   f3 n = f_scl(N, inl);
-  float pc = (A->e - S[b].e) * inl;
+  real pc = (A->e - S[b].e) * inl;
   f3 p = f_scl(n, pc);
-  float s = A->s, c = A->c;
-  if (!(fabsf(f_dot(n, A->u)) > fabsf(s) + 1e-3f)) return 0;
+  real s = A->s, c = A->c;
+  if (!(FABS(f_dot(n, A->u)) > FABS(s) + (real)1e-3f)) return 0;
   f3 d = F3(-A->u.x, -A->u.y, -A->u.z);
   f3 dp = f_cross(d, n);
-  float dpl2 = f_dot(dp, dp);
+  real dpl2 = f_dot(dp, dp);
   f3 r_;
-  if (dpl2 > 1e-12f) { dp = f_scl(dp, 1.0f / sqrtf(dpl2)); r_ = f_cross(dp, d); }
+  if (dpl2 > (real)1e-12f) { dp = f_scl(dp, 1 / SQRT(dpl2)); r_ = f_cross(dp, d); }
   else r_ = A->e1;
   f3 g1 = F3(c * d.x - s * r_.x, c * d.y - s * r_.y, c * d.z - s * r_.z);
   f3 g2 = F3(c * d.x + s * r_.x, c * d.y + s * r_.y, c * d.z + s * r_.z);
   f3 F1 = F3(R * ((-s) * d.x - c * r_.x), R * ((-s) * d.y - c * r_.y), R * ((-s) * d.z - c * r_.z));
   f3 F2 = F3(R * ((-s) * d.x + c * r_.x), R * ((-s) * d.y + c * r_.y), R * ((-s) * d.z + c * r_.z));
-  float k1 = f_dot(n, f_sub(p, F1)) / f_dot(n, g1);
-  float k2 = f_dot(n, f_sub(p, F2)) / f_dot(n, g2);
+  real k1 = f_dot(n, f_sub(p, F1)) / f_dot(n, g1);
+  real k2 = f_dot(n, f_sub(p, F2)) / f_dot(n, g2);
   f3 E1 = f_add(F1, f_scl(g1, k1)), E2 = f_add(F2, f_scl(g2, k2));
-  *o = f_scl(f_add(E1, E2), 0.5f);
-  *av = f_scl(f_sub(E1, E2), 0.5f);
-  float ad = f_dot(*av, d), aa = f_dot(*av, *av);
-  float arg = 1.0f - (ad * ad) / ((c * c) * aa);
-  if (arg < 0.0f) arg = 0.0f;
-  float lam = sqrtf(arg);
+  *o = f_scl(f_add(E1, E2), (real)0.5f);
+  *av = f_scl(f_sub(E1, E2), (real)0.5f);
+  real ad = f_dot(*av, d), aa = f_dot(*av, *av);
+  real arg = 1 - (ad * ad) / ((c * c) * aa);
+  if (arg < 0) arg = 0;
+  real lam = SQRT(arg);
   *bv = f_scl(f_cross(*av, n), lam);
-  if (!(f_dot(*bv, *bv) > 1e-12f * aa)) return 0;
+  if (!(f_dot(*bv, *bv) > (real)1e-12f * aa)) return 0;
   return 1;
 }
 
@@ -418,12 +490,12 @@ static void ellipse64(const side64 *S, const side32 *S32, double R, int a, int b
   d3 dp = d_cross(d, n);
   double dpl2 = d_dot(dp, dp);
   d3 r_;
-  /* degenerate-branch choice follows the binary32 decision */
+  /* degenerate-branch choice follows the decision arithmetic */
   f3 d32 = F3(-S32[a].u.x, -S32[a].u.y, -S32[a].u.z);
   f3 N32 = f_sub(S32[a].w, S32[b].w);
-  f3 n32 = f_scl(N32, 1.0f / sqrtf(f_dot(N32, N32)));
+  f3 n32 = f_scl(N32, 1 / SQRT(f_dot(N32, N32)));
   f3 dp32 = f_cross(d32, n32);
-  if (f_dot(dp32, dp32) > 1e-12f) { dp = d_div(dp, sqrt(dpl2)); r_ = d_cross(dp, d); }
+  if (f_dot(dp32, dp32) > (real)1e-12f) { dp = d_div(dp, sqrt(dpl2)); r_ = d_cross(dp, d); }
   else r_ = A->e1;
   d3 g1 = d_sub(d_scl(d, c), d_scl(r_, s)), g2 = d_add(d_scl(d, c), d_scl(r_, s));
   d3 F1 = d_scl(d_sub(d_scl(d, -s), d_scl(r_, c)), R);
@@ -442,8 +514,8 @@ static void ellipse64(const side64 *S, const side32 *S32, double R, int a, int b
  * sphere (Sec. 5 "the circle edge of the strut's end section"), read as
  * the tangency circle: centre R sin(beta) u, radius R cos(beta).  Parametrised by
  * the strut frame so that t is the angle around the strut axis. */
-static void circle32(const side32 *S, float R, int b, f3 *o, f3 *av, f3 *bv) {
-  float rs = R * S[b].s, rr = R * S[b].c;
+static void circle32(const side32 *S, real R, int b, f3 *o, f3 *av, f3 *bv) {
+  real rs = R * S[b].s, rr = R * S[b].c;
   *o = f_scl(S[b].u, rs);
   *av = f_scl(S[b].e2, rr);
   *bv = f_scl(S[b].e1, rr);
@@ -455,13 +527,13 @@ static void circle64(const side64 *S, double R, int b, d3 *o, d3 *av, d3 *bv) {
 }
 
 /* parameter t of point P on conic (o,a,b): sin t = Q.a/|a|^2, cos t = Q.b/|b|^2 */
-static float conic_t32(f3 o, f3 av, f3 bv, f3 P, float *us, float *uc) {
+static real conic_t32(f3 o, f3 av, f3 bv, f3 P, real *us, real *uc) {
   f3 Q = f_sub(P, o);
-  float st = f_dot(Q, av) / f_dot(av, av);
-  float ct = f_dot(Q, bv) / f_dot(bv, bv);
-  float il = 1.0f / sqrtf(st * st + ct * ct);
+  real st = f_dot(Q, av) / f_dot(av, av);
+  real ct = f_dot(Q, bv) / f_dot(bv, bv);
+  real il = 1 / SQRT(st * st + ct * ct);
   *us = st * il; *uc = ct * il;
-  return orc_atan2p(st, ct);
+  return ATAN2P(st, ct);
 }
 static double conic_t64(d3 o, d3 av, d3 bv, d3 P) {
   d3 Q = d_sub(P, o);
@@ -469,14 +541,14 @@ static double conic_t64(d3 o, d3 av, d3 bv, d3 P) {
 }
 
 /* ------------------------------------------------------------------------- */
-/* validity tests (binary32)                                                  */
+/* validity tests                                                             */
 /* ------------------------------------------------------------------------- */
 /* junction of three struts: no other strut strictly above (tolerance delta),
  * and on the forward nappe (tau >= -delta, else the sphere is above). */
-static int valid_strut_pt(const side32 *S, int d, uint32_t excl, f3 y, float tau, float delta) {
+static int valid_strut_pt(const side32 *S, int d, smask excl, f3 y, real tau, real delta) {
   if (tau < -delta) return 0;
   for (int m = 1; m <= d; m++) {
-    if (excl & (1u << m)) continue;
+    if (excl & BIT(m)) continue;
     if (h32(S, m, y) - tau > delta) return 0;
   }
   return 1;
@@ -484,18 +556,18 @@ static int valid_strut_pt(const side32 *S, int d, uint32_t excl, f3 y, float tau
 /* sphere junction (sphere, b, c): no other strut above the sphere by more than delta
  * (tolerant, like strut junctions: near-coincident junctions then cluster into one
  * vertex of higher valence). */
-static int valid_sphere_junction(const side32 *S, int d, uint32_t excl, f3 y, float delta) {
+static int valid_sphere_junction(const side32 *S, int d, smask excl, f3 y, real delta) {
   for (int m = 1; m <= d; m++) {
-    if (excl & (1u << m)) continue;
+    if (excl & BIT(m)) continue;
     if (h32(S, m, y) > delta) return 0;
   }
   return 1;
 }
 /* a point of an end circle is exposed only if every other strut is below it by more
  * than delta: ties with the sphere go to the struts (zero-area holes vanish). */
-static int valid_sphere_pt(const side32 *S, int d, uint32_t excl, f3 y, float delta) {
+static int valid_sphere_pt(const side32 *S, int d, smask excl, f3 y, real delta) {
   for (int m = 1; m <= d; m++) {
-    if (excl & (1u << m)) continue;
+    if (excl & BIT(m)) continue;
     if (h32(S, m, y) > -delta) return 0;
   }
   return 1;
@@ -504,7 +576,21 @@ static int valid_sphere_pt(const side32 *S, int d, uint32_t excl, f3 y, float de
 /* ------------------------------------------------------------------------- */
 /* per-node meta-mesh                                                         */
 /* ------------------------------------------------------------------------- */
-typedef struct { int a, b, c, r; f3 y; float tau; } junc_t;
+typedef struct { int a, b, c, r; f3 y; real tau; } junc_t;
+
+/* scratch of one node (heap, grown on demand) */
+typedef struct {
+  junc_t *J; int capJ;
+  int *lab, *cid; int capL;
+  vert_t *V; int capV;
+  arc_t *A; int capA;
+  int *Q; real *tq, *us, *uc; int capQ;
+} work_t;
+
+static void work_free(work_t *w) {
+  free(w->J); free(w->lab); free(w->cid); free(w->V); free(w->A);
+  free(w->Q); free(w->tq); free(w->us); free(w->uc);
+}
 
 static int node_metamesh(orc_lat *L, int64_t n) {
   node_mm *M = &L->mm[n];
@@ -518,31 +604,31 @@ static int node_metamesh(orc_lat *L, int64_t n) {
   M->hole_off = (int32_t *)calloc(1, sizeof(int32_t));
   if (st != ORC_OK) { M->status = st; return st; }
   if (d == 0) return ORC_OK;
-  float R = L->rad[n];
-  float delta = TOL_REL * R, dc = CTOL_REL * R;
+  real R = L->rad[n];
+  real delta = TOL_REL * R, dc = CTOL_REL * R;
+  work_t W;
+  memset(&W, 0, sizeof W);
+#define FAIL(code) do { work_free(&W); M->status = (code); return M->status; } while (0)
 
-  /* 1. junctions of every triple a<b<c of sides {0..d}, lexicographic order.  A node with
-   * more valid junctions than the capacity of its degree class (reading R13:
-   * degree 1-4: 24, 5-8: 96, 9-12: 192, 13-16: 240, 17-23: 336, 24-31: 448) is flagged
-   * JCAP -- the fixed per-node workspace of the model. */
-  const int maxj = d <= 4 ? 24 : d <= 8 ? 96 : d <= 12 ? 192 : d <= 16 ? 240 : d <= 23 ? 336 : 448;
-  junc_t *J = (junc_t *)malloc(sizeof(junc_t) * ORC_MAXJ);
+  /* 1. junctions of every triple a<b<c of sides {0..d}, lexicographic order, root-minor */
   int nj = 0;
   for (int a = 0; a <= d; a++)
     for (int b = a + 1; b <= d; b++)
       for (int c = b + 1; c <= d; c++) {
-        f3 y[2]; float tau[2];
+        f3 y[2]; real tau[2];
         if (!junction32(S, R, a, b, c, y, tau)) continue;
-        uint32_t excl = (1u << a) | (1u << b) | (1u << c);
+        smask excl = BIT(a) | BIT(b) | BIT(c);
         for (int r = 0; r < 2; r++) {
           int ok = a == 0 ? valid_sphere_junction(S, d, excl, y[r], delta)
                           : valid_strut_pt(S, d, excl, y[r], tau[r], delta);
           if (!ok) continue;
-          if (nj >= maxj) { free(J); M->status = ORC_E_JCAP; return M->status; }
+          /* a vertex further along a strut than 0.45 of its length (x cos beta) lies where
+           * the neighbouring node's meta-mesh takes over: the strut is too short for the model */
           int ks[3] = {a, b, c};
           for (int q = 0; q < 3; q++)
-            if (ks[q] > 0 && tau[r] > 0.45f * (S[ks[q]].L * S[ks[q]].c)) { free(J); M->status = ORC_E_SHORT; return M->status; }
-          J[nj].a = a; J[nj].b = b; J[nj].c = c; J[nj].r = r; J[nj].y = y[r]; J[nj].tau = tau[r];
+            if (ks[q] > 0 && tau[r] > (real)0.45f * (S[ks[q]].L * S[ks[q]].c)) FAIL(ORC_E_SHORT);
+          if (!grow((void **)&W.J, &W.capJ, nj, sizeof(junc_t))) FAIL(ORC_E_JCAP);
+          W.J[nj].a = a; W.J[nj].b = b; W.J[nj].c = c; W.J[nj].r = r; W.J[nj].y = y[r]; W.J[nj].tau = tau[r];
           nj++;
         }
       }
@@ -550,118 +636,127 @@ static int node_metamesh(orc_lat *L, int64_t n) {
   /* 2. clustering: connected components of the graph "junctions within delta_c (max-norm)";
    *    a component is one vertex (of higher valence when several junctions coincide),
    *    positioned at and ordered by its lowest-index junction. */
-  vert_t *V = (vert_t *)calloc(ORC_MAXC + ORC_MAXA, sizeof(vert_t));
-  int *lab = (int *)malloc(sizeof(int) * (size_t)(nj + 1));
+  W.lab = (int *)malloc(sizeof(int) * (size_t)(nj + 1));
+  W.cid = (int *)malloc(sizeof(int) * (size_t)(nj + 1));
+  junc_t *J = W.J;
+  int *lab = W.lab;
   for (int j = 0; j < nj; j++) lab[j] = j;
   for (int changed = 1; changed;) {
     changed = 0;
     for (int j = 0; j < nj; j++)
       for (int k = 0; k < nj; k++)
-        if (lab[k] < lab[j] && fabsf(J[j].y.x - J[k].y.x) <= dc && fabsf(J[j].y.y - J[k].y.y) <= dc &&
-            fabsf(J[j].y.z - J[k].y.z) <= dc) { lab[j] = lab[k]; changed = 1; }
+        if (lab[k] < lab[j] && FABS(J[j].y.x - J[k].y.x) <= dc && FABS(J[j].y.y - J[k].y.y) <= dc &&
+            FABS(J[j].y.z - J[k].y.z) <= dc) { lab[j] = lab[k]; changed = 1; }
   }
   int nc = 0;
-  int *cid = (int *)malloc(sizeof(int) * (size_t)(nj + 1));
   for (int j = 0; j < nj; j++) {
     if (lab[j] == j) {
-      if (nc >= ORC_MAXC) { free(J); free(V); free(lab); free(cid); M->status = ORC_E_CCAP; return M->status; }
-      cid[j] = nc;
-      V[nc].kind = 0; V[nc].ja = J[j].a; V[nc].jb = J[j].b; V[nc].jc = J[j].c; V[nc].jr = J[j].r;
-      V[nc].y = J[j].y; V[nc].mask = 0; V[nc].seam_arc = -1;
+      if (!grow((void **)&W.V, &W.capV, nc, sizeof(vert_t))) FAIL(ORC_E_CCAP);
+      W.cid[j] = nc;
+      vert_t *V = &W.V[nc];
+      V->kind = 0; V->ja = J[j].a; V->jb = J[j].b; V->jc = J[j].c; V->jr = J[j].r;
+      V->y = J[j].y; V->mask = 0; V->seam_arc = -1;
       nc++;
     }
   }
   for (int j = 0; j < nj; j++) {
-    uint32_t bits = (1u << J[j].a) | (1u << J[j].b) | (1u << J[j].c);
+    smask bits = BIT(J[j].a) | BIT(J[j].b) | BIT(J[j].c);
     /* a strut junction at tangent length ~0 lies on the nodal sphere: it ties with side 0 */
-    if (fabsf(J[j].tau) <= delta) bits |= 1u;
-    V[cid[lab[j]]].mask |= bits;
+    if (FABS(J[j].tau) <= delta) bits |= 1;
+    W.V[W.cid[lab[j]]].mask |= bits;
   }
-  free(lab);
-  free(cid);
-  free(J);
   int nv = nc;
 
   /* 3. arcs: for every pair of sides, walk the conic through its vertices.  A conic
    * carrying no vertex can only be one closed arc, which is then the whole loop of its
    * strut side(s): it is tested only when its strut sides appear in no vertex. */
-  arc_t *A = (arc_t *)calloc(ORC_MAXA, sizeof(arc_t));
   int na = 0;
-  uint32_t in_vertex = 0;
-  for (int q = 0; q < nc; q++) in_vertex |= V[q].mask;
+  smask in_vertex = 0;
+  for (int q = 0; q < nc; q++) in_vertex |= W.V[q].mask;
   for (int a = 0; a <= d; a++)
     for (int b = a + 1; b <= d; b++) {
       f3 o, av, bv;
+      smask pm = BIT(a) | BIT(b);
       {
-        uint32_t pm0 = (1u << a) | (1u << b);
         int has = 0;
-        for (int q = 0; q < nc && !has; q++) has = (V[q].mask & pm0) == pm0;
-        uint32_t strut_bits = a == 0 ? (1u << b) : pm0;
+        for (int q = 0; q < nc && !has; q++) has = (W.V[q].mask & pm) == pm;
+        smask strut_bits = a == 0 ? BIT(b) : pm;
         if (!has && (in_vertex & strut_bits)) continue;
       }
       if (a == 0) circle32(S, R, b, &o, &av, &bv);
       else if (!ellipse32(S, R, a, b, &o, &av, &bv)) {
         /* a pair whose plane section is unbounded cannot carry an arc only if no
          * vertex lies on it; otherwise the node is outside the model */
-        uint32_t pm = (1u << a) | (1u << b);
         for (int q = 0; q < nc; q++)
-          if ((V[q].mask & pm) == pm) { free(V); free(A); M->status = ORC_E_CONIC; return M->status; }
+          if ((W.V[q].mask & pm) == pm) FAIL(ORC_E_CONIC);
         continue;
       }
-      uint32_t pm = (1u << a) | (1u << b);
-      int Q[ORC_MAXQ]; float tq[ORC_MAXQ], us[ORC_MAXQ], uc[ORC_MAXQ];
       int nq = 0;
       for (int q = 0; q < nc; q++)
-        if ((V[q].mask & pm) == pm) {
-          if (nq >= ORC_MAXQ) { free(V); free(A); M->status = ORC_E_QCAP; return M->status; }
-          Q[nq] = q;
-          tq[nq] = conic_t32(o, av, bv, V[q].y, &us[nq], &uc[nq]);
+        if ((W.V[q].mask & pm) == pm) {
+          if (nq >= W.capQ) {
+            int cap = W.capQ;
+            if (!grow((void **)&W.Q, &cap, nq, sizeof(int)) || !(W.tq = (real *)realloc(W.tq, sizeof(real) * (size_t)cap)) ||
+                !(W.us = (real *)realloc(W.us, sizeof(real) * (size_t)cap)) || !(W.uc = (real *)realloc(W.uc, sizeof(real) * (size_t)cap)))
+              FAIL(ORC_E_QCAP);
+            W.capQ = cap;
+          }
+          W.Q[nq] = q;
+          W.tq[nq] = conic_t32(o, av, bv, W.V[q].y, &W.us[nq], &W.uc[nq]);
           nq++;
         }
+      int *Q = W.Q;
+      real *tq = W.tq, *us = W.us, *uc = W.uc;
       /* insertion sort by (t, cluster index) */
       for (int i = 1; i < nq; i++)
         for (int j = i; j > 0 && (tq[j] < tq[j - 1] || (tq[j] == tq[j - 1] && Q[j] < Q[j - 1])); j--) {
           int ti = Q[j]; Q[j] = Q[j - 1]; Q[j - 1] = ti;
-          float tf = tq[j]; tq[j] = tq[j - 1]; tq[j - 1] = tf;
+          real tf = tq[j]; tq[j] = tq[j - 1]; tq[j - 1] = tf;
           tf = us[j]; us[j] = us[j - 1]; us[j - 1] = tf;
           tf = uc[j]; uc[j] = uc[j - 1]; uc[j - 1] = tf;
         }
       int nint = nq == 0 ? 1 : nq;
       for (int i = 0; i < nint; i++) {
-        float ms, mc, t0, dt;
+        real ms, mc, t0, dt;
         int vs, ve;
-        if (nq == 0) { ms = 0.0f; mc = 1.0f; t0 = 0.0f; dt = TWO_PI_F; vs = ve = -1; }
-        else if (nq == 1) { ms = -us[0]; mc = -uc[0]; t0 = tq[0]; dt = TWO_PI_F; vs = ve = Q[0]; }
+        if (nq == 0) { ms = 0; mc = 1; t0 = 0; dt = TWO_PI_R; vs = ve = -1; }
+        else if (nq == 1) { ms = -us[0]; mc = -uc[0]; t0 = tq[0]; dt = TWO_PI_R; vs = ve = Q[0]; }
         else {
           int j = (i + 1) % nq;
-          dt = j == 0 ? (tq[0] + TWO_PI_F) - tq[nq - 1] : tq[j] - tq[i];
-          if (!(dt > 0.0f)) { free(V); free(A); M->status = ORC_E_CHAIN; return M->status; }
-          float sx = us[i] + us[j], sc = uc[i] + uc[j];
-          float l2 = sx * sx + sc * sc;
-          if (l2 > 1e-6f) {
-            float l = sqrtf(l2);
+          dt = j == 0 ? (tq[0] + TWO_PI_R) - tq[nq - 1] : tq[j] - tq[i];
+          if (!(dt > 0)) FAIL(ORC_E_CHAIN);
+          real sx = us[i] + us[j], sc = uc[i] + uc[j];
+          real l2 = sx * sx + sc * sc;
+          if (l2 > (real)1e-6f) {
+            real l = SQRT(l2);
             ms = sx / l; mc = sc / l;
-            if (dt > PI_F) { ms = -ms; mc = -mc; }
+            if (dt > PI_R) { ms = -ms; mc = -mc; }
           } else { ms = uc[i]; mc = -us[i]; }
           t0 = tq[i]; vs = Q[i]; ve = Q[j];
         }
         f3 y = F3((o.x + av.x * ms) + bv.x * mc, (o.y + av.y * ms) + bv.y * mc, (o.z + av.z * ms) + bv.z * mc);
-        float tmid = a == 0 ? 0.0f : h32(S, a, y);
+        real tmid = a == 0 ? 0 : h32(S, a, y);
         int ok = a == 0 ? valid_sphere_pt(S, d, pm, y, delta)
                         : valid_strut_pt(S, d, pm, y, tmid, delta);
         if (!ok) continue;
-        if (na >= ORC_MAXA) { free(V); free(A); M->status = ORC_E_ACAP; return M->status; }
-        arc_t *E = &A[na];
+        if (!grow((void **)&W.A, &W.capA, na, sizeof(arc_t))) FAIL(ORC_E_ACAP);
+        arc_t *E = &W.A[na];
+        memset(E, 0, sizeof *E);
         E->lo = a; E->hi = b; E->t0 = t0; E->dt = dt; E->o = o; E->a = av; E->b = bv; E->tmid = tmid;
         if (vs < 0) {  /* closed conic without vertex: add its seam (t = 0) */
-          V[nv].kind = 1; V[nv].mask = pm; V[nv].seam_arc = na;
-          V[nv].y = F3(o.x + bv.x, o.y + bv.y, o.z + bv.z);
+          if (!grow((void **)&W.V, &W.capV, nv, sizeof(vert_t))) FAIL(ORC_E_CCAP);
+          vert_t *V = &W.V[nv];
+          memset(V, 0, sizeof *V);
+          V->kind = 1; V->mask = pm; V->seam_arc = na;
+          V->y = F3(o.x + bv.x, o.y + bv.y, o.z + bv.z);
           vs = ve = nv++;
         }
         E->vs = vs; E->ve = ve;
         na++;
       }
     }
+  vert_t *V = W.V;
+  arc_t *A = W.A;
 
   /* An AMBIGUOUS strut-strut arc (a,b) -- tangent length at its midpoint within the tie
    * tolerance of the sphere -- whose two end vertices are also joined by the end-circle
@@ -669,7 +764,7 @@ static int node_metamesh(orc_lat *L, int64_t n) {
    * arc is dropped (R10).  Seam references are renumbered. */
   {
     int w = 0;
-    int remap[ORC_MAXA];
+    int *remap = (int *)malloc(sizeof(int) * (size_t)(na + 1));
     for (int i = 0; i < na; i++) {
       int drop = 0;
       if (A[i].lo > 0 && A[i].vs != A[i].ve && A[i].tmid < delta) {
@@ -687,77 +782,84 @@ static int node_metamesh(orc_lat *L, int64_t n) {
       if (!drop) A[w++] = A[i];
     }
     for (int q = nc; q < nv; q++) V[q].seam_arc = remap[V[q].seam_arc];
+    free(remap);
     na = w;
   }
 
   if (getenv("ORC_DEBUG")) {
     for (int q = 0; q < nv; q++)
-      fprintf(stderr, "node %lld v%d mask %x y/R (%.5f %.5f %.5f)\n", (long long)n, q, V[q].mask, V[q].y.x / R, V[q].y.y / R, V[q].y.z / R);
+      fprintf(stderr, "node %lld v%d mask %llx y/R (%.5f %.5f %.5f)\n", (long long)n, q, (unsigned long long)V[q].mask,
+              (double)(V[q].y.x / R), (double)(V[q].y.y / R), (double)(V[q].y.z / R));
     for (int i = 0; i < na; i++)
-      fprintf(stderr, "node %lld arc%d (%d,%d) v%d->v%d t0=%.5f dt=%.5f\n", (long long)n, i, A[i].lo, A[i].hi, A[i].vs, A[i].ve, A[i].t0, A[i].dt);
+      fprintf(stderr, "node %lld arc%d (%d,%d) v%d->v%d t0=%.7f dt=%.7f\n", (long long)n, i, A[i].lo, A[i].hi, A[i].vs, A[i].ve,
+              (double)A[i].t0, (double)A[i].dt);
   }
   /* every junction vertex must carry arcs */
   for (int q = 0; q < nc; q++) {
     int used = 0;
     for (int i = 0; i < na && !used; i++) used = A[i].vs == q || A[i].ve == q;
-    if (!used) { free(V); free(A); M->status = ORC_E_UNREF; return M->status; }
+    if (!used) FAIL(ORC_E_UNREF);
   }
 
   /* 4. arc loops: one per strut end, ordered by angle around the strut axis
    *    (Sec. 4.1 "sequentially interconnected, forming an arc loop") */
   loop_t *LE = (loop_t *)malloc(sizeof(loop_t) * (size_t)(2 * na + 1));
+  real *key = (real *)malloc(sizeof(real) * (size_t)(na + 1));
+#undef FAIL
+#define FAIL(code) do { free(LE); free(key); work_free(&W); M->status = (code); return M->status; } while (0)
   int nle = 0;
   for (int k = 1; k <= d; k++) {
     M->loop_off[k - 1] = nle;
     int beg = nle;
     f3 as = S[k].as, e1 = S[k].e1, e2 = S[k].e2;
-    float key[ORC_MAXA];
     for (int i = 0; i < na; i++) {
       if (A[i].lo != k && A[i].hi != k) continue;
-      int fwd = f_dot(f_cross(A[i].a, A[i].b), as) < 0.0f;
+      int fwd = f_dot(f_cross(A[i].a, A[i].b), as) < 0;
       int vs = fwd ? A[i].vs : A[i].ve, ve = fwd ? A[i].ve : A[i].vs;
-      float ps = orc_atan2p(f_dot(V[vs].y, e2), f_dot(V[vs].y, e1));
-      if (ps < 0.0f) ps += TWO_PI_F;
-      float dph;
-      if (vs == ve) dph = TWO_PI_F;
+      real ps = ATAN2P(f_dot(V[vs].y, e2), f_dot(V[vs].y, e1));
+      if (ps < 0) ps += TWO_PI_R;
+      real dph;
+      if (vs == ve) dph = TWO_PI_R;
       else {
-        float pe = orc_atan2p(f_dot(V[ve].y, e2), f_dot(V[ve].y, e1));
-        if (pe < 0.0f) pe += TWO_PI_F;
+        real pe = ATAN2P(f_dot(V[ve].y, e2), f_dot(V[ve].y, e1));
+        if (pe < 0) pe += TWO_PI_R;
         dph = pe - ps;
-        if (dph <= 0.0f) dph += TWO_PI_F;
+        if (dph <= 0) dph += TWO_PI_R;
       }
       LE[nle].arc = i; LE[nle].fwd = fwd; LE[nle].phs = ps; LE[nle].dph = dph;
       key[nle - beg] = ps;
       nle++;
     }
     int cnt = nle - beg;
-    if (cnt == 0) { free(V); free(A); free(LE); M->status = ORC_E_EMPTY; return M->status; }
+    if (cnt == 0) FAIL(ORC_E_EMPTY);
     for (int i = 1; i < cnt; i++)
       for (int j = i; j > 0 && (key[j] < key[j - 1] || (key[j] == key[j - 1] && LE[beg + j].arc < LE[beg + j - 1].arc)); j--) {
         loop_t t = LE[beg + j]; LE[beg + j] = LE[beg + j - 1]; LE[beg + j - 1] = t;
-        float tf = key[j]; key[j] = key[j - 1]; key[j - 1] = tf;
+        real tf = key[j]; key[j] = key[j - 1]; key[j - 1] = tf;
       }
     if (getenv("ORC_DEBUG")) {
       fprintf(stderr, "node %lld strut side %d loop:", (long long)n, k);
       for (int i = 0; i < cnt; i++) {
         arc_t *E = &A[LE[beg + i].arc];
-        fprintf(stderr, " [arc%d (%d,%d) v%d->v%d fwd%d ps=%.5f dph=%.5f]", LE[beg + i].arc, E->lo, E->hi, E->vs, E->ve,
-                LE[beg + i].fwd, LE[beg + i].phs, LE[beg + i].dph);
+        fprintf(stderr, " [arc%d (%d,%d) v%d->v%d fwd%d ps=%.7f dph=%.7f]", LE[beg + i].arc, E->lo, E->hi, E->vs, E->ve,
+                LE[beg + i].fwd, (double)LE[beg + i].phs, (double)LE[beg + i].dph);
       }
       fprintf(stderr, "\n");
     }
-    float sum = 0.0f;
+    real sum = 0;
     for (int i = 0; i < cnt; i++) {
       loop_t *x = &LE[beg + i], *y = &LE[beg + (i + 1) % cnt];
       int xe = x->fwd ? A[x->arc].ve : A[x->arc].vs;
       int ys = y->fwd ? A[y->arc].vs : A[y->arc].ve;
-      if (xe != ys) { free(V); free(A); free(LE); M->status = ORC_E_CHAIN; return M->status; }
+      if (xe != ys) FAIL(ORC_E_CHAIN);
       sum += x->dph;
     }
-    if (fabsf(sum - TWO_PI_F) > 1e-3f) { free(V); free(A); free(LE); M->status = ORC_E_ANGLE; return M->status; }
+    if (FABS(sum - TWO_PI_R) > (real)1e-3f) FAIL(ORC_E_ANGLE);
     for (int i = 1; i < cnt; i++) LE[beg + i].phs = LE[beg + i - 1].phs + LE[beg + i - 1].dph;
   }
   M->loop_off[d] = nle;
+  free(key);
+  key = NULL;
 
   /* 5. holes: cap arcs chained around the exposed nodal sphere, traversed
    *    clockwise about each strut's outward direction (Sec. 5 holes) */
@@ -783,7 +885,7 @@ static int node_metamesh(orc_lat *L, int64_t n) {
         int hj = S[A[j].hi].sign < 0;
         if ((hj ? A[j].vs : A[j].ve) == endv) nxt = j;
       }
-      if (nxt < 0) { free(V); free(A); free(LE); free(HE); free(hoff); free(used); M->status = ORC_E_HOLE; return M->status; }
+      if (nxt < 0) { free(HE); free(hoff); free(used); FAIL(ORC_E_HOLE); }
       cur = nxt;
     }
   }
@@ -793,7 +895,7 @@ static int node_metamesh(orc_lat *L, int64_t n) {
   /* 6. binary64 geometry for the topology decided above */
   side64 S64[ORC_MAXD + 1];
   build_sides64(L, n, S64);
-  double R64 = R;
+  double R64 = L->rad[n];
   for (int i = 0; i < na; i++) {
     arc_t *E = &A[i];
     if (E->lo == 0) circle64(S64, R64, E->hi, &E->o64, &E->a64, &E->b64);
@@ -810,17 +912,20 @@ static int node_metamesh(orc_lat *L, int64_t n) {
     if (E->vs == E->ve) { E->t064 = ts; E->dt64 = 2 * M_PI; continue; }
     double te = conic_t64(E->o64, E->a64, E->b64, V[E->ve].y64);
     double dd = te - ts;
-    /* pick the 2*pi branch closest to the binary32 span */
+    /* pick the 2*pi branch closest to the decided span */
     double k = floor(((double)E->dt - dd) / (2 * M_PI) + 0.5);
     E->t064 = ts; E->dt64 = dd + 2 * M_PI * k;
   }
 
   M->nv = nv; M->na = na; M->nh = nh;
   M->v = V; M->a = A; M->le = LE; M->he = HE;
+  W.V = NULL; W.A = NULL;
+  work_free(&W);
   free(M->hole_off);
   M->hole_off = hoff;
   M->status = ORC_OK;
   return ORC_OK;
+#undef FAIL
 }
 
 /* compute the meta-mesh of selected nodes (nodes == NULL: all); a node in error keeps
@@ -833,12 +938,49 @@ int orc_metamesh(orc_lat *L, const int64_t *nodes, int64_t n_sel) {
     if (node_metamesh(L, n) != ORC_OK) {
       node_mm *M = &L->mm[n];
       bad++;
-      for (int k = 0; k <= M->d; k++) M->loop_off[k] = 0;
+      for (int k = 0; k <= M->d && M->loop_off; k++) M->loop_off[k] = 0;
       M->nv = M->na = M->nh = 0;
     }
   }
   L->tri_ready = 0;
   return (int)(bad > 2147483647 ? 2147483647 : bad);
+}
+
+/* Topology digest of a node: status, d, counts, tie masks, arc sides and endpoints, loop
+ * order (arc, direction), hole contours -- no floating-point values.  FNV-1a 64. */
+static uint64_t fnv(uint64_t h, uint64_t v) {
+  for (int i = 0; i < 8; i++) { h ^= (v >> (8 * i)) & 0xff; h *= 0x100000001b3ull; }
+  return h;
+}
+static uint64_t node_topo_hash(const node_mm *M) {
+  uint64_t h = 0xcbf29ce484222325ull;
+  h = fnv(h, (uint64_t)M->status); h = fnv(h, (uint64_t)M->d);
+  if (M->status) return h;
+  h = fnv(h, (uint64_t)M->nv); h = fnv(h, (uint64_t)M->na); h = fnv(h, (uint64_t)M->nh);
+  for (int q = 0; q < M->nv; q++) h = fnv(h, M->v[q].mask);
+  for (int i = 0; i < M->na; i++) {
+    const arc_t *E = &M->a[i];
+    h = fnv(h, (uint64_t)E->lo | ((uint64_t)E->hi << 16) | ((uint64_t)E->vs << 32) | ((uint64_t)E->ve << 48));
+  }
+  for (int k = 0; k <= M->d; k++) h = fnv(h, (uint64_t)M->loop_off[k]);
+  for (int i = 0; i < M->loop_off[M->d]; i++) h = fnv(h, (uint64_t)M->le[i].arc | ((uint64_t)M->le[i].fwd << 32));
+  for (int k = 0; k <= M->nh; k++) h = fnv(h, (uint64_t)(M->nh ? M->hole_off[k] : 0));
+  int nhe = M->nh ? M->hole_off[M->nh] : 0;
+  for (int i = 0; i < nhe; i++) h = fnv(h, (uint64_t)M->he[i].arc | ((uint64_t)M->he[i].fwd << 32));
+  return h;
+}
+
+/* Meta-mesh of selected nodes, one at a time with nothing kept: status[i] and the
+ * topology digest hash[i] (either may be NULL).  For scans of whole large lattices. */
+void orc_metamesh_scan(orc_lat *L, const int64_t *nodes, int64_t n_sel, int32_t *status, uint64_t *hash) {
+  for (int64_t i = 0; i < n_sel; i++) {
+    int64_t n = nodes[i];
+    node_metamesh(L, n);
+    if (status) status[i] = L->mm[n].status;
+    if (hash) hash[i] = node_topo_hash(&L->mm[n]);
+    node_free(&L->mm[n]);
+  }
+  L->tri_ready = 0;
 }
 
 /* ------------------------------------------------------------------------- */
@@ -852,12 +994,12 @@ int orc_node_counts(const orc_lat *L, int64_t n, int32_t *out /* status,d,nv,na,
   return M->done;
 }
 
-/* vertices: mask, kind, pos32[3], pos64[3] */
-void orc_node_verts(const orc_lat *L, int64_t n, uint32_t *mask, float *pos32, double *pos64) {
+/* vertices: mask (64-bit), pos32[3] (decision arithmetic, as float), pos64[3] */
+void orc_node_verts(const orc_lat *L, int64_t n, uint64_t *mask, float *pos32, double *pos64) {
   const node_mm *M = &L->mm[n];
   for (int q = 0; q < M->nv; q++) {
     mask[q] = M->v[q].mask;
-    pos32[3 * q] = M->v[q].y.x; pos32[3 * q + 1] = M->v[q].y.y; pos32[3 * q + 2] = M->v[q].y.z;
+    pos32[3 * q] = (float)M->v[q].y.x; pos32[3 * q + 1] = (float)M->v[q].y.y; pos32[3 * q + 2] = (float)M->v[q].y.z;
     pos64[3 * q] = M->v[q].y64.x; pos64[3 * q + 1] = M->v[q].y64.y; pos64[3 * q + 2] = M->v[q].y64.z;
   }
 }
@@ -868,7 +1010,8 @@ void orc_node_arcs(const orc_lat *L, int64_t n, int32_t *ints, float *f32, doubl
   for (int i = 0; i < M->na; i++) {
     const arc_t *E = &M->a[i];
     ints[4 * i] = E->lo; ints[4 * i + 1] = E->hi; ints[4 * i + 2] = E->vs; ints[4 * i + 3] = E->ve;
-    float f[11] = {E->t0, E->dt, E->o.x, E->o.y, E->o.z, E->a.x, E->a.y, E->a.z, E->b.x, E->b.y, E->b.z};
+    float f[11] = {(float)E->t0, (float)E->dt, (float)E->o.x, (float)E->o.y, (float)E->o.z, (float)E->a.x, (float)E->a.y,
+                   (float)E->a.z, (float)E->b.x, (float)E->b.y, (float)E->b.z};
     double g[11] = {E->t064, E->dt64, E->o64.x, E->o64.y, E->o64.z, E->a64.x, E->a64.y, E->a64.z, E->b64.x, E->b64.y, E->b64.z};
     memcpy(f32 + 11 * i, f, sizeof f);
     memcpy(f64 + 11 * i, g, sizeof g);
@@ -882,7 +1025,7 @@ void orc_node_loops(const orc_lat *L, int64_t n, int32_t *loop_off, int32_t *int
   int ne = M->loop_off ? M->loop_off[M->d] : 0;
   for (int i = 0; i < ne; i++) {
     ints[2 * i] = M->le[i].arc; ints[2 * i + 1] = M->le[i].fwd;
-    f32[2 * i] = M->le[i].phs; f32[2 * i + 1] = M->le[i].dph;
+    f32[2 * i] = (float)M->le[i].phs; f32[2 * i + 1] = (float)M->le[i].dph;
   }
 }
 
@@ -904,10 +1047,11 @@ void orc_csr(const orc_lat *L, int64_t *off, int64_t *strut) {
 /* ------------------------------------------------------------------------- */
 /* Eq. 11: N = floor((t2 - t1) / (2 acos(1 - CE))) + 1, taken in binary32 with
  * th0 = (float)(2 acos(1 - CE)) evaluated once in binary64. */
-static inline int arc_N(float dt, float th0) { return (int)floorf(dt / th0) + 1; }
+static inline int arc_N(real dt, real th0) { return (int)FLOOR(dt / th0) + 1; }
 
 float orc_theta0(double ce) { return (float)(2.0 * acos(1.0 - ce)); }
 int orc_subdiv_count(float dt, float th0) { return arc_N(dt, th0); }
+static real theta0_dec(double ce) { return (real)(2.0 * acos(1.0 - ce)); }
 
 /* Eq. 12 point jj of arc (binary64): endpoints are the shared vertices exactly */
 static d3 arc_point64(const node_mm *M, const arc_t *E, int N, int jj) {
@@ -923,7 +1067,7 @@ static int64_t loop_csr(const orc_lat *L, int64_t n, int64_t s) {
   return -1;
 }
 
-typedef struct { int n; float *ang; d3 *pt; } ring_t;
+typedef struct { int n; real *ang; d3 *pt; } ring_t;
 
 /* the loop of strut s at node n as a ring of points (binary64) and stitch angles
  * (binary32: ang_j = phs + j * (dph / N) within each arc) */
@@ -936,7 +1080,7 @@ static int loop_ring(const orc_lat *L, int64_t n, int64_t s, ring_t *rg, int wan
   int tot = 0;
   for (int i = b; i < e; i++) tot += arc_N(M->a[M->le[i].arc].dt, L->th0);
   rg->n = tot;
-  rg->ang = (float *)malloc(sizeof(float) * (size_t)tot);
+  rg->ang = (real *)malloc(sizeof(real) * (size_t)tot + 8);
   if (want_pts) rg->pt = (d3 *)malloc(sizeof(d3) * (size_t)tot);
   d3 on = d_of(node_pos(L, n));
   int p = 0;
@@ -944,9 +1088,9 @@ static int loop_ring(const orc_lat *L, int64_t n, int64_t s, ring_t *rg, int wan
     const loop_t *x = &M->le[i];
     const arc_t *E = &M->a[x->arc];
     int N = arc_N(E->dt, L->th0);
-    float step = x->dph / (float)N;
+    real step = x->dph / (real)N;
     for (int j = 0; j < N; j++) {
-      rg->ang[p] = x->phs + (float)j * step;
+      rg->ang[p] = x->phs + (real)j * step;
       if (want_pts) rg->pt[p] = d_add(on, arc_point64(M, E, N, x->fwd ? j : N - j));
       p++;
     }
@@ -958,13 +1102,13 @@ static void ring_free(ring_t *r) { free(r->ang); free(r->pt); }
 
 /* rotation of ring B so that it starts at its first point at/after A's start
  * angle (binary32 decisions) */
-static int band_rotation(const ring_t *A, const ring_t *B, float *brel) {
-  float a0 = A->ang[0];
+static int band_rotation(const ring_t *A, const ring_t *B, real *brel) {
+  real a0 = A->ang[0];
   int k = 0;
   for (int j = 0; j < B->n; j++) {
-    float r = B->ang[j] - a0;
-    if (r < 0.0f) r += TWO_PI_F;
-    if (r >= TWO_PI_F) r -= TWO_PI_F;
+    real r = B->ang[j] - a0;
+    if (r < 0) r += TWO_PI_R;
+    if (r >= TWO_PI_R) r -= TWO_PI_R;
     brel[j] = r;
     if (r < brel[k]) k = j;
   }
@@ -981,12 +1125,12 @@ static void tri_out(double *out, d3 p1, d3 p2, d3 p3) {
 
 /* band of strut s: merge rings A (end i0) and B (end i1) by stitch angle.
  * Writes triangles [from, to) of the band's nA+nB (out may be NULL). */
-static void band_emit(const ring_t *A, const ring_t *B, int k, const float *brel, int64_t from, int64_t to, double *out) {
+static void band_emit(const ring_t *A, const ring_t *B, int k, const real *brel, int64_t from, int64_t to, double *out) {
   int nA = A->n, nB = B->n;
   int i = 0, j = 0;
   for (int64_t t = 0; t < nA + nB && t < to; t++) {
-    float an = (i + 1 < nA) ? A->ang[i + 1] - A->ang[0] : TWO_PI_F;
-    float bn = (j + 1 < nB) ? brel[(j + 1 + k) % nB] : brel[k] + TWO_PI_F;
+    real an = (i + 1 < nA) ? A->ang[i + 1] - A->ang[0] : TWO_PI_R;
+    real bn = (j + 1 < nB) ? brel[(j + 1 + k) % nB] : brel[k] + TWO_PI_R;
     int advA = i < nA && (j == nB || an <= bn);
     if (t >= from && out) {
       double *o = out + 12 * (t - from);
@@ -1036,7 +1180,7 @@ static int hole_ring(const orc_lat *L, int64_t n, int h, d3 **pts, d3 *bp) {
  * ascending with their holes in order (fan i = 0..M-1). */
 int64_t orc_triangulate(orc_lat *L, double ce) {
   L->ce = ce;
-  L->th0 = orc_theta0(ce);
+  L->th0 = theta0_dec(ce);
   free(L->band_n); free(L->strut_tri_off); free(L->hole_base); free(L->hole_M);
   free(L->hole_tri_off); free(L->hole_bp);
   int64_t S = L->n_struts;
@@ -1046,7 +1190,7 @@ int64_t orc_triangulate(orc_lat *L, double ce) {
     ring_t A, B;
     int ra = loop_ring(L, L->ends[2 * s], s, &A, 0), rb = loop_ring(L, L->ends[2 * s + 1], s, &B, 0);
     if (ra == 0 && rb == 0 && A.n > 0 && B.n > 0) {
-      float *brel = (float *)malloc(sizeof(float) * (size_t)B.n);
+      real *brel = (real *)malloc(sizeof(real) * (size_t)B.n + 8);
       int k = band_rotation(&A, &B, brel);
       L->band_n[3 * s] = A.n; L->band_n[3 * s + 1] = B.n; L->band_n[3 * s + 2] = k;
       free(brel);
@@ -1099,7 +1243,7 @@ int64_t orc_strut_triangles(const orc_lat *L, int64_t s, double *out) {
   int ra = loop_ring(L, L->ends[2 * s], s, &A, 1), rb = loop_ring(L, L->ends[2 * s + 1], s, &B, 1);
   int64_t cnt = 0;
   if (ra == 0 && rb == 0 && A.n > 0 && B.n > 0) {
-    float *brel = (float *)malloc(sizeof(float) * (size_t)B.n);
+    real *brel = (real *)malloc(sizeof(real) * (size_t)B.n + 8);
     int k = band_rotation(&A, &B, brel);
     band_emit(&A, &B, k, brel, 0, A.n + B.n, out);
     cnt = A.n + B.n;

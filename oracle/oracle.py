@@ -10,34 +10,38 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "mm_oracle.c")
-_LIB = os.path.join(_HERE, "liborc.so")
+_LIBS = {32: os.path.join(_HERE, "liborc.so"), 64: os.path.join(_HERE, "liborc64.so")}
 _lock = threading.Lock()
-_lib = None
+_libs = {}
 
 # binary32 topology decisions must not be contracted into FMAs or reassociated
 CFLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-std=c11", "-fPIC", "-shared", "-Wall"]
+# liborc64.so: the same source with every decision in binary64 (DESIGN.md Sec. 9 pin)
+CFLAGS64 = ["-DORC_REAL64"]
 
-ORC_STATUS = {0: "ok", 1: "degree>31", 2: "bad strut", 3: "junction capacity", 4: "cluster capacity",
-              5: "arc capacity", 6: "unbounded conic", 7: "unreferenced vertex", 8: "loop chain",
+ORC_STATUS = {0: "ok", 1: "degree>63", 2: "bad strut", 3: "(reserved)", 4: "(reserved)",
+              5: "(reserved)", 6: "unbounded conic", 7: "unreferenced vertex", 8: "loop chain",
               9: "loop angle sum", 10: "empty loop", 11: "hole chain", 12: "strut too short",
-              13: "conic vertex capacity"}
+              13: "(reserved)"}
+MAX_DEGREE = 63
 
 
 def build_oracle(force: bool = False) -> str:
-    """Compile the C oracle with gcc (building the checker is not using it)."""
+    """Compile the C oracle (binary32 decisions) and its binary64-decision twin with gcc
+    (building the checker is not using it)."""
     with _lock:
-        if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-            tmp = _LIB + f".tmp{os.getpid()}"
-            subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, _SRC, "-lm"])
-            os.replace(tmp, _LIB)
-    return _LIB
+        for bits, lib in _LIBS.items():
+            if force or not os.path.exists(lib) or os.path.getmtime(lib) < os.path.getmtime(_SRC):
+                tmp = lib + f".tmp{os.getpid()}"
+                subprocess.check_call(["gcc", *CFLAGS, *(CFLAGS64 if bits == 64 else []), "-o", tmp, _SRC, "-lm"])
+                os.replace(tmp, lib)
+    return _LIBS[32]
 
 
-def _load():
-    global _lib
-    if _lib is None:
+def _load(bits: int = 32):
+    if bits not in _libs:
         build_oracle()
-        lib = C.CDLL(_LIB)
+        lib = C.CDLL(_LIBS[bits])
         P = C.c_void_p
         i64, i32, f32, f64 = C.c_int64, C.c_int32, C.c_float, C.c_double
         lib.orc_create.restype = P
@@ -45,6 +49,8 @@ def _load():
         lib.orc_destroy.argtypes = [P]
         lib.orc_metamesh.restype = C.c_int
         lib.orc_metamesh.argtypes = [P, P, i64]
+        lib.orc_metamesh_scan.argtypes = [P, P, i64, P, P]
+        lib.orc_set_jitter.argtypes = [P, f64, C.c_uint64]
         lib.orc_node_counts.restype = C.c_int
         lib.orc_node_counts.argtypes = [P, i64, P]
         for name in ("orc_node_verts", "orc_node_arcs", "orc_node_loops"):
@@ -73,8 +79,8 @@ def _load():
         lib.orc_aux_plane.argtypes = [P, f64, P, f64, f64, P, P]
         lib.orc_eq9.restype = C.c_int
         lib.orc_eq9.argtypes = [P, P, P, P, P, P, P]
-        _lib = lib
-    return _lib
+        _libs[bits] = lib
+    return _libs[bits]
 
 
 def _p(a: np.ndarray):
@@ -84,8 +90,9 @@ def _p(a: np.ndarray):
 class Oracle:
     """Per-lattice oracle state: CSR, per-node meta-meshes, triangulation."""
 
-    def __init__(self, xyz, node_r, ends):
-        self.lib = _load()
+    def __init__(self, xyz, node_r, ends, bits: int = 32):
+        """bits = 32: the oracle (binary32 decisions); bits = 64: its binary64-decision twin."""
+        self.lib = _load(bits)
         self.xyz = np.ascontiguousarray(xyz, dtype=np.float32)
         self.node_r = np.ascontiguousarray(node_r, dtype=np.float32)
         self.ends = np.ascontiguousarray(ends, dtype=np.int64)
@@ -94,8 +101,8 @@ class Oracle:
         self.h = self.lib.orc_create(_p(self.xyz), _p(self.node_r), self.n_nodes, _p(self.ends), self.n_struts)
 
     @classmethod
-    def from_lattice(cls, lat):
-        return cls(lat.xyz, lat.node_r, lat.ends)
+    def from_lattice(cls, lat, bits: int = 32):
+        return cls(lat.xyz, lat.node_r, lat.ends, bits)
 
     def __del__(self):
         if getattr(self, "h", None):
@@ -110,6 +117,18 @@ class Oracle:
         nodes = np.ascontiguousarray(nodes, dtype=np.int64)
         return self.lib.orc_metamesh(self.h, _p(nodes), len(nodes))
 
+    def scan(self, nodes) -> tuple[np.ndarray, np.ndarray]:
+        """Meta-mesh `nodes` one at a time, keeping nothing: (status int32, topology digest uint64)."""
+        nodes = np.ascontiguousarray(nodes, dtype=np.int64)
+        st = np.zeros(len(nodes), np.int32)
+        hs = np.zeros(len(nodes), np.uint64)
+        self.lib.orc_metamesh_scan(self.h, _p(nodes), len(nodes), _p(st), _p(hs))
+        return st, hs
+
+    def set_jitter(self, eps: float, seed: int) -> None:
+        """binary64 twin only: seeded relative jitter of the side parameters (0 = off)."""
+        self.lib.orc_set_jitter(self.h, float(eps), int(seed))
+
     def csr(self):
         off = np.zeros(self.n_nodes + 1, np.int64)
         st = np.zeros(2 * self.n_struts, np.int64)
@@ -121,7 +140,7 @@ class Oracle:
         done = self.lib.orc_node_counts(self.h, n, _p(cnt))
         status, d, nv, na, nh, nle, nhe = (int(x) for x in cnt)
         out = dict(done=bool(done), status=status, d=d, nv=nv, na=na, nh=nh)
-        mask = np.zeros(nv, np.uint32)
+        mask = np.zeros(nv, np.uint64)
         p32 = np.zeros((nv, 3), np.float32)
         p64 = np.zeros((nv, 3), np.float64)
         self.lib.orc_node_verts(self.h, n, _p(mask), _p(p32), _p(p64))

@@ -17,10 +17,10 @@ LIB_PATH = os.path.join(_HERE, "lib", "liblmm.so")
 LMM_HOST, LMM_DEVICE = 0, 1
 (LMM_BUF_CSR_OFF, LMM_BUF_CSR_ENT, LMM_BUF_NODE_HDR, LMM_BUF_VERT, LMM_BUF_ARC, LMM_BUF_LOOP_HDR,
  LMM_BUF_LOOP_ENT, LMM_BUF_HOLE_HDR, LMM_BUF_HOLE_ENT, LMM_BUF_BAND, LMM_BUF_STRUT_OFF, LMM_BUF_HOLE_M,
- LMM_BUF_HOLE_OFF, LMM_BUF_HOLE_BP, LMM_BUF_NODE_HOLE0) = range(15)
+ LMM_BUF_HOLE_OFF, LMM_BUF_HOLE_BP, LMM_BUF_NODE_HOLE0, LMM_BUF_SLAB_KEY, LMM_BUF_VMASK_HI) = range(17)
 KERNEL_CLASSES = ["csr", "bucket", "metamesh", "count", "scan", "emit"]
 STL_RECORD = 50
-# slab layout constants (lmm_common.cuh): base = K * csr_off[n] + K0 * n
+# slab layout constants (lmm_common.cuh): base = K * off + K0 * n for the node's slab key (off, n)
 SLAB = {"v": (2, 2), "a": (3, 2), "l": (6, 4), "h": (2, 2), "he": (3, 2)}
 
 
@@ -81,12 +81,32 @@ def _check(rc):
 def _ptr(x):
     """(pointer, where) of a numpy array or a torch tensor."""
     if isinstance(x, np.ndarray):
-        assert x.flags["C_CONTIGUOUS"]
+        if not x.flags["C_CONTIGUOUS"]:
+            raise ValueError("array must be C-contiguous")
         return x.ctypes.data_as(C.c_void_p), LMM_HOST
     if hasattr(x, "data_ptr"):
-        assert x.is_contiguous()
+        if not x.is_contiguous():
+            raise ValueError("tensor must be contiguous")
         return C.c_void_p(x.data_ptr()), (LMM_DEVICE if x.is_cuda else LMM_HOST)
     raise TypeError(type(x))
+
+
+def _dtype_name(x) -> str:
+    return str(x.dtype).replace("torch.", "")
+
+
+def _nbytes(x) -> int:
+    return int(x.nbytes) if isinstance(x, np.ndarray) else int(x.numel() * x.element_size())
+
+
+def _require(x, dtype: str, shape_tail: tuple, what: str):
+    """Validate dtype and trailing shape before a pointer crosses the C-ABI (a short or
+    mistyped buffer would be read out of bounds)."""
+    if _dtype_name(x) != dtype:
+        raise TypeError(f"{what}: dtype {_dtype_name(x)}, expected {dtype}")
+    shp = tuple(x.shape)
+    if len(shp) != 1 + len(shape_tail) or shp[1:] != shape_tail:
+        raise ValueError(f"{what}: shape {shp}, expected [n, {', '.join(map(str, shape_tail))}]")
 
 
 def lmm_create(device: int = 0, stream: int | None = None):
@@ -102,8 +122,14 @@ def lmm_destroy(h):
 
 def lmm_load_lattice(h, xyz, ends, r_end):
     """xyz float32 [N,3], ends int64 [S,2], r_end float32 [S,2]: all host (numpy) or all device (torch)."""
+    _require(xyz, "float32", (3,), "xyz")
+    _require(ends, "int64", (2,), "ends")
+    _require(r_end, "float32", (2,), "r_end")
+    if r_end.shape[0] != ends.shape[0]:
+        raise ValueError(f"r_end has {r_end.shape[0]} rows, ends {ends.shape[0]}")
     (px, wx), (pe, we), (pr, wr) = _ptr(xyz), _ptr(ends), _ptr(r_end)
-    assert wx == we == wr, "inputs must all be host or all device"
+    if not (wx == we == wr):
+        raise ValueError("inputs must all be host or all device")
     _check(load_library().lmm_load_lattice(h, px, int(xyz.shape[0]), pe, pr, int(ends.shape[0]), wx))
 
 
@@ -122,6 +148,9 @@ def lmm_metamesh_stats(h) -> dict:
 
 def lmm_set_emit_mask(h, node_mask=None, strut_mask=None):
     """uint8 masks (numpy host or torch device arrays), None = all."""
+    for m, what in ((node_mask, "node_mask"), (strut_mask, "strut_mask")):
+        if m is not None and _dtype_name(m) != "uint8":
+            raise TypeError(f"{what}: dtype {_dtype_name(m)}, expected uint8")
     pn, wn = _ptr(node_mask) if node_mask is not None else (None, None)
     ps, ws = _ptr(strut_mask) if strut_mask is not None else (None, None)
     where = wn if wn is not None else (ws if ws is not None else LMM_HOST)
@@ -136,6 +165,8 @@ def lmm_triangulate(h, chord_error: float) -> int:
 
 def lmm_write_triangles(h, first: int, count: int, out):
     """out: uint8 buffer of >= 50*count bytes (numpy host array, or torch tensor host/device)."""
+    if _nbytes(out) < STL_RECORD * int(count):
+        raise ValueError(f"output buffer holds {_nbytes(out)} bytes, {STL_RECORD * int(count)} needed")
     p, w = _ptr(out)
     _check(load_library().lmm_write_triangles(h, int(first), int(count), p, w))
     return out

@@ -2,7 +2,7 @@
 
     python -m paper_2405_15197_b200.build        # or __graft_entry__.build()
 
-metamesh.cu is compiled with -fmad=false: its binary32 topology decisions follow the
+metamesh.cu and spill.cu are compiled with -fmad=false: its binary32 topology decisions follow the
 fixed-order specification of DESIGN.md Sec. 4 (no implicitly contracted multiply-adds; the
 specification's own FMAs are written explicitly).
 """
@@ -26,6 +26,7 @@ SOURCES = {
     "lattice.cu": [],
     "scan.cu": [],
     "metamesh.cu": ["-fmad=false"],
+    "spill.cu": ["-fmad=false"],
     "triangulate.cu": [],
 }
 

@@ -58,6 +58,41 @@ static void resolve_timers(lmm_ctx *c) {
   c->ev_pending.clear();
 }
 
+// Slab arrays: regular slots K off + K0 n for (off, n) < (2S, N), then the overflow reserve of
+// roff virtual CSR entries and rn virtual nodes (spill.cu).  Growing with preserve keeps the
+// regular region (the bucketed nodes' results); the overflow region is refilled by the caller.
+int slabs_alloc(lmm_ctx *c, int64_t roff, int64_t rn, bool preserve) {
+  const int64_t S2 = 2 * c->S, N = c->N;
+  // emit records address a node's arc slab as 3 off + 2 n in 32 bits (lmm_load_lattice bound)
+  const int64_t lim = (1ll << 32) - 1 - (3 * S2 + 2 * N);
+  if (lim <= 0) return LMM_E_ARG;
+  if (3 * roff + 2 * rn > lim) { roff = lim / 6; rn = lim / 4; }
+  struct Slab { DevBuf *b; size_t rec; int k, k0; };
+  const Slab sl[] = {{&c->vert, sizeof(float4), SLAB_V_K, SLAB_V_K0}, {&c->arc, sizeof(ArcRec), SLAB_A_K, SLAB_A_K0},
+                     {&c->loop, sizeof(LoopRec), SLAB_L_K, SLAB_L_K0}, {&c->hole_hdr, sizeof(int2), SLAB_H_K, SLAB_H_K0},
+                     {&c->hole_ent, sizeof(HoleEnt), SLAB_HE_K, SLAB_HE_K0}};
+  for (const Slab &q : sl) {
+    const size_t bytes = q.rec * (size_t)(q.k * (S2 + roff) + q.k0 * (N + rn) + 1);
+    if (preserve && q.b->p && q.b->bytes < bytes) {
+      DevBuf nb;
+      int rc;
+      if ((rc = dev_alloc(nb, bytes))) return rc;
+      CUDA_TRY(cudaMemcpyAsync(nb.p, q.b->p, q.rec * (size_t)(q.k * S2 + q.k0 * N), cudaMemcpyDeviceToDevice, c->stream));
+      CUDA_TRY(cudaStreamSynchronize(c->stream));
+      dev_free(*q.b);
+      *q.b = nb;
+    } else {
+      int rc;
+      if ((rc = dev_alloc(*q.b, bytes))) return rc;
+    }
+  }
+  int rc;
+  if ((rc = dev_alloc(c->vmask_hi, sizeof(uint32_t) * (size_t)(SLAB_V_K * roff + SLAB_V_K0 * rn + 1)))) return rc;
+  c->ovf_off = roff;
+  c->ovf_n = rn;
+  return LMM_OK;
+}
+
 extern "C" {
 
 LMM_API const char *lmm_version(void) { return "liblmm 0.1 (sm_100a)"; }
@@ -97,7 +132,8 @@ static void free_all(lmm_ctx *c) {
   DevBuf *bufs[] = {&c->node, &c->ends, &c->csr_off, &c->csr_ent, &c->csr_tmp, &c->strut_csr, &c->deg_hist, &c->bucket_nodes,
                     &c->bucket_cnt, &c->node_hdr, &c->vert, &c->arc, &c->loop_hdr, &c->loop, &c->hole_hdr,
                     &c->hole_ent, &c->band, &c->strut_off, &c->node_hole0, &c->node_hole0_64, &c->hole_M,
-                    &c->hole_off, &c->hole_bp, &c->hole_node, &c->node_mask, &c->strut_mask, &c->mbits, &c->macc, &c->cmap, &c->brec, &c->ring_n, &c->tmp64, &c->scratch, &c->mm_side, &c->mm_state, &c->tri3, &c->scan_tmp};
+                    &c->hole_off, &c->hole_bp, &c->hole_node, &c->node_mask, &c->strut_mask, &c->mbits, &c->macc, &c->cmap, &c->brec, &c->ring_n, &c->tmp64, &c->scratch, &c->mm_side, &c->mm_state, &c->tri3, &c->scan_tmp,
+                    &c->skey, &c->vmask_hi, &c->spill_list, &c->spill_ctl, &c->spill_ws};
   for (DevBuf *b : bufs) dev_free(*b);
   for (int i = 0; i < LMM_NSTAGE; i++) dev_free(c->stage[i]);
 }
@@ -173,13 +209,12 @@ LMM_API int lmm_build_metamesh(lmm_ctx *c) {
   int rc;
   if ((rc = degree_buckets(c))) return rc;
   if ((rc = dev_alloc(c->node_hdr, sizeof(int4) * (N + 1)))) return rc;
-  if ((rc = dev_alloc(c->vert, sizeof(float4) * (SLAB_V_K * S2 + SLAB_V_K0 * N + 1)))) return rc;
-  if ((rc = dev_alloc(c->arc, sizeof(ArcRec) * (SLAB_A_K * S2 + SLAB_A_K0 * N + 1)))) return rc;
   if ((rc = dev_alloc(c->loop_hdr, sizeof(int2) * (S2 + 1)))) return rc;
-  if ((rc = dev_alloc(c->loop, sizeof(LoopRec) * (SLAB_L_K * S2 + SLAB_L_K0 * N + 1)))) return rc;
-  if ((rc = dev_alloc(c->hole_hdr, sizeof(int2) * (SLAB_H_K * S2 + SLAB_H_K0 * N + 1)))) return rc;
-  if ((rc = dev_alloc(c->hole_ent, sizeof(HoleEnt) * (SLAB_HE_K * S2 + SLAB_HE_K0 * N + 1)))) return rc;
+  // overflow reserve for the spilled nodes' virtual slab slots: ~0.2 % of the regular slabs
+  if ((rc = slabs_alloc(c, S2 / 512 + 1024, N / 512 + 64, false))) return rc;
+  if ((rc = slab_key_init(c))) return rc;
   if ((rc = metamesh_run(c))) return rc;
+  if ((rc = spill_run(c))) return rc;
   c->mm_ok = true;
   return LMM_OK;
 }
@@ -298,18 +333,20 @@ static DevBuf *buf_of(lmm_ctx *c, int id, size_t *bytes) {
     case LMM_BUF_CSR_OFF: b = &c->csr_off; n = sizeof(int) * (N + 1); break;
     case LMM_BUF_CSR_ENT: b = &c->csr_ent; n = sizeof(int2) * S2; break;
     case LMM_BUF_NODE_HDR: b = &c->node_hdr; n = sizeof(int4) * N; break;
-    case LMM_BUF_VERT: b = &c->vert; n = sizeof(float4) * (SLAB_V_K * S2 + SLAB_V_K0 * N); break;
-    case LMM_BUF_ARC: b = &c->arc; n = sizeof(ArcRec) * (SLAB_A_K * S2 + SLAB_A_K0 * N); break;
+    case LMM_BUF_VERT: b = &c->vert; n = sizeof(float4) * (SLAB_V_K * (S2 + c->ovf_off) + SLAB_V_K0 * (N + c->ovf_n)); break;
+    case LMM_BUF_ARC: b = &c->arc; n = sizeof(ArcRec) * (SLAB_A_K * (S2 + c->ovf_off) + SLAB_A_K0 * (N + c->ovf_n)); break;
     case LMM_BUF_LOOP_HDR: b = &c->loop_hdr; n = sizeof(int2) * S2; break;
-    case LMM_BUF_LOOP_ENT: b = &c->loop; n = sizeof(LoopRec) * (SLAB_L_K * S2 + SLAB_L_K0 * N); break;
-    case LMM_BUF_HOLE_HDR: b = &c->hole_hdr; n = sizeof(int2) * (SLAB_H_K * S2 + SLAB_H_K0 * N); break;
-    case LMM_BUF_HOLE_ENT: b = &c->hole_ent; n = sizeof(HoleEnt) * (SLAB_HE_K * S2 + SLAB_HE_K0 * N); break;
+    case LMM_BUF_LOOP_ENT: b = &c->loop; n = sizeof(LoopRec) * (SLAB_L_K * (S2 + c->ovf_off) + SLAB_L_K0 * (N + c->ovf_n)); break;
+    case LMM_BUF_HOLE_HDR: b = &c->hole_hdr; n = sizeof(int2) * (SLAB_H_K * (S2 + c->ovf_off) + SLAB_H_K0 * (N + c->ovf_n)); break;
+    case LMM_BUF_HOLE_ENT: b = &c->hole_ent; n = sizeof(HoleEnt) * (SLAB_HE_K * (S2 + c->ovf_off) + SLAB_HE_K0 * (N + c->ovf_n)); break;
     case LMM_BUF_BAND: b = &c->band; n = sizeof(int4) * S; break;
     case LMM_BUF_STRUT_OFF: b = &c->strut_off; n = sizeof(int64_t) * (S + 1); break;
     case LMM_BUF_HOLE_M: b = &c->hole_M; n = sizeof(int) * c->H; break;
     case LMM_BUF_HOLE_OFF: b = &c->hole_off; n = sizeof(int64_t) * (c->H + 1); break;
     case LMM_BUF_HOLE_BP: b = &c->hole_bp; n = sizeof(float4) * c->H; break;
     case LMM_BUF_NODE_HOLE0: b = &c->node_hole0_64; n = sizeof(int64_t) * (N + 1); break;
+    case LMM_BUF_SLAB_KEY: b = &c->skey; n = sizeof(int2) * N; break;
+    case LMM_BUF_VMASK_HI: b = &c->vmask_hi; n = sizeof(uint32_t) * (SLAB_V_K * c->ovf_off + SLAB_V_K0 * c->ovf_n); break;
     default: return nullptr;
   }
   if (!b->p) n = 0;

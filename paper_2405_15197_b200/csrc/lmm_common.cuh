@@ -9,7 +9,9 @@
 
 #include "../../include/lmm.h"
 
-#define LMM_MAXD 31
+#define LMM_MAXD 31         // degree-bucketed kernels (metamesh.cu): sides 0..31 in 32-bit masks
+#define LMM_MAXD_SPILL 63   // spill kernel (spill.cu): sides 0..63 in 64-bit masks
+#define LMM_NODE_SPILL 0xfe // internal node status: left for the spill kernel (never reported)
 #define LMM_TOL_REL 1e-4f   // delta   = TOL * R  : tie tolerance
 #define LMM_CTOL_REL 1e-3f  // delta_c = CTOL * R : vertex clustering radius
 #define LMM_PI_F 3.14159265358979324f
@@ -36,20 +38,31 @@ __host__ __device__ inline int slab_cap(int d, int k, int k0) { return k * d + k
 
 // arc record: 12 x 32 bit (48 B)
 struct ArcRec {
-  uint32_t ids;   // lo | hi<<8 | vs<<16 | ve<<24
+  uint32_t ids;   // lo | hi<<6 | vs<<12 | ve<<22 (arc_ids): sides 0..63, vertex ids 0..1023
   float t0, dt;
   float ox, oy, oz, ax, ay, az, bx, by, bz;
 };
 static_assert(sizeof(ArcRec) == 48, "arc record is 48 bytes");
+// arc sides (lo < hi, 0 = sphere) and end vertices packed in ArcRec.ids
+__host__ __device__ __forceinline__ uint32_t arc_ids(int lo, int hi, int vs, int ve) {
+  return (uint32_t)lo | ((uint32_t)hi << 6) | ((uint32_t)vs << 12) | ((uint32_t)ve << 22);
+}
+__host__ __device__ __forceinline__ int arc_lo(uint32_t i) { return (int)(i & 63u); }
+__host__ __device__ __forceinline__ int arc_hi(uint32_t i) { return (int)((i >> 6) & 63u); }
+__host__ __device__ __forceinline__ int arc_vs(uint32_t i) { return (int)((i >> 12) & 1023u); }
+__host__ __device__ __forceinline__ int arc_ve(uint32_t i) { return (int)(i >> 22); }
 
 // loop entry: arc | fwd<<16, phs, dph, cum (first point index within the loop)
 struct LoopRec {
   uint32_t arc_fwd;
   float phs, dph;
-  int32_t cum;   // point offset in the ring (count pass, low 24 bits) | start vertex << 24 (meta-mesh)
+  int32_t cum;   // point offset in the ring (count pass, low 22 bits) | start vertex << 22 (meta-mesh)
 };
-__host__ __device__ inline int le_cum(int32_t c) { return c & 0xffffff; }
-__host__ __device__ inline int le_vid(int32_t c) { return (int)((uint32_t)c >> 24); }
+#define LE_VID_SHIFT 22
+#define LE_CUM_MASK 0x3fffff
+#define LE_VID_MASK ((int32_t)0xffc00000)
+__host__ __device__ inline int le_cum(int32_t c) { return c & LE_CUM_MASK; }
+__host__ __device__ inline int le_vid(int32_t c) { return (int)((uint32_t)c >> LE_VID_SHIFT); }
 static_assert(sizeof(LoopRec) == 16, "loop record is 16 bytes");
 
 // hole entry: arc | fwd<<16, cum

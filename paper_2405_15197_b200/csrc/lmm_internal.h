@@ -39,6 +39,15 @@ struct lmm_ctx {
   DevBuf loop;       // LoopRec slab
   DevBuf hole_hdr;   // int2 slab
   DevBuf hole_ent;   // HoleEnt slab
+  DevBuf skey;       // int2 [N] slab key (off, n): slab base of node n is K off + K0 n;
+                     //   spilled nodes get a virtual key (2S + voff, N + vn) in the overflow reserve
+  DevBuf vmask_hi;   // uint32 per overflow vertex slot: tie-mask bits 32..63 (degree > 31)
+  int64_t ovf_off = 0, ovf_n = 0;   // overflow reserve behind the regular slabs (virtual CSR entries, nodes)
+  DevBuf spill_list; // int [N] nodes for the spill kernel
+  DevBuf spill_ctl;  // unsigned long long [8] spill control words
+  DevBuf spill_ws;   // per-CTA spill workspace
+  int64_t spill_wsb = 0;   // spill workspace bytes per CTA
+  int64_t n_spill = 0;     // nodes meta-meshed by the spill kernel in the last build
   bool mm_ok = false;
   // triangulation
   double ce = 0.0;
@@ -109,6 +118,12 @@ int lattice_build(lmm_ctx *c, const float *xyz_dev, const int64_t *ends_dev, con
 int degree_buckets(lmm_ctx *c);
 // metamesh.cu
 int metamesh_run(lmm_ctx *c);
+// spill.cu
+int slab_key_init(lmm_ctx *c);
+int spill_run(lmm_ctx *c);
+// lmm_api.cu: slab arrays with an overflow reserve of roff virtual CSR entries / rn virtual
+// nodes; preserve = keep the regular region's contents when growing
+int slabs_alloc(lmm_ctx *c, int64_t roff, int64_t rn, bool preserve);
 // scan.cu
 int scan_exclusive_i64(lmm_ctx *c, const int64_t *in, int64_t *out, int64_t n, int64_t *total_host);
 int scan_exclusive_i32_to_i64(lmm_ctx *c, const int *in, int64_t *out, int64_t n, int64_t *total_host);

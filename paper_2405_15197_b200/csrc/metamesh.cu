@@ -18,6 +18,7 @@
 #include <cooperative_groups/reduce.h>
 
 #include "lmm_internal.h"
+#include "mm_node.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -29,6 +30,7 @@ extern "C" LMM_API int lmm_debug_phase_cycles(unsigned long long *out) {
 #endif
 
 namespace {
+using namespace mm;
 
 // per-bucket capacities <MAXS, MAXJ, MAXV, MAXA, MAXLE, MAXH> (degree 1-4, 5-8, 9-12, 13-16, 17-23, 24-31)
 // (MAXJ = the junction capacity of the degree class, reading R13, as the oracle's)
@@ -119,188 +121,6 @@ struct alignas(16) WS_C : WSCore<MAXS, MAXV> {
   int hoff[MAXH + 1];
   uint32_t he[MAXA];
 };
-
-// packed fp32 pairs (sm_100 add/mul .f32x2, round-to-nearest per lane)
-__device__ __forceinline__ unsigned long long f2u(float2 a) {
-  return (unsigned long long)__float_as_uint(a.x) | ((unsigned long long)__float_as_uint(a.y) << 32);
-}
-__device__ __forceinline__ float2 u2f(unsigned long long u) {
-  return make_float2(__uint_as_float((unsigned)u), __uint_as_float((unsigned)(u >> 32)));
-}
-__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
-  unsigned long long r;
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2u(a)), "l"(f2u(b)));
-  return u2f(r);
-}
-__device__ __forceinline__ float2 add2(float2 a, float2 b) {
-  unsigned long long r;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2u(a)), "l"(f2u(b)));
-  return u2f(r);
-}
-__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
-  unsigned long long r;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(f2u(a)), "l"(f2u(b)), "l"(f2u(c)));
-  return u2f(r);
-}
-// h_m at two points at once, each lane rounded like the scalar hs(m, y) - tau: the product, two
-// explicit fused multiply-adds, then + (-e) and + (-tau).  (Never write a packed add of a packed
-// product: ptxas contracts add.rn.f32x2 of a mul.rn.f32x2 result into FFMA2 even under
-// -fmad=false; tests/test_abi.py checks the PTX for such pairs.)
-__device__ __forceinline__ float2 side_h2(float4 p0, float4 p1, float2 Yx, float2 Yy, float2 Yz, float2 nT) {
-  float2 h = mul2(make_float2(p0.x, p0.y), Yx);
-  h = fma2(make_float2(p0.z, p0.w), Yy, h);
-  h = fma2(make_float2(p1.x, p1.y), Yz, h);
-  return add2(add2(h, make_float2(p1.z, p1.w)), nT);
-}
-
-template <class WS> struct Node {
-  WS &w;
-  int d;
-  float R;
-  __device__ f3 W(int k) const { const float4 q = w.w4[k]; return F3(q.x, q.y, q.z); }
-  __device__ float E(int k) const { return w.w4[k].w; }
-  __device__ f3 U(int k) const { return F3(w.ux[k], w.uy[k], w.uz[k]); }
-  __device__ f3 AS(int k) const { return F3(w.asx[k], w.asy[k], w.asz[k]); }
-  __device__ f3 E1(int k) const { return F3(w.e1x[k], w.e1y[k], w.e1z[k]); }
-  __device__ f3 E2(int k) const { return F3(w.e2x[k], w.e2y[k], w.e2z[k]); }
-  __device__ f3 V(int q) const { return F3(w.vx[q], w.vy[q], w.vz[q]); }
-  __device__ float h(int k, f3 y) const { return k == 0 ? 0.0f : hs(k, y); }
-  // strut side k >= 1: fma(w.z, y.z, fma(w.y, y.y, w.x y.x)) - e
-  __device__ float hs(int k, f3 y) const {
-    const float4 q = w.w4[k];
-    return __fsub_rn(f_dot(F3(q.x, q.y, q.z), y), q.w);
-  }
-
-  // triple junction (oracle junction32), without branches: the three
-  // rejection tests become a flag and the divisors of rejected lanes are replaced by 1 (their
-  // roots are never used), so the group stays converged; accepted lanes compute exactly the
-  // specification's operations
-  __device__ bool junction_bf(int a, int b, int c, f3 *y, float *tau) const {
-    f3 Wa = W(a), Wb = W(b), Wc = W(c);
-    float Ea = E(a), Eb = E(b), Ec = E(c);   // side 0 (the sphere) has W = 0, E = 0
-    f3 n1 = f_sub(Wa, Wb), n2 = f_sub(Wa, Wc);
-    float q1 = Ea - Eb, q2 = Ea - Ec;
-    f3 m = f_cross(n1, n2);
-    float mm = f_dot(m, m);
-    float nn1 = f_dot(n1, n1), nn2 = f_dot(n2, n2);
-    bool ok = mm > (1e-8f * nn1) * nn2;
-    mm = ok ? mm : 1.0f;
-    f3 c1 = f_cross(n2, m), c2 = f_cross(m, n1);
-    float imm = 1.0f / mm;
-    f3 y0 = F3(__fmaf_rn(q2, c2.x, __fmul_rn(q1, c1.x)) * imm, __fmaf_rn(q2, c2.y, __fmul_rn(q1, c1.y)) * imm,
-               __fmaf_rn(q2, c2.z, __fmul_rn(q1, c1.z)) * imm);
-    float iml = 1.0f / sqrtf(mm);
-    f3 mh = f_scl(m, iml);
-    float tau0 = f_dot(Wa, y0) - Ea;
-    float tau1 = f_dot(Wa, mh);
-    float A = __fmaf_rn(-tau1, tau1, 1.0f);
-    ok = ok && A > 1e-6f;
-    A = ok ? A : 1.0f;
-    float Bp = __fmaf_rn(-tau0, tau1, f_dot(y0, mh));
-    float C = __fmaf_rn(-tau0, tau0, __fmaf_rn(-R, R, f_dot(y0, y0)));
-    float disc = __fmaf_rn(Bp, Bp, -__fmul_rn(A, C));
-    ok = ok && !(disc < 0.0f);
-    disc = ok ? disc : 0.0f;
-    float sq = sqrtf(disc);
-    float iA = 1.0f / A;
-    float l0 = (-Bp - sq) * iA, l1 = (-Bp + sq) * iA;
-    y[0] = F3(__fmaf_rn(mh.x, l0, y0.x), __fmaf_rn(mh.y, l0, y0.y), __fmaf_rn(mh.z, l0, y0.z));
-    tau[0] = __fmaf_rn(l0, tau1, tau0);
-    y[1] = F3(__fmaf_rn(mh.x, l1, y0.x), __fmaf_rn(mh.y, l1, y0.y), __fmaf_rn(mh.z, l1, y0.z));
-    tau[1] = __fmaf_rn(l1, tau1, tau0);
-    return ok;
-  }
-
-  // branch-free over the sides (same boolean as the early-exit form)
-  __device__ bool valid_strut_pt(uint32_t excl, f3 y, float tau, float delta) const {
-    bool ok = !(tau < -delta);
-#pragma unroll 1
-    for (int m = 1; m <= d; m++) {
-      bool viol = hs(m, y) - tau > delta;
-      ok = ok && (((excl >> m) & 1u) || !viol);
-    }
-    return ok;
-  }
-  // both roots of a triple junction in one pass over the sides: strut junctions
-  // (valid_strut_pt) or, for a sphere triple (tau taken as 0; h - 0 == h exactly), the
-  // tolerant sphere-junction test "no other strut above the sphere by more than delta".
-  // The two roots go through packed f32x2 operations: every lane of those rounds like the
-  // scalar op (same bits as hs(m, y) - tau), h - e as h + (-e), h - tau as h + (-tau).
-  __device__ void valid_junction_pair(bool sphere, uint32_t excl, f3 y0, float t0, f3 y1, float t1, float delta,
-                                      bool *ok0, bool *ok1) const {
-    bool k0 = *ok0 && (sphere || !(t0 < -delta)), k1 = *ok1 && (sphere || !(t1 < -delta));
-    if (sphere) { t0 = 0.0f; t1 = 0.0f; }
-    const float2 Yx = make_float2(y0.x, y1.x), Yy = make_float2(y0.y, y1.y), Yz = make_float2(y0.z, y1.z);
-    const float2 nT = make_float2(-t0, -t1);
-    uint32_t v0 = 0u, v1 = 0u, mb = 2u;   // sides violated by each root (bit m)
-    for (int m = 1; m <= d; m++, mb <<= 1) {
-      const float4 p0 = w.wp[m][0], p1 = w.wp[m][1];
-      const float2 h = side_h2(p0, p1, Yx, Yy, Yz, nT);
-      v0 |= h.x > delta ? mb : 0u;
-      v1 |= h.y > delta ? mb : 0u;
-    }
-    *ok0 = k0 && !(v0 & ~excl); *ok1 = k1 && !(v1 & ~excl);
-  }
-  // end-circle (cap) point: strictly exposed
-  __device__ bool valid_sphere_pt(uint32_t excl, f3 y, float delta) const {
-    bool ok = true;
-#pragma unroll 1
-    for (int m = 1; m <= d; m++) ok = ok && (((excl >> m) & 1u) || !(hs(m, y) > -delta));
-    return ok;
-  }
-
-  // PAPER.md Eq. 7: strut a's ellipse in the auxiliary plane P_{a,b}
-  __device__ bool ellipse(int a, int b, f3 *o, f3 *av, f3 *bv) const {
-    f3 N = f_sub(W(a), W(b));
-    float inl = 1.0f / sqrtf(f_dot(N, N));
-    f3 n = f_scl(N, inl);
-    float pc = (E(a) - E(b)) * inl;
-    f3 p = f_scl(n, pc);
-    float s = w.s[a], c = w.c[a];
-    f3 u = U(a);
-    if (!(fabsf(f_dot(n, u)) > fabsf(s) + 1e-3f)) return false;
-    f3 dd = F3(-u.x, -u.y, -u.z);
-    f3 dp = f_cross(dd, n);
-    float dpl2 = f_dot(dp, dp);
-    f3 r_;
-    if (dpl2 > 1e-12f) { dp = f_scl(dp, 1.0f / sqrtf(dpl2)); r_ = f_cross(dp, dd); }
-    else r_ = E1(a);
-    f3 g1 = F3(c * dd.x - s * r_.x, c * dd.y - s * r_.y, c * dd.z - s * r_.z);
-    f3 g2 = F3(c * dd.x + s * r_.x, c * dd.y + s * r_.y, c * dd.z + s * r_.z);
-    f3 F1 = F3(R * ((-s) * dd.x - c * r_.x), R * ((-s) * dd.y - c * r_.y), R * ((-s) * dd.z - c * r_.z));
-    f3 F2 = F3(R * ((-s) * dd.x + c * r_.x), R * ((-s) * dd.y + c * r_.y), R * ((-s) * dd.z + c * r_.z));
-    float k1 = f_dot(n, f_sub(p, F1)) / f_dot(n, g1);
-    float k2 = f_dot(n, f_sub(p, F2)) / f_dot(n, g2);
-    f3 E1v = f_add(F1, f_scl(g1, k1)), E2v = f_add(F2, f_scl(g2, k2));
-    *o = f_scl(f_add(E1v, E2v), 0.5f);
-    *av = f_scl(f_sub(E1v, E2v), 0.5f);
-    float ad = f_dot(*av, dd), aa = f_dot(*av, *av);
-    float arg = 1.0f - (ad * ad) / ((c * c) * aa);
-    if (arg < 0.0f) arg = 0.0f;
-    float lam = sqrtf(arg);
-    *bv = f_scl(f_cross(*av, n), lam);
-    if (!(f_dot(*bv, *bv) > 1e-12f * aa)) return false;
-    return true;
-  }
-
-  // end-section (tangency) circle of strut b, parametrised by its strut frame
-  __device__ void circle(int b, f3 *o, f3 *av, f3 *bv) const {
-    float rs = R * w.s[b], rr = R * w.c[b];
-    *o = f_scl(U(b), rs);
-    *av = f_scl(E2(b), rr);
-    *bv = f_scl(E1(b), rr);
-  }
-};
-
-__device__ __forceinline__ float conic_t(f3 o, f3 av, f3 bv, f3 P, float *us, float *uc) {
-  f3 Q = f_sub(P, o);
-  float st = f_dot(Q, av) / f_dot(av, av);
-  float ct = f_dot(Q, bv) / f_dot(bv, bv);
-  float il = 1.0f / sqrtf(st * st + ct * ct);
-  *us = st * il;
-  *uc = ct * il;
-  return atan2p(st, ct);
-}
 
 template <int G> __device__ __forceinline__ int excl_scan(cg::thread_block_tile<G> &g, int v, int *total) {
   int x = v;
@@ -411,38 +231,7 @@ __device__ void part_a(cg::thread_block_tile<G> &g, WS &ws, const MMParams &P, i
       int2 ent = P.csr_ent[off + idx];
       int far = ent.y & 0x7fffffff;
       int endbit = (unsigned)ent.y >> 31;
-      float4 pf = P.node[far];
-      f3 po = F3(on.x, on.y, on.z), pfar = F3(pf.x, pf.y, pf.z);
-      f3 D = f_sub(pfar, po);
-      float Ln = sqrtf(f_dot(D, D));
-      if (!(Ln > 0.0f)) err = LMM_NODE_STRUT;
-      else {
-        f3 u = f_div(D, Ln);
-        float s = (R - pf.w) / Ln;
-        if (!(fabsf(s) < 0.9f)) err = LMM_NODE_STRUT;
-        else {
-          float c = sqrtf(1.0f - s * s);
-          f3 wv = f_div(u, c);
-          const float ek = (R * s) / c;
-          ws.w4[k] = make_float4(wv.x, wv.y, wv.z, ek);
-          ws.wp[k][0] = make_float4(wv.x, wv.x, wv.y, wv.y);
-          ws.wp[k][1] = make_float4(wv.z, wv.z, -ek, -ek);
-          ws.ux[k] = u.x; ws.uy[k] = u.y; ws.uz[k] = u.z;
-          ws.s[k] = s; ws.c[k] = c; ws.L[k] = Ln;
-          ws.lim[k] = 0.45f * (Ln * c);
-          ws.sign[k] = endbit ? -1 : 1;
-          // strut frame from p[i1] - p[i0]
-          f3 Da = endbit ? f_sub(po, pfar) : f_sub(pfar, po);
-          f3 as = f_nrm(Da);
-          float ax = fabsf(as.x), ay = fabsf(as.y), az = fabsf(as.z);
-          f3 ref = (ax <= ay && ax <= az) ? F3(1.0f, 0.0f, 0.0f) : (ay <= az ? F3(0.0f, 1.0f, 0.0f) : F3(0.0f, 0.0f, 1.0f));
-          f3 e1 = f_nrm(f_cross(as, ref));
-          f3 e2 = f_cross(as, e1);
-          ws.asx[k] = as.x; ws.asy[k] = as.y; ws.asz[k] = as.z;
-          ws.e1x[k] = e1.x; ws.e1y[k] = e1.y; ws.e1z[k] = e1.z;
-          ws.e2x[k] = e2.x; ws.e2y[k] = e2.y; ws.e2z[k] = e2.z;
-        }
-      }
+      if (!mm::setup_side(ws, k, on, P.node[far], endbit)) err = LMM_NODE_STRUT;
     }
   }
   if (g.any(err != 0)) status = LMM_NODE_STRUT;
@@ -827,7 +616,7 @@ __device__ void part_b(cg::thread_block_tile<G> &g, WS &ws, const MMParams &P, i
             ws.vmask[spos] = (1u << a) | (1u << b);
             vs = ve = spos;
           }
-          A.ids = (uint32_t)a | ((uint32_t)b << 8) | ((uint32_t)vs << 16) | ((uint32_t)ve << 24);
+          A.ids = arc_ids(a, b, vs, ve);
           A.t0 = t0v[i]; A.dt = dtv[i];
           ws.atmid[pos + i] = tmv[i];
           A.ox = o.x; A.oy = o.y; A.oz = o.z;
@@ -849,14 +638,14 @@ __device__ void part_b(cg::thread_block_tile<G> &g, WS &ws, const MMParams &P, i
     #pragma unroll 1
     for (int i = lane; i < na; i += G) {
       uint32_t ids = ws.arcs[i].ids;
-      int lo = ids & 0xff, hi = (ids >> 8) & 0xff, vs = (ids >> 16) & 0xff, ve = ids >> 24;
+      int lo = arc_lo(ids), hi = arc_hi(ids), vs = arc_vs(ids), ve = arc_ve(ids);
       int drop = 0;
       if (lo > 0 && vs != ve && ws.atmid[i] < delta) {
         int ca = 0, cb = 0;
         for (int j = 0; j < na; j++) {
           uint32_t jd = ws.arcs[j].ids;
-          if ((jd & 0xff) != 0) continue;
-          int js = (jd >> 16) & 0xff, je = jd >> 24, jh = (jd >> 8) & 0xff;
+          if (arc_lo(jd) != 0) continue;
+          int js = arc_vs(jd), je = arc_ve(jd), jh = arc_hi(jd);
           if (!((js == vs && je == ve) || (js == ve && je == vs))) continue;
           if (jh == lo) ca = 1;
           if (jh == hi) cb = 1;
@@ -889,7 +678,7 @@ __device__ void part_b(cg::thread_block_tile<G> &g, WS &ws, const MMParams &P, i
     #pragma unroll 1
     for (int i = lane; i < na; i += G) {
       const uint32_t ids = ws.arcs[i].ids;
-      used |= (1ull << ((ids >> 16) & 0xff)) | (1ull << (ids >> 24));
+      used |= (1ull << arc_vs(ids)) | (1ull << arc_ve(ids));
     }
     used = cg::reduce(g, used, cg::bit_or<unsigned long long>());
     const unsigned long long need = nc >= 64 ? ~0ull : (1ull << nc) - 1ull;
@@ -943,8 +732,8 @@ __device__ void part_c(cg::thread_block_tile<G> &g, WS &ws, const MMParams &P, i
     #pragma unroll 1
     for (int i = lane; i < na; i += G) {
       const ArcRec &A = ws.arcs[i];
-      const int lo = A.ids & 0xff, hi = (A.ids >> 8) & 0xff;
-      const int avs = (A.ids >> 16) & 0xff, ave = A.ids >> 24;
+      const int lo = arc_lo(A.ids), hi = arc_hi(A.ids);
+      const int avs = arc_vs(A.ids), ave = arc_ve(A.ids);
       for (int x = 0; x < 2; x++) {
         int k = x ? hi : lo;
         if (k == 0) continue;
@@ -977,7 +766,7 @@ __device__ void part_c(cg::thread_block_tile<G> &g, WS &ws, const MMParams &P, i
     #pragma unroll 1
     for (int i = lane; i < na; i += G) {
       uint32_t ids = ws.arcs[i].ids;
-      int lo = ids & 0xff, hi = (ids >> 8) & 0xff;
+      int lo = arc_lo(ids), hi = arc_hi(ids);
       if (lo) atomicAdd(&ws.lcnt[lo], 1);
       atomicAdd(&ws.lcnt[hi], 1);
     }
@@ -997,7 +786,7 @@ __device__ void part_c(cg::thread_block_tile<G> &g, WS &ws, const MMParams &P, i
     #pragma unroll 1
     for (int i = lane; i < na; i += G) {
       uint32_t ids = ws.arcs[i].ids;
-      int lo = ids & 0xff, hi = (ids >> 8) & 0xff;
+      int lo = arc_lo(ids), hi = arc_hi(ids);
       if (lo) ws.lslot[ws.lpos[lo] + atomicAdd(&ws.lfill[lo], 1)] = 2 * i;
       ws.lslot[ws.lpos[hi] + atomicAdd(&ws.lfill[hi], 1)] = 2 * i + 1;
     }
@@ -1028,8 +817,8 @@ __device__ void part_c(cg::thread_block_tile<G> &g, WS &ws, const MMParams &P, i
           for (int i = 0; i < cnt; i++) {
             int sx = slot[i], sy = slot[(i + 1) % cnt];
             const uint32_t X = ws.arcs[sx >> 1].ids, Y = ws.arcs[sy >> 1].ids;
-            int xe = ws.efw[sx] ? (X >> 24) : ((X >> 16) & 0xff);
-            int ys = ws.efw[sy] ? ((Y >> 16) & 0xff) : (Y >> 24);
+            int xe = ws.efw[sx] ? arc_ve(X) : arc_vs(X);
+            int ys = ws.efw[sy] ? arc_vs(Y) : arc_ve(Y);
             if (xe != ys) { e = LMM_NODE_CHAIN; break; }
             sum += ws.edp[sx];
           }
@@ -1052,7 +841,7 @@ __device__ void part_c(cg::thread_block_tile<G> &g, WS &ws, const MMParams &P, i
           L.arc_fwd = (uint32_t)(slot[i] >> 1) | ((uint32_t)ws.efw[slot[i]] << 16);
           L.phs = ph;
           L.dph = ws.edp[slot[i]];
-          L.cum = (int32_t)((ws.efw[slot[i]] ? (aid >> 16) & 0xffu : aid >> 24) << 24);   // start vertex
+          L.cum = (int32_t)((uint32_t)(ws.efw[slot[i]] ? arc_vs(aid) : arc_ve(aid)) << LE_VID_SHIFT);   // start vertex
         }
       }
       nle += tot;
@@ -1065,7 +854,7 @@ __device__ void part_c(cg::thread_block_tile<G> &g, WS &ws, const MMParams &P, i
   bool anycap = false;   // nodes without cap arcs (the sphere fully covered) have no holes
   if (status == 0 && d > 0) {
     #pragma unroll 1
-    for (int i = lane; i < na; i += G) anycap = anycap || (ws.arcs[i].ids & 0xff) == 0;
+    for (int i = lane; i < na; i += G) anycap = anycap || arc_lo(ws.arcs[i].ids) == 0;
     anycap = g.any(anycap);
   }
   if (status == 0 && d > 0 && anycap) {
@@ -1077,26 +866,26 @@ __device__ void part_c(cg::thread_block_tile<G> &g, WS &ws, const MMParams &P, i
       (void)used;
       for (int i = 0; i < na && !st; i++) {
         const ArcRec &Ai = ws.arcs[i];
-        if ((Ai.ids & 0xff) != 0 || ((usedw[i >> 6] >> (i & 63)) & 1)) continue;
+        if (arc_lo(Ai.ids) != 0 || ((usedw[i >> 6] >> (i & 63)) & 1)) continue;
         if (nh >= MAXH) { st = LMM_NODE_ACAP; break; }
         ws.hoff[nh++] = nhe;
         int cur = i;
-        int hb0 = (Ai.ids >> 8) & 0xff;
+        int hb0 = arc_hi(Ai.ids);
         int hf0 = ws.sign[hb0] < 0;
-        int start_v = hf0 ? ((Ai.ids >> 16) & 0xff) : (Ai.ids >> 24);
+        int start_v = hf0 ? arc_vs(Ai.ids) : arc_ve(Ai.ids);
         for (;;) {
           usedw[cur >> 6] |= 1ull << (cur & 63);
           const ArcRec &C = ws.arcs[cur];
-          int hf = ws.sign[(C.ids >> 8) & 0xff] < 0;
+          int hf = ws.sign[arc_hi(C.ids)] < 0;
           ws.he[nhe++] = (uint32_t)cur | ((uint32_t)hf << 16);
-          int endv = hf ? (C.ids >> 24) : ((C.ids >> 16) & 0xff);
+          int endv = hf ? arc_ve(C.ids) : arc_vs(C.ids);
           if (endv == start_v) break;
           int nxt = -1;
           for (int j = 0; j < na && nxt < 0; j++) {
             const ArcRec &Aj = ws.arcs[j];
-            if ((Aj.ids & 0xff) != 0 || ((usedw[j >> 6] >> (j & 63)) & 1)) continue;
-            int hj = ws.sign[(Aj.ids >> 8) & 0xff] < 0;
-            if ((hj ? ((Aj.ids >> 16) & 0xff) : (Aj.ids >> 24)) == endv) nxt = j;
+            if (arc_lo(Aj.ids) != 0 || ((usedw[j >> 6] >> (j & 63)) & 1)) continue;
+            int hj = ws.sign[arc_hi(Aj.ids)] < 0;
+            if ((hj ? arc_vs(Aj.ids) : arc_ve(Aj.ids)) == endv) nxt = j;
           }
           if (nxt < 0) { st = LMM_NODE_HOLE; break; }
           cur = nxt;
@@ -1173,14 +962,15 @@ metamesh_kernel(MMParams P) {
   }
 }
 
-// nodes of degree 0 or > LMM_MAXD
+// nodes of degree 0 (nothing to mesh), 32..63 (left for the spill kernel, spill.cu) and
+// > 63 (outside the model: sides 0..63 in one 64-bit tie mask)
 __global__ void trivial_nodes_kernel(const int *csr_off, int N, int4 *node_hdr, int2 *loop_hdr) {
   int n = blockIdx.x * blockDim.x + threadIdx.x;
   if (n >= N) return;
   int d = csr_off[n + 1] - csr_off[n];
   if (d == 0) node_hdr[n] = make_int4(0, 0, 0, 0);
   else if (d > LMM_MAXD) {
-    node_hdr[n] = make_int4(LMM_NODE_DEGREE | (d << 8), 0, 0, 0);
+    node_hdr[n] = make_int4((d > LMM_MAXD_SPILL ? LMM_NODE_DEGREE : LMM_NODE_SPILL) | (d << 8), 0, 0, 0);
     for (int k = 0; k < d; k++) loop_hdr[csr_off[n] + k] = make_int2(0, 0);
   }
 }

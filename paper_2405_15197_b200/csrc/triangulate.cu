@@ -43,6 +43,7 @@ static_assert(sizeof(BandRec) == 64, "band record is 4 x 16 bytes");
 struct TriParams {
   const float4 *node;
   const int *csr_off;
+  const int2 *skey;         // [N] slab key of each node
   const int2 *csr_ent;
   const int2 *ends;
   const int2 *strut_csr;
@@ -84,11 +85,12 @@ __device__ __forceinline__ float wrap_rel(float b, float a0) {
   return r;
 }
 
-__device__ __forceinline__ int64_t vbase(const int *off, int n) { return slab_base(off[n], n, SLAB_V_K, SLAB_V_K0); }
-__device__ __forceinline__ int64_t abase(const int *off, int n) { return slab_base(off[n], n, SLAB_A_K, SLAB_A_K0); }
-__device__ __forceinline__ int64_t lbase(const int *off, int n) { return slab_base(off[n], n, SLAB_L_K, SLAB_L_K0); }
-__device__ __forceinline__ int64_t hbase(const int *off, int n) { return slab_base(off[n], n, SLAB_H_K, SLAB_H_K0); }
-__device__ __forceinline__ int64_t hebase(const int *off, int n) { return slab_base(off[n], n, SLAB_HE_K, SLAB_HE_K0); }
+// slab bases of a node from its slab key (off, n) (spilled nodes: virtual keys)
+__device__ __forceinline__ int64_t vbase(int2 k) { return slab_base(k.x, k.y, SLAB_V_K, SLAB_V_K0); }
+__device__ __forceinline__ int64_t abase(int2 k) { return slab_base(k.x, k.y, SLAB_A_K, SLAB_A_K0); }
+__device__ __forceinline__ int64_t lbase(int2 k) { return slab_base(k.x, k.y, SLAB_L_K, SLAB_L_K0); }
+__device__ __forceinline__ int64_t hbase(int2 k) { return slab_base(k.x, k.y, SLAB_H_K, SLAB_H_K0); }
+__device__ __forceinline__ int64_t hebase(int2 k) { return slab_base(k.x, k.y, SLAB_HE_K, SLAB_HE_K0); }
 
 // LoopRec.arc_fwd = arc | fwd << 16 | N << 17 (N written by the count pass)
 __device__ __forceinline__ int le_arc(uint32_t af) { return af & 0xffff; }
@@ -98,7 +100,7 @@ __device__ __forceinline__ int le_N(uint32_t af) { return af >> 17; }
 // Eq. 12 point jj of an arc, node-local; the endpoints are the shared vertices exactly
 __device__ __forceinline__ f3 arc_point(const ArcRec &A, const float4 *vslab, int N, int jj) {
   if (jj == 0 || jj == N) {
-    int v = jj == 0 ? (A.ids >> 16) & 0xff : (A.ids >> 24);
+    int v = jj == 0 ? arc_vs(A.ids) : arc_ve(A.ids);
     float4 p = __ldg(&vslab[v]);
     return F3(p.x, p.y, p.z);
   }
@@ -133,7 +135,7 @@ __device__ __forceinline__ int ring_counts(LoopRec *__restrict__ le, int cnt, co
 #pragma unroll
     for (int k = 0; k < 4; k++) af[k] = i0 + k < cnt ? (le[i0 + k].arc_fwd & 0x1ffffu) : 0u;
 #pragma unroll
-    for (int k = 0; k < 4; k++) vt[k] = i0 + k < cnt ? (le[i0 + k].cum & (int)0xff000000) : 0;
+    for (int k = 0; k < 4; k++) vt[k] = i0 + k < cnt ? (le[i0 + k].cum & LE_VID_MASK) : 0;
 #pragma unroll
     for (int k = 0; k < 4; k++) dt[k] = i0 + k < cnt ? __ldg(&arc[le_arc(af[k])].dt) : 0.0f;
 #pragma unroll
@@ -159,9 +161,9 @@ __global__ void k_ring_count(TriParams P, int64_t S2, int *ring_n) {
   const int n = ((unsigned)ent.y >> 31) ? e.y : e.x;   // the node this entry belongs to
   int nr = 0;
   if ((P.node_hdr[n].x & 0xff) == 0) {
-    const int off = P.csr_off[n];
+    const int2 key = P.skey[n];
     const int2 L = P.loop_hdr[i];
-    nr = ring_counts(P.loop + lbase(P.csr_off, n) + L.x, L.y, P.arc + slab_base(off, n, SLAB_A_K, SLAB_A_K0), P.th0);
+    nr = ring_counts(P.loop + lbase(key) + L.x, L.y, P.arc + abase(key), P.th0);
   }
   ring_n[i] = nr;
 }
@@ -229,16 +231,16 @@ __global__ void k_band_merge(TriParams P) {
   int2 ce = P.strut_csr[s];
   int2 LA = P.loop_hdr[ce.x], LB = P.loop_hdr[ce.y];
   {
-    const int offA = P.csr_off[e.x], offB = P.csr_off[e.y];
+    const int2 kA = P.skey[e.x], kB = P.skey[e.y];
     const float4 na = P.node[e.x], nb = P.node[e.y];
-    rq[1] = make_float4(__int_as_float(LB.x | (LB.y << 16)), __uint_as_float(3u * offA + 2u * e.x),
-                        __uint_as_float(3u * offB + 2u * e.y), __uint_as_float((unsigned)(offA + e.x)));
-    rq[2] = make_float4(__uint_as_float((unsigned)(offB + e.y)), na.x, na.y, na.z);
+    rq[1] = make_float4(__int_as_float(LB.x | (LB.y << 16)), __uint_as_float(3u * kA.x + 2u * kA.y),
+                        __uint_as_float(3u * kB.x + 2u * kB.y), __uint_as_float((unsigned)(kA.x + kA.y)));
+    rq[2] = make_float4(__uint_as_float((unsigned)(kB.x + kB.y)), na.x, na.y, na.z);
     rq[3] = make_float4(nb.x, nb.y, nb.z, 0.0f);
   }
   SeqKey A, B;
-  A.le = P.loop + lbase(P.csr_off, e.x) + LA.x; A.cnt = LA.y;
-  B.le = P.loop + lbase(P.csr_off, e.y) + LB.x; B.cnt = LB.y;
+  A.le = P.loop + lbase(P.skey[e.x]) + LA.x; A.cnt = LA.y;
+  B.le = P.loop + lbase(P.skey[e.y]) + LB.x; B.cnt = LB.y;
   A.enter(0, 0);
   const float a0 = A.phs;     // ring A first entry phi
   // rotation of ring B: its first point with the smallest angle relative to A's start
@@ -309,10 +311,11 @@ __global__ void k_hole_count(TriParams P) {
   if (g0 == g1) return;
   const float4 on = P.node[n];
   const float R = on.w;
-  const float4 *vs = P.vert + vbase(P.csr_off, (int)n);
-  const ArcRec *as = P.arc + abase(P.csr_off, (int)n);
-  const int2 *hh = P.hole_hdr + hbase(P.csr_off, (int)n);
-  HoleEnt *he = P.hole_ent + hebase(P.csr_off, (int)n);
+  const int2 key = P.skey[n];
+  const float4 *vs = P.vert + vbase(key);
+  const ArcRec *as = P.arc + abase(key);
+  const int2 *hh = P.hole_hdr + hbase(key);
+  HoleEnt *he = P.hole_ent + hebase(key);
   for (int64_t g = g0; g < g1; g++) {
     int2 H = hh[g - g0];
     int M = 0;
@@ -465,7 +468,22 @@ struct RingRef {
   const float4 *vs;
   float ox, oy, oz;
   int cnt;
+  // the ring's entries in global memory (rings of more than MAXRE entries): 32-bit words,
+  // entry e at gent + e * gst, arc_fwd at word 0, cum at word gco
+  const uint32_t *gent;
+  int gst, gco;
 };
+
+// entry e of ring r: the first MAXRE from shared memory, the rest from global memory
+__device__ __forceinline__ void ring_entry(const WarpRing &w, int r, const RingRef &R, int e, uint32_t &af, int &cum) {
+  if (e < MAXRE) {
+    af = w.le[r][e].arc_fwd;
+    cum = w.le[r][e].cum;
+  } else {
+    af = __ldg(R.gent + (int64_t)e * R.gst);
+    cum = (int)__ldg(R.gent + (int64_t)e * R.gst + R.gco);
+  }
+}
 
 __device__ __forceinline__ ArcRec lds_arc(const ArcRec *p) {
   const float4 *q = reinterpret_cast<const float4 *>(p);
@@ -479,14 +497,15 @@ __device__ __forceinline__ ArcRec lds_arc(const ArcRec *p) {
 
 // Eq. 12 point idx of ring r, whose loop entry is e; endpoints are the shared vertices
 __device__ __forceinline__ f3 ring_point_e(const WarpRing &w, int r, const RingRef &R, int e, int idx) {
-  const LoopRec L = w.le[r][e];
+  LoopRec L;
+  ring_entry(w, r, R, e, L.arc_fwd, L.cum);
   const int N = le_N(L.arc_fwd), fwd = le_fwd(L.arc_fwd);
   const int j = idx - le_cum(L.cum);
   const int jj = fwd ? j : N - j;
   f3 p;
   if (jj == 0 || jj == N) {
     const uint32_t ids = e < MAXRA ? w.arc[r][e].ids : __ldg(&R.arcs[le_arc(L.arc_fwd)].ids);
-    const int v = jj == 0 ? (ids >> 16) & 0xff : (ids >> 24);
+    const int v = jj == 0 ? arc_vs(ids) : arc_ve(ids);
     const float4 q = __ldg(&R.vs[v]);
     p = F3(q.x, q.y, q.z);
   } else {
@@ -503,7 +522,16 @@ __device__ __forceinline__ f3 ring_point_e(const WarpRing &w, int r, const RingR
 // point idx of ring r, its entry found by a scan of the entry starts (windowed bands, holes)
 __device__ __forceinline__ f3 ring_point(const WarpRing &w, int r, const RingRef &R, int idx) {
   int e = 0;
-  for (int k = 1; k < R.cnt; k++) e += (le_cum(w.le[r][k].cum) <= idx) ? 1 : 0;
+  if (R.cnt <= MAXRE) {
+    for (int k = 1; k < R.cnt; k++) e += (le_cum(w.le[r][k].cum) <= idx) ? 1 : 0;
+  } else {   // long ring (spilled nodes): last entry starting at or before idx, binary search
+    int lo = 0, hi = R.cnt - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (le_cum((int)__ldg(R.gent + (int64_t)mid * R.gst + R.gco)) <= idx) lo = mid; else hi = mid - 1;
+    }
+    e = lo;
+  }
   return ring_point_e(w, r, R, e, idx);
 }
 
@@ -720,9 +748,13 @@ __device__ void emit_band(const TriParams &P, WarpRing &w, const Pts &pt, const 
   RA.arcs = P.arc + H.aA;
   RA.vs = P.vert + 2 * (int64_t)H.pA;
   RA.ox = H.oax; RA.oy = H.oay; RA.oz = H.oaz; RA.cnt = rec_cnt(H.lAc);
+  RA.gent = reinterpret_cast<const uint32_t *>(P.loop + 2 * (int64_t)H.aA + rec_first(H.lAc));
+  RA.gst = 4; RA.gco = 3;
   RB.arcs = P.arc + H.aB;
   RB.vs = P.vert + 2 * (int64_t)H.pB;
   RB.ox = H.obx; RB.oy = H.oby; RB.oz = H.obz; RB.cnt = rec_cnt(H.lBc);
+  RB.gent = reinterpret_cast<const uint32_t *>(P.loop + 2 * (int64_t)H.aB + rec_first(H.lBc));
+  RB.gst = 4; RB.gco = 3;
   const int qb = (int)(ta - base), qe = (int)(tb - base);
   prefetch(0);
   if (nA + nB + 2 <= pt.cap && RA.cnt <= MAXRA && RB.cnt <= MAXRA) {
@@ -796,15 +828,18 @@ __device__ void emit_hole(const TriParams &P, WarpRing &w, const Pts &pt, int g,
   if (ta >= tb) return;
   const int n = P.hole_node[g];
   const int64_t g0 = P.node_hole0[n];
-  const int2 H = P.hole_hdr[hbase(P.csr_off, n) + (g - g0)];
+  const int2 key = P.skey[n];
+  const int2 H = P.hole_hdr[hbase(key) + (g - g0)];
   const float4 on = P.node[n];
   const float4 bp4 = P.hole_bp[g];
   const f3 bp = F3(on.x + bp4.x, on.y + bp4.y, on.z + bp4.z);
   RingRef RH;
-  RH.arcs = P.arc + abase(P.csr_off, n); RH.vs = P.vert + vbase(P.csr_off, n);
+  RH.arcs = P.arc + abase(key); RH.vs = P.vert + vbase(key);
   RH.ox = on.x; RH.oy = on.y; RH.oz = on.z; RH.cnt = H.y;
-  // hole entries (arc_fwd, cum) in the loop-entry slots of ring 0
-  const HoleEnt *he = P.hole_ent + hebase(P.csr_off, n) + H.x;
+  // hole entries (arc_fwd, cum) in the loop-entry slots of ring 0 (the first MAXRE)
+  const HoleEnt *he = P.hole_ent + hebase(key) + H.x;
+  RH.gent = reinterpret_cast<const uint32_t *>(he);
+  RH.gst = 2; RH.gco = 1;
   __syncwarp();
   if (lane < H.y) {
     HoleEnt E = he[lane];
@@ -905,6 +940,7 @@ TriParams make_params(lmm_ctx *c) {
   TriParams P;
   P.node = (const float4 *)c->node.p;
   P.csr_off = (const int *)c->csr_off.p;
+  P.skey = (const int2 *)c->skey.p;
   P.csr_ent = (const int2 *)c->csr_ent.p;
   P.ends = (const int2 *)c->ends.p;
   P.strut_csr = (const int2 *)c->strut_csr.p;

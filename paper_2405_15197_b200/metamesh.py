@@ -66,7 +66,9 @@ class MetaMesher:
             csr_off=B.lmm_buffer(h, B.LMM_BUF_CSR_OFF, np.int32),
             csr_ent=B.lmm_buffer(h, B.LMM_BUF_CSR_ENT, np.int32, 2),
             node_hdr=B.lmm_buffer(h, B.LMM_BUF_NODE_HDR, np.int32, 4),
+            skey=B.lmm_buffer(h, B.LMM_BUF_SLAB_KEY, np.int32, 2),
             vert=B.lmm_buffer(h, B.LMM_BUF_VERT, np.float32, 4),
+            vmask_hi=B.lmm_buffer(h, B.LMM_BUF_VMASK_HI, np.uint32),
             arc=B.lmm_buffer(h, B.LMM_BUF_ARC, np.uint32, 12),
             loop_hdr=B.lmm_buffer(h, B.LMM_BUF_LOOP_HDR, np.int32, 2),
             loop=B.lmm_buffer(h, B.LMM_BUF_LOOP_ENT, np.uint32, 4),
@@ -81,20 +83,41 @@ class MetaMesher:
         h = self.h
         off = B.lmm_buffer(h, B.LMM_BUF_CSR_OFF, np.int32, None, n, 2).astype(np.int64)
         d = int(off[1] - off[0])
+        key = B.lmm_buffer(h, B.LMM_BUF_SLAB_KEY, np.int32, 2, n, 1)[0].astype(np.int64)
+        hdr = B.lmm_buffer(h, B.LMM_BUF_NODE_HDR, np.int32, 4, n, 1)
+        N, S = self.stats_sizes()
+        S2 = 2 * S
+        # a spilled node's slots hold exactly its virtual degree; a regular node's its degree
+        cap = _virtual_degree(hdr[0]) if key[1] >= N else d
 
-        def slab(buf, key, dtype, cols):
-            k, k0 = B.SLAB[key]
-            return B.lmm_buffer(h, buf, dtype, cols, k * int(off[0]) + k0 * n, k * d + k0)
-        return dict(
+        def slab(buf, k, dtype, cols):
+            kk, k0 = B.SLAB[k]
+            return B.lmm_buffer(h, buf, dtype, cols, kk * int(key[0]) + k0 * int(key[1]), kk * cap + k0)
+        out = dict(
             csr_off=np.array([0, d], np.int32),
-            node_hdr=B.lmm_buffer(h, B.LMM_BUF_NODE_HDR, np.int32, 4, n, 1),
+            node_hdr=hdr,
+            skey=np.zeros((1, 2), np.int32),
             vert=slab(B.LMM_BUF_VERT, "v", np.float32, 4),
+            vmask_hi=np.zeros(2 * cap + 2, np.uint32),
             arc=slab(B.LMM_BUF_ARC, "a", np.uint32, 12),
             loop_hdr=B.lmm_buffer(h, B.LMM_BUF_LOOP_HDR, np.int32, 2, int(off[0]), d),
             loop=slab(B.LMM_BUF_LOOP_ENT, "l", np.uint32, 4),
             hole_hdr=slab(B.LMM_BUF_HOLE_HDR, "h", np.int32, 2),
             hole_ent=slab(B.LMM_BUF_HOLE_ENT, "he", np.uint32, 2),
         )
+        if key[1] >= N:      # a spilled node: its mask bits 32..63 from the overflow region
+            kk, k0 = B.SLAB["v"]
+            out["vmask_hi"] = B.lmm_buffer(h, B.LMM_BUF_VMASK_HI, np.uint32, None,
+                                           kk * int(key[0] - S2) + k0 * int(key[1] - N), kk * cap + k0)
+        out["skey_global"] = (int(key[0]), int(key[1]), S2, N)
+        return out
+
+    def stats_sizes(self):
+        """(n_nodes, n_struts) of the loaded lattice."""
+        if not hasattr(self, "_sizes"):
+            off = B.lmm_buffer(self.h, B.LMM_BUF_CSR_OFF, np.int32)
+            self._sizes = (len(off) - 1, int(off[-1]) // 2)
+        return self._sizes
 
     def tri_buffers(self) -> dict:
         h = self.h
@@ -108,24 +131,49 @@ class MetaMesher:
         )
 
 
-def _base(off, n, key):
-    k, k0 = B.SLAB[key]
-    return k * int(off[n]) + k0 * n
+def _virtual_degree(hdr) -> int:
+    """The smallest degree whose slab capacities (K d + K0) hold the node's counts."""
+    nv, na = int(hdr[1]) & 0xFFFF, (int(hdr[1]) >> 16) & 0xFFFF
+    nh, nle = int(hdr[2]) & 0xFFFF, (int(hdr[2]) >> 16) & 0xFFFF
+    nhe = int(hdr[3])
+    D = 0
+    for cnt, k in ((nv, "v"), (na, "a"), (nle, "l"), (nh, "h"), (nhe, "he")):
+        kk, k0 = B.SLAB[k]
+        D = max(D, -(-(cnt - k0) // kk))
+    return D
 
 
 def decode_node(bufs: dict, n: int) -> dict:
-    """The meta-mesh of node n in the oracle's per-node format."""
+    """The meta-mesh of node n in the oracle's per-node format (slabs at the node's slab key)."""
     off = bufs["csr_off"]
     hdr = bufs["node_hdr"][n]
     status, d = int(hdr[0]) & 0xFF, int(hdr[0]) >> 8
     nv, na = int(hdr[1]) & 0xFFFF, (int(hdr[1]) >> 16) & 0xFFFF
     nh, nle = int(hdr[2]) & 0xFFFF, (int(hdr[2]) >> 16) & 0xFFFF
     nhe = int(hdr[3])
-    vb, ab, lb, hb, heb = (_base(off, n, k) for k in ("v", "a", "l", "h", "he"))
+    koff, kn = (int(x) for x in bufs["skey"][n])
+
+    def base(k):
+        kk, k0 = B.SLAB[k]
+        return kk * koff + k0 * kn
+    vb, ab, lb, hb, heb = (base(k) for k in ("v", "a", "l", "h", "he"))
     v = bufs["vert"][vb:vb + nv]
+    mask = v[:, 3].copy().view(np.uint32).astype(np.uint64)
+    if "skey_global" in bufs:                       # node_buffers(): the slabs were sliced out
+        gk, gn, S2, N = bufs["skey_global"]
+        spilled = gn >= N
+        hi = bufs["vmask_hi"][:nv]
+    else:
+        S2, N = int(off[-1]), len(off) - 1
+        spilled = kn >= N
+        kk, k0 = B.SLAB["v"]
+        hb0 = vb - (kk * S2 + k0 * N)
+        hi = bufs["vmask_hi"][hb0:hb0 + nv] if spilled else None
+    if spilled and hi is not None and len(hi):
+        mask |= hi.astype(np.uint64) << np.uint64(32)
     a = bufs["arc"][ab:ab + na]
     ids = a[:, 0].astype(np.int64)
-    a_int = np.stack([ids & 0xFF, (ids >> 8) & 0xFF, (ids >> 16) & 0xFF, ids >> 24], 1).astype(np.int32)
+    a_int = np.stack([ids & 63, (ids >> 6) & 63, (ids >> 12) & 1023, ids >> 22], 1).astype(np.int32)
     lh = bufs["loop_hdr"][off[n]:off[n] + d]
     loop_off = np.zeros(d + 1, np.int32)
     if d:
@@ -139,15 +187,15 @@ def decode_node(bufs: dict, n: int) -> dict:
         hole_off[nh] = hh[-1, 0] + hh[-1, 1]
     he = bufs["hole_ent"][heb:heb + nhe]
     return dict(
-        status=status, d=d, nv=nv, na=na, nh=nh,
-        v_mask=v[:, 3].copy().view(np.uint32), v_pos32=v[:, :3].copy(),
+        status=status, d=d, nv=nv, na=na, nh=nh, spilled=bool(spilled),
+        v_mask=mask, v_pos32=v[:, :3].copy(),
         a_int=a_int, a_f32=a[:, 1:12].copy().view(np.float32),
         loop_off=loop_off,
         l_int=np.stack([le[:, 0] & 0xFFFF, (le[:, 0] >> 16) & 1], 1).astype(np.int32),
         l_N=(le[:, 0] >> 17).astype(np.int32),
         l_f32=le[:, 1:3].copy().view(np.float32),
-        l_cum=(le[:, 3] & 0xFFFFFF).astype(np.int32),
-        l_vid=(le[:, 3] >> 24).astype(np.int32),
+        l_cum=(le[:, 3] & 0x3FFFFF).astype(np.int32),
+        l_vid=(le[:, 3] >> 22).astype(np.int32),
         hole_off=hole_off,
         h_int=np.stack([he[:, 0] & 0xFFFF, (he[:, 0] >> 16) & 1], 1).astype(np.int32),
     )

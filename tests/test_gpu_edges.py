@@ -1,6 +1,7 @@
-"""Edge cases of the CUDA path through the C-ABI: empty and degenerate inputs, the
-maximum supported node degree (31) and one past it, isolated nodes, ragged sizes,
-argument and state errors (fail loudly, never silently)."""
+"""Edge cases of the CUDA path through the C-ABI: empty and degenerate inputs, node degrees
+across the bucket limit (31) up to the model's limit (63) and one past it, nodes whose
+junctions / vertices / arcs exceed their degree bucket's workspace (the spill kernel),
+isolated nodes, ragged sizes, argument and state errors (fail loudly, never silently)."""
 import numpy as np
 import pytest
 
@@ -68,17 +69,20 @@ def test_isolated_nodes_next_to_struts():
     mm.close()
 
 
-def test_max_degree_31_parity():
-    lat = synth.star(_fib_dirs(31), 1.0, 0.05)
+@pytest.mark.parametrize("k", [31, 32, 40, 63])
+def test_high_degree_star_parity(k):
+    """Degree 31 is the last degree bucket; 32..63 go to the spill kernel (Sec. 4.3.3:
+    "multiple warps to meta-mesh a single strut"): bit-exact with the oracle, no error node."""
+    lat = synth.star(_fib_dirs(k), 1.0, 0.05)
     mm, _, T = _full_parity(lat)
     assert mm.stats()["n_error_nodes"] == 0 and T > 0
     mm.close()
 
 
-def test_degree_32_is_flagged_like_the_oracle():
-    """One past the supported degree: the node gets status 1 (degree > 31) on both sides;
+def test_degree_64_is_flagged_like_the_oracle():
+    """One past the model's limit (sides 0..63 in one 64-bit tie mask): status 1 on both sides;
     its struts contribute no band, the far nodes still get their meta-mesh."""
-    lat = synth.star(_fib_dirs(32), 1.0, 0.05)
+    lat = synth.star(_fib_dirs(64), 1.0, 0.05)
     mm, orc, T = _full_parity(lat)
     st = mm.stats()
     assert st["n_error_nodes"] == 1 and st["err_hist"][1] == 1
@@ -127,16 +131,65 @@ def test_errors_are_loud():
     mm.close()
 
 
-@pytest.mark.parametrize("k", [8, 11, 12, 16])
-def test_umbrella_vertex_capacity_like_the_oracle(k):
+@pytest.mark.parametrize("k", [8, 11, 12, 16, 24])
+def test_umbrella_vertex_any_valence(k):
     """k struts on a cone around an axis meet in ONE k-valent vertex (C(k, 3) junctions at a
-    point): representable up to the junction capacity of the degree class (R13),
-    flagged JCAP beyond it -- identically by kernel and oracle."""
+    point).  Beyond the junction workspace of the node's degree bucket the node goes to the
+    spill kernel: 0 error nodes, bit-exact with the oracle, for every k."""
     d = [[np.sin(1.0) * np.cos(t), np.sin(1.0) * np.sin(t), np.cos(1.0)] for t in np.linspace(0, 2 * np.pi, k, endpoint=False)]
     lat = synth.star(d, 1.0, 0.05)
     mm, orc, T = _full_parity(lat)
-    st = mm.stats()
-    assert st["n_error_nodes"] == (1 if k >= 12 else 0)
+    assert mm.stats()["n_error_nodes"] == 0
+    assert orc.node(0)["nv"] == k + 1          # the apex plus k sphere junctions around the hole
+    mm.close()
+
+
+def _cone_star(dirs, R, r_far, name):
+    """A hub of sphere radius R whose struts narrow to r_far at unit length (strongly conical)."""
+    dirs = np.asarray(dirs, float)
+    dirs /= np.linalg.norm(dirs, axis=1)[:, None]
+    xyz = np.concatenate([[[0.0, 0.0, 0.0]], dirs]).astype(np.float32)
+    r = np.concatenate([[R], [r_far] * len(dirs)]).astype(np.float32)
+    ends = np.array([[0, i + 1] for i in range(len(dirs))], np.int64)
+    return synth.Lattice(xyz, ends, r, name)
+
+
+@pytest.mark.parametrize("shape,R,holes", [("tet", 0.5, 4), ("tet", 0.6, 4), ("oct", 0.65, 8), ("oct", 0.68, 8)])
+def test_many_hole_short_cone_nodes(shape, R, holes):
+    """Short, strongly tapered struts whose end circles cut the nodal sphere into several
+    exposed regions (4 holes at a tetrahedral hub, 8 at an octahedral one): more vertices
+    than the bucket's vertex slab holds (2d + 2), so the node is meta-meshed by the spill
+    kernel into an overflow slab slot.  Bit-exact with the oracle, watertight output."""
+    dirs = {"tet": [[1, 1, 1], [1, -1, -1], [-1, 1, -1], [-1, -1, 1]],
+            "oct": [[1, 0, 0], [-1, 0, 0], [0, 1, 0], [0, -1, 0], [0, 0, 1], [0, 0, -1]]}[shape]
+    lat = _cone_star(dirs, R, 0.05, f"{shape}-cone{R}")
+    mm, orc, T = _full_parity(lat)
+    assert mm.stats()["n_error_nodes"] == 0
+    assert orc.node(0)["nh"] == holes
+    from test_gpu_parity import _mesh_edges_ok
+    counts, chi = _mesh_edges_ok(mm.triangles(0, T))
+    assert counts == {2} and chi == 2
+    mm.close()
+
+
+def test_spill_mixed_with_buckets():
+    """Spilled hubs next to ordinary bucketed nodes in one lattice: the bands of struts between
+    a spilled node and a regular node join the overflow slab slot with the regular one."""
+    hubs = []
+    xyz, ends, r = [], [], []
+    for h, (k, base) in enumerate([(40, (0, 0, 0)), (12, (5, 0, 0)), (33, (10, 0, 0))]):
+        c = len(xyz)
+        xyz.append(base)
+        r.append(0.05)
+        for u in _fib_dirs(k):
+            ends.append((c, len(xyz)))
+            xyz.append(tuple(np.asarray(base) + u))
+            r.append(0.05)
+    # join hub 0's and hub 1's neighbourhoods with a strut between two leaves
+    ends.append((1, 42))
+    lat = synth.Lattice(np.array(xyz, np.float32), np.array(ends, np.int64), np.array(r, np.float32), "hubs")
+    mm, orc, T = _full_parity(lat)
+    assert mm.stats()["n_error_nodes"] == 0
     mm.close()
 
 

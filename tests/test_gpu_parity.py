@@ -112,8 +112,7 @@ def _triangulation_parity(built, name, ce):
     tri = mm.triangles(0, T).astype(np.float64)
     ref = orc.write_triangles()
     r = float(lat.node_r.min())
-    tol = GEOM_TOL * r + 4e-7 * np.abs(ref[:, 1:]).max()
-    assert np.max(np.abs(tri[:, 1:] - ref[:, 1:])) < tol
+    assert_triangles_close(tri, ref, r, (name, ce))
     # facet normals agree wherever the facet is not tiny
     # facet normals: error bounded by vertex error / shortest altitude
     v1, v2, v3 = ref[:, 1], ref[:, 2], ref[:, 3]
