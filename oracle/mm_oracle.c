@@ -592,7 +592,7 @@ static void work_free(work_t *w) {
   free(w->Q); free(w->tq); free(w->us); free(w->uc);
 }
 
-static int node_metamesh(orc_lat *L, int64_t n) {
+static int node_metamesh_at(orc_lat *L, int64_t n, int level) {
   node_mm *M = &L->mm[n];
   node_free(M);
   M->done = 1;
@@ -605,7 +605,7 @@ static int node_metamesh(orc_lat *L, int64_t n) {
   if (st != ORC_OK) { M->status = st; return st; }
   if (d == 0) return ORC_OK;
   real R = L->rad[n];
-  real delta = TOL_REL * R, dc = CTOL_REL * R;
+  real delta = TOL_REL * R, dc = (CTOL_REL * R) * (real)(1 << level);
   work_t W;
   memset(&W, 0, sizeof W);
 #define FAIL(code) do { work_free(&W); M->status = (code); return M->status; } while (0)
@@ -928,6 +928,19 @@ static int node_metamesh(orc_lat *L, int64_t n) {
 #undef FAIL
 }
 
+#ifndef ORC_MAX_LEVEL
+#define ORC_MAX_LEVEL 4
+#endif
+static int node_metamesh(orc_lat *L, int64_t n) {
+  int st = ORC_OK;
+  for (int level = 0; level <= ORC_MAX_LEVEL; level++) {
+    st = node_metamesh_at(L, n, level);
+    if (!(st == ORC_E_CHAIN || st == ORC_E_HOLE || st == ORC_E_UNREF || st == ORC_E_ANGLE || st == ORC_E_EMPTY)) break;
+    if (getenv("ORC_DEBUG")) fprintf(stderr, "node %lld: status %d at level %d\n", (long long)n, st, level);
+  }
+  return st;
+}
+
 /* compute the meta-mesh of selected nodes (nodes == NULL: all); a node in error keeps
  * only its status (no partial topology) */
 int orc_metamesh(orc_lat *L, const int64_t *nodes, int64_t n_sel) {
@@ -962,8 +975,20 @@ static uint64_t node_topo_hash(const node_mm *M) {
     const arc_t *E = &M->a[i];
     h = fnv(h, (uint64_t)E->lo | ((uint64_t)E->hi << 16) | ((uint64_t)E->vs << 32) | ((uint64_t)E->ve << 48));
   }
+  /* loops as cyclic sequences (their first entry, the smallest angle around the strut axis,
+   * is a representation choice that flips where a vertex sits at angle 0): each rotated to
+   * start at its lowest arc index */
   for (int k = 0; k <= M->d; k++) h = fnv(h, (uint64_t)M->loop_off[k]);
-  for (int i = 0; i < M->loop_off[M->d]; i++) h = fnv(h, (uint64_t)M->le[i].arc | ((uint64_t)M->le[i].fwd << 32));
+  for (int k = 0; k < M->d; k++) {
+    const int b = M->loop_off[k], e = M->loop_off[k + 1], c = e - b;
+    int r = 0;
+    for (int i = 1; i < c; i++)
+      if (M->le[b + i].arc < M->le[b + r].arc) r = i;
+    for (int i = 0; i < c; i++) {
+      const loop_t *x = &M->le[b + (r + i) % c];
+      h = fnv(h, (uint64_t)x->arc | ((uint64_t)x->fwd << 32));
+    }
+  }
   for (int k = 0; k <= M->nh; k++) h = fnv(h, (uint64_t)(M->nh ? M->hole_off[k] : 0));
   int nhe = M->nh ? M->hole_off[M->nh] : 0;
   for (int i = 0; i < nhe; i++) h = fnv(h, (uint64_t)M->he[i].arc | ((uint64_t)M->he[i].fwd << 32));
@@ -1215,7 +1240,9 @@ int64_t orc_triangulate(orc_lat *L, double ce) {
       int tot = hole_ring(L, n, h, &P, &bp);
       free(P);
       int64_t g = L->hole_base[n] + h;
-      L->hole_M[g] = tot;
+      /* a contour of two points (a lune of two one-segment arcs) has coincident chords: it
+       * encloses no area at this chord error and gets no fan (reading R7) */
+      L->hole_M[g] = tot == 2 ? 0 : tot;
       L->hole_bp[g] = bp;
     }
   }
@@ -1262,6 +1289,7 @@ int64_t orc_node_hole_triangles(const orc_lat *L, int64_t n, double *out) {
   for (int h = 0; h < M->nh; h++) {
     d3 *P, bp;
     int tot = hole_ring(L, n, h, &P, &bp);
+    if (tot == 2) { free(P); continue; }   /* flat lune: no fan (as orc_triangulate) */
     d3 apex = d_add(on, bp);
     for (int i = 0; i < tot; i++) {
       if (out) tri_out(out + 12 * cnt, apex, d_add(on, P[i]), d_add(on, P[(i + 1) % tot]));

@@ -12,6 +12,7 @@
 #define LMM_MAXD 31         // degree-bucketed kernels (metamesh.cu): sides 0..31 in 32-bit masks
 #define LMM_MAXD_SPILL 63   // spill kernel (spill.cu): sides 0..63 in 64-bit masks
 #define LMM_NODE_SPILL 0xfe // internal node status: left for the spill kernel (never reported)
+#define LMM_MAX_LEVEL 4     // vertex resolution delta_c 2^level, level 0..4 (reading R10)
 #define LMM_TOL_REL 1e-4f   // delta   = TOL * R  : tie tolerance
 #define LMM_CTOL_REL 1e-3f  // delta_c = CTOL * R : vertex clustering radius
 #define LMM_PI_F 3.14159265358979324f

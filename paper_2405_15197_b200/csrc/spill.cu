@@ -46,6 +46,7 @@ struct SpillParams {
   const int *csr_off;
   const int2 *csr_ent;
   const int *list;
+  const int *level;                // first vertex-resolution level of each listed node
   int n_list;
   int4 *node_hdr;
   int2 *skey;
@@ -158,7 +159,7 @@ struct TEnt { float t0, dt, tmid; int vs, ve; };  // an interval of a conic
 __device__ __forceinline__ int ceil_div_pos(int x, int k) { return x <= 0 ? 0 : (x + k - 1) / k; }
 
 // the meta-mesh of node n; returns its status (0 = ok).  `need` > 0 on workspace shortage.
-__device__ int spill_node(const SpillParams &P, SpillWS &ws, int n, int64_t *need) {
+__device__ int spill_node(const SpillParams &P, SpillWS &ws, int n, int level, int64_t *need) {
   __shared__ int sm[NW + 2];
   __shared__ int sm1;
   __shared__ unsigned long long smo;
@@ -170,7 +171,8 @@ __device__ int spill_node(const SpillParams &P, SpillWS &ws, int n, int64_t *nee
   const int d = P.csr_off[n + 1] - off;
   const float4 on = P.node[n];
   const float R = on.w;
-  const float delta = LMM_TOL_REL * R, dc = LMM_CTOL_REL * R;
+  // vertex resolution of this attempt: delta_c 2^level (reading R10, re-decision)
+  const float delta = LMM_TOL_REL * R, dc = (LMM_CTOL_REL * R) * (float)(1 << level);
   const int ns = d + 1;
   Carve cv{P.ws + (int64_t)blockIdx.x * P.wsb, P.wsb};
   *need = 0;
@@ -640,12 +642,22 @@ __device__ int spill_node(const SpillParams &P, SpillWS &ws, int n, int64_t *nee
   return 0;
 }
 
+// a decided topology that is not a closed cell complex: re-decide at a coarser vertex resolution
+__device__ __forceinline__ bool retry_status(int st) {
+  return st == LMM_NODE_CHAIN || st == LMM_NODE_HOLE || st == LMM_NODE_UNREF || st == LMM_NODE_ANGLE || st == LMM_NODE_EMPTY;
+}
+
 __global__ void __launch_bounds__(ST, 1) k_spill(SpillParams P) {
   __shared__ SpillWS ws;
   for (int i = blockIdx.x; i < P.n_list; i += gridDim.x) {
     const int n = P.list[i];
     int64_t need = 0;
-    const int st = spill_node(P, ws, n, &need);
+    int st = 0;
+    for (int level = P.level[i]; level <= LMM_MAX_LEVEL; level++) {
+      st = spill_node(P, ws, n, level, &need);
+      __syncthreads();
+      if (need > 0 || !retry_status(st)) break;
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
       if (need > 0) atomicMax(&P.ctl[1], (unsigned long long)need);
@@ -662,14 +674,19 @@ __global__ void __launch_bounds__(ST, 1) k_spill(SpillParams P) {
   }
 }
 
-// nodes left for the spill kernel: capacity refusals of the buckets and degrees 32..63
-__global__ void k_spill_list(const int4 *node_hdr, int64_t N, int *list, unsigned long long *ctl) {
+// nodes left for the spill kernel: capacity refusals of the buckets and degrees 32..63 (from
+// vertex resolution level 0), and bucketed nodes whose level-0 topology did not close (from level 1)
+__global__ void k_spill_list(const int4 *node_hdr, int64_t N, int *list, int *level, unsigned long long *ctl) {
   const int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (n >= N) return;
   const int st = node_hdr[n].x & 0xff;
-  const bool sp = st == LMM_NODE_JCAP || st == LMM_NODE_CCAP || st == LMM_NODE_ACAP || st == LMM_NODE_QCAP ||
-                  st == LMM_NODE_SPILL;
-  if (sp) list[atomicAdd(&ctl[3], 1ull)] = (int)n;
+  const bool cap = st == LMM_NODE_JCAP || st == LMM_NODE_CCAP || st == LMM_NODE_ACAP || st == LMM_NODE_QCAP ||
+                   st == LMM_NODE_SPILL;
+  if (cap || retry_status(st)) {
+    const int i = (int)atomicAdd(&ctl[3], 1ull);
+    list[i] = (int)n;
+    level[i] = cap ? 0 : 1;
+  }
 }
 
 __global__ void k_skey_init(const int *csr_off, int64_t N, int2 *skey) {
@@ -695,10 +712,11 @@ int spill_run(lmm_ctx *c) {
   if (!N) return LMM_OK;
   int rc;
   if ((rc = dev_alloc(c->spill_ctl, sizeof(unsigned long long) * 8))) return rc;
-  if ((rc = dev_alloc(c->spill_list, sizeof(int) * (N + 1)))) return rc;
+  if ((rc = dev_alloc(c->spill_list, sizeof(int) * 2 * (N + 1)))) return rc;
+  int *list = (int *)c->spill_list.p, *lvl = list + (N + 1);
   unsigned long long *ctl = (unsigned long long *)c->spill_ctl.p;
   CUDA_TRY(cudaMemsetAsync(ctl, 0, sizeof(unsigned long long) * 8, c->stream));
-  (c->n_launch++), k_spill_list<<<(unsigned)((N + 255) / 256), 256, 0, c->stream>>>((const int4 *)c->node_hdr.p, N, (int *)c->spill_list.p, ctl);
+  (c->n_launch++), k_spill_list<<<(unsigned)((N + 255) / 256), 256, 0, c->stream>>>((const int4 *)c->node_hdr.p, N, list, lvl, ctl);
   CUDA_TRY(cudaGetLastError());
   if (!c->pinned_scalar) CUDA_TRY(cudaMallocHost((void **)&c->pinned_scalar, 64));
   unsigned long long *h = (unsigned long long *)(c->pinned_scalar + 4);   // 4 words
@@ -716,7 +734,8 @@ int spill_run(lmm_ctx *c) {
     P.node = (const float4 *)c->node.p;
     P.csr_off = (const int *)c->csr_off.p;
     P.csr_ent = (const int2 *)c->csr_ent.p;
-    P.list = (const int *)c->spill_list.p;
+    P.list = list;
+    P.level = lvl;
     P.n_list = (int)ns;
     P.node_hdr = (int4 *)c->node_hdr.p;
     P.skey = (int2 *)c->skey.p;

@@ -353,7 +353,9 @@ __global__ void k_hole_count(TriParams P) {
     float nl = n2 > 0.0f ? rsqrtf(n2) : 0.0f;   // a contour without area keeps Eq. 13's b - o
     float dx = (p0.x + bx * inv) + R * nx * nl, dy = (p0.y + by * inv) + R * ny * nl, dz = (p0.z + bz * inv) + R * nz * nl;
     float dl = R * rsqrtf(dx * dx + dy * dy + dz * dz);
-    P.hole_M[g] = M;
+    // a contour of two points (a lune of two one-segment arcs: coincident chords) encloses no
+    // area at this chord error and gets no fan (reading R7)
+    P.hole_M[g] = M == 2 ? 0 : M;
     P.hole_bp[g] = make_float4(dx * dl, dy * dl, dz * dl, 0.0f);
     P.hole_node[g] = (int)n;
   }

@@ -193,6 +193,25 @@ def test_spill_mixed_with_buckets():
     mm.close()
 
 
+def test_redecided_stars_parity():
+    """tests/golden/stoch290_redecided_stars.json: the configs[2] nodes whose topology closes
+    only at a coarser vertex resolution (reading R10): the kernel re-decides them
+    exactly like the oracle (spill kernel, levels 1..4), 0 error nodes, watertight output."""
+    import json
+    import os
+    from test_gpu_parity import _mesh_edges_ok
+    J = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "stoch290_redecided_stars.json")))
+    for st in J["stars"]:
+        lat = synth.Lattice(np.array(st["xyz"], np.float32), np.array(st["ends"], np.int64),
+                            np.array(st["r"], np.float32), f"star{st['node']}")
+        for ce in (1e-2, 1e-3):
+            mm, orc, T = _full_parity(lat, ce)
+            assert mm.stats()["n_error_nodes"] == 0, st["node"]
+            counts, chi = _mesh_edges_ok(mm.triangles(0, T))
+            assert counts == {2} and chi == 2, (st["node"], ce)
+            mm.close()
+
+
 def test_index_region_worked_example():
     """PAPER.md Sec. 4.3.2: an index region [0, 5, 15, 32, 47, ...] is the exclusive prefix sum of
     per-item counts 5, 10, 17, 15.  Four hub nodes of degree 5, 10, 17 and 15 (ids 0-3, leaves

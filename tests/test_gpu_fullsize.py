@@ -14,7 +14,9 @@ one (orc_metamesh on a node subset; a band needs only its two end nodes):
     the bench-sized device chunk that holds them) within tolerance;
   * sampled hole fans of boundary nodes: triangle counts exact, triangles within tolerance;
 and properties that hold at any size are checked on the whole output: offsets are the
-exclusive prefix sums of the band / hole sizes, no node in error, totals consistent.
+exclusive prefix sums of the band / hole sizes, no node in error, every strut has its band,
+totals consistent; and sampled neighbourhoods (a node's fans + all its bands) are welded
+and checked watertight (manifold, oriented, bounded only by the far-end rings).
 """
 import numpy as np
 import pytest
@@ -70,27 +72,74 @@ def test_fullsize_whole_output_properties(full):
     lat, mm, T, orc, _ = full
     st = mm.stats()
     assert st["n_struts"] == lat.n_struts and st["n_nodes"] == lat.n_nodes
-    # nodes the model cannot represent (status != 0) must be the oracle's too
+    # every node the model defines is meshed: no node in error, so every strut has its band
     bad = _error_nodes(mm)
-    assert len(bad) == st["n_error_nodes"] and len(bad) <= 1e-6 * lat.n_nodes
-    if len(bad):
-        assert orc.metamesh(bad) == len(bad)
-        tol = 1e-4 * float(lat.node_r.min())
-        from paper_2405_15197_b200 import decode_node
-        for n in bad:
-            assert_node_parity(decode_node(mm.node_buffers(int(n)), 0), orc.node(int(n)), tol, int(n))
+    assert len(bad) == st["n_error_nodes"]
+    if len(bad):        # diagnose before failing: the oracle must agree on each of them
+        orc.metamesh(bad)
+        print("error nodes:", [(int(n), orc.node(int(n))["status"]) for n in bad[:20]])
+    assert len(bad) == 0, (len(bad), st["err_hist"])
     tb = mm.tri_buffers()
     band = tb["band"].astype(np.int64)
     soff = tb["strut_off"]
     assert soff[0] == 0 and np.array_equal(np.diff(soff), band[:, 0] + band[:, 1])
-    ok = ~np.isin(lat.ends, bad).any(axis=1)          # struts with both end nodes representable
-    assert np.all(band[ok, 0] > 0) and np.all(band[ok, 1] > 0)
-    assert np.all(band[~ok, :2] == 0)
+    assert np.all(band[:, 0] > 0) and np.all(band[:, 1] > 0)
     hoff = tb["hole_off"]                             # hole offsets follow the bands
     assert hoff[0] == 0 and np.array_equal(np.diff(hoff), tb["hole_M"].astype(np.int64))
     assert soff[-1] + hoff[-1] == T
     h0 = tb["node_hole0"]
     assert h0[0] == 0 and np.all(np.diff(h0) >= 0) and h0[-1] == len(tb["hole_M"])
+
+
+N_NEIGH_SAMPLE = 400
+
+
+def test_fullsize_sampled_neighbourhoods_watertight(full):
+    """Watertightness at full size, in the bench launch configuration: for sampled nodes (random
+    and every degree class) the patch of the node's hole fans plus the whole bands of all its
+    struts, welded by exact binary32 coordinates, is a manifold, consistently oriented surface
+    whose only boundary is the far-end rings of its bands (one closed ring per strut).  Every
+    seam of the mesh (band-band along a shared arc, band-fan, shared vertices) lies around some
+    node, so the samples cover every kind of seam."""
+    lat, mm, T, orc, out = full
+    rng = np.random.default_rng(77)
+    deg = lat.degrees()
+    pick = [rng.choice(np.flatnonzero(deg > 0), N_NEIGH_SAMPLE, replace=False)]
+    for d in np.unique(deg[deg > 0]):
+        idx = np.flatnonzero(deg == d)
+        pick.append(rng.choice(idx, min(4, len(idx)), replace=False))
+    nodes = np.unique(np.concatenate(pick))
+    tb = mm.tri_buffers()
+    band, soff = tb["band"].astype(np.int64), tb["strut_off"]
+    hoff, h0 = tb["hole_off"], tb["node_hole0"]
+    nTb = int(soff[-1])
+    inc = {}
+    for n in nodes:
+        inc[int(n)] = np.flatnonzero((lat.ends[:, 0] == n) | (lat.ends[:, 1] == n))
+    # every requested record range, fetched in output order through the bench-sized chunks
+    req = []
+    for n, ss in inc.items():
+        for s_ in ss:
+            req.append((int(soff[s_]), int(soff[s_ + 1] - soff[s_]), n))
+        a, b = nTb + int(hoff[h0[n]]), nTb + int(hoff[h0[n + 1]])
+        if b > a:
+            req.append((a, b - a, n))
+    got = {n: [] for n in inc}
+    cache = {}
+    for first, cnt, n in sorted(req):
+        got[n].append(_chunk_records(mm, out, T, first, cnt, cache))
+    for n, ss in inc.items():
+        tris = np.concatenate(got[n])
+        V = tris[:, 1:, :].reshape(-1, 3)
+        _, inv = np.unique(V, axis=0, return_inverse=True)
+        F = inv.reshape(-1, 3)
+        e = np.concatenate([F[:, [0, 1]], F[:, [1, 2]], F[:, [2, 0]]])
+        und, cnt = np.unique(np.sort(e, axis=1), axis=0, return_counts=True)
+        _, dcnt = np.unique(e, axis=0, return_counts=True)
+        assert set(cnt.tolist()) <= {1, 2}, (n, set(cnt.tolist()))
+        assert not np.any(dcnt > 1), n                      # seams traversed in opposite directions
+        far = np.where(lat.ends[ss, 0] == n, band[ss, 1], band[ss, 0])   # far-end ring sizes
+        assert int((cnt == 1).sum()) == int(far.sum()), (n, int((cnt == 1).sum()), int(far.sum()))
 
 
 def test_fullsize_sampled_nodes(full):

@@ -480,3 +480,86 @@ def test_emitted_arc_chords_within_chord_error(oracle_mod, ce):
                 dev = np.linalg.norm(w - np.outer(lam, seg), axis=1).max()
                 worst = max(worst, dev / (ce * semi))
     assert 0.5 < worst <= 1.0 + 1e-6   # tight: some segment comes close to the bound
+
+
+# ---------------------------------------------------------------------------------------
+# the binary32 decision specification against binary64 decisions
+# ---------------------------------------------------------------------------------------
+def _pin_lattices():
+    """~130k nodes of every generator family, near the origin (binary32 positions resolve
+    1e-7 relative), including the sharp-angle family (struts down to 10 deg apart)."""
+    return [synth.stochastic(28, seed=11), synth.stochastic(28, seed=12),
+            synth.stochastic(28, seed=13, min_angle_deg=10.0), synth.stochastic(24, seed=14, min_angle_deg=10.0),
+            synth.jitter(synth.graded_radii(synth.octet(12, 12, 12), 0.02, 0.06, 0), 0.05, 15),
+            synth.jitter(synth.graded_radii(synth.bcc(16, 16, 16), 0.03, 0.07, 2), 0.08, 16),
+            synth.graded_radii(synth.octet(10, 10, 10), 0.03, 0.06, 1), synth.bcc(14, 14, 14)]
+
+
+def _scan_worker(args):
+    import oracle as O
+    lat, bits, eps, seed = args
+    orc = O.Oracle.from_lattice(lat, bits)
+    if eps:
+        orc.set_jitter(eps, seed)
+    st, hs = orc.scan(np.arange(lat.n_nodes, dtype=np.int64))
+    return st, hs
+
+
+@pytest.mark.slow
+def test_binary32_topology_equals_binary64_away_from_ties(oracle_mod):
+    """Every node's topology (counts, tie masks, arc sides/endpoints, loop order, hole
+    contours) decided with the binary32 specification equals the topology decided by the
+    same algorithm with every decision in binary64 and libm atan2 (liborc64), except on
+    nodes whose binary64 topology itself changes under a seeded relative jitter of 4e-6 of
+    the side parameters (near ties; counted and bounded).  Pins the binary32 operation order
+    (fused multiply-adds, reciprocals) against an independent precision: a decision the spec
+    got wrong by more than rounding shows up as a mismatch on a stable node."""
+    import multiprocessing as mp
+    lats = _pin_lattices()
+    jobs = []
+    for lat in lats:
+        jobs += [(lat, 32, 0.0, 0), (lat, 64, 0.0, 0)] + [(lat, 64, 4e-6, s) for s in (1, 2, 3)]
+    with mp.get_context("fork").Pool(min(8, os.cpu_count() or 1)) as pool:
+        res = pool.map(_scan_worker, jobs)
+    total = stable = mism = unstable = 0
+    for i, lat in enumerate(lats):
+        (st32, h32), (st64, h64), *jit = res[5 * i:5 * i + 5]
+        stab = np.ones(lat.n_nodes, bool)
+        for _, hj in jit:
+            stab &= hj == h64
+        bad = stab & (h32 != h64)
+        total += lat.n_nodes
+        stable += int(stab.sum())
+        unstable += int((~stab).sum())
+        mism += int(bad.sum())
+        assert not bad.any(), (lat.name, np.flatnonzero(bad)[:10], st32[bad][:10], st64[bad][:10])
+    assert total >= 100_000
+    assert unstable <= 0.01 * total, (unstable, total)
+    print(f"binary32 vs binary64 topology: {total} nodes, {stable} stable and identical, {unstable} near ties")
+
+
+def _golden_stars(name):
+    J = json.load(open(os.path.join(GOLD, name)))
+    out = []
+    for st in J["stars"]:
+        out.append((st["node"], synth.Lattice(np.array(st["xyz"], np.float32), np.array(st["ends"], np.int64),
+                                              np.array(st["r"], np.float32), f"star{st['node']}")))
+    return out
+
+
+@pytest.mark.parametrize("ce", [1e-2, 1e-3])
+def test_redecided_stars_close_watertight(oracle_mod, ce):
+    """tests/golden/stoch290_redecided_stars.json: the 7 nodes of configs[2] (stoch290) whose
+    topology at vertex resolution delta_c does not close (tiny hole triangles partly clustered,
+    a thin hole band between nearly coincident end circles).  Re-decided at a coarser
+    resolution (reading R10) every one meshes, and each star (hub + its struts, a
+    tree) triangulates watertight, manifold, oriented, chi = 2 (reading R7: flat 2-point
+    hole contours get no fan)."""
+    for node, lat in _golden_stars("stoch290_redecided_stars.json"):
+        orc = oracle_mod.Oracle.from_lattice(lat)
+        assert orc.metamesh() == 0, node
+        orc.triangulate(ce)
+        inv = mesh_invariants(orc.write_triangles())
+        assert inv["edge_counts"] == {2} and inv["directed_dups"] == 0, (node, inv)
+        assert inv["chi"] == 2 and inv["degenerate"] == 0, (node, inv)
+        assert inv["volume"] > 0, node
