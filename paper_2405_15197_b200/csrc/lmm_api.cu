@@ -188,14 +188,21 @@ LMM_API int lmm_load_lattice(lmm_ctx *c, const float *xyz, int64_t n_nodes, cons
     de = (const int64_t *)p;
     dx = (const float *)(p + be);
     dr = (const float *)(p + be + bx);
-    if (n_struts) CUDA_TRY(cudaMemcpyAsync((void *)de, ends, be, cudaMemcpyHostToDevice, c->stream));
-    if (n_nodes) CUDA_TRY(cudaMemcpyAsync((void *)dx, xyz, bx, cudaMemcpyHostToDevice, c->stream));
-    if (n_struts) CUDA_TRY(cudaMemcpyAsync((void *)dr, r_end, br, cudaMemcpyHostToDevice, c->stream));
+    // every exit below frees the staging copy (stream-ordered after the copies)
+    cudaError_t e = cudaSuccess;
+    if (n_struts && e == cudaSuccess) e = cudaMemcpyAsync((void *)de, ends, be, cudaMemcpyHostToDevice, c->stream);
+    if (n_nodes && e == cudaSuccess) e = cudaMemcpyAsync((void *)dx, xyz, bx, cudaMemcpyHostToDevice, c->stream);
+    if (n_struts && e == cudaSuccess) e = cudaMemcpyAsync((void *)dr, r_end, br, cudaMemcpyHostToDevice, c->stream);
+    if (e != cudaSuccess) {
+      cudaFreeAsync(tmp, c->stream);
+      cudaStreamSynchronize(c->stream);
+      return LMM_E_CUDA;
+    }
   }
   c->has_node_mask = c->has_strut_mask = false;
   int rc = lattice_build(c, dx, de, dr);
   if (tmp) cudaFreeAsync(tmp, c->stream);
-  if (rc) return rc;
+  if (rc) { cudaStreamSynchronize(c->stream); return rc; }
   c->lattice_ok = true;
   return LMM_OK;
 }
@@ -270,7 +277,9 @@ LMM_API int lmm_set_emit_mask(lmm_ctx *c, const uint8_t *node_mask, const uint8_
 }
 
 LMM_API int lmm_triangulate(lmm_ctx *c, double ce, int64_t *n_tri) {
-  if (!c || !(ce > 0.0) || !(ce <= 1.0)) return LMM_E_ARG;
+  // CE >= 1e-8: an arc's subdivision count N (< 2 pi / theta0 + 1) fits the 15 bits of the
+  // loop entry (theta0 = 2 acos(1 - CE) > 2 pi / 32767 for CE > 4.6e-9)
+  if (!c || !(ce >= 1e-8) || !(ce <= 1.0)) return LMM_E_ARG;
   if (!c->mm_ok) return LMM_E_STATE;
   CUDA_TRY(cudaSetDevice(c->device));
   c->tri_ok = false;
@@ -310,19 +319,23 @@ LMM_API int lmm_write_triangles(lmm_ctx *c, int64_t first, int64_t count, void *
   unsigned char *dst = (unsigned char *)out;
   int b = 0;
   bool used[LMM_NSTAGE] = {};
-  for (int64_t t = 0; t < count; t += CH, b = b + 1 == LMM_NSTAGE ? 0 : b + 1) {
+  rc = LMM_OK;
+  for (int64_t t = 0; t < count && rc == LMM_OK; t += CH, b = b + 1 == LMM_NSTAGE ? 0 : b + 1) {
     int64_t n = count - t < CH ? count - t : CH;
-    if (used[b]) CUDA_TRY(cudaStreamWaitEvent(c->stream, c->stage_ev[b], 0));   // buffer b copied out
-    if ((rc = triangulate_emit(c, first + t, n, c->stage[b].p, c->stream))) return rc;
-    CUDA_TRY(cudaEventRecord(c->emit_ev[b], c->stream));
-    CUDA_TRY(cudaStreamWaitEvent(c->copy_stream[b], c->emit_ev[b], 0));
-    CUDA_TRY(cudaMemcpyAsync(dst + t * 50, c->stage[b].p, (size_t)n * 50, cudaMemcpyDeviceToHost, c->copy_stream[b]));
-    CUDA_TRY(cudaEventRecord(c->stage_ev[b], c->copy_stream[b]));
+    // buffer b copied out before it is refilled
+    if (used[b] && cudaStreamWaitEvent(c->stream, c->stage_ev[b], 0) != cudaSuccess) { rc = LMM_E_CUDA; break; }
+    if ((rc = triangulate_emit(c, first + t, n, c->stage[b].p, c->stream))) break;
+    if (cudaEventRecord(c->emit_ev[b], c->stream) != cudaSuccess ||
+        cudaStreamWaitEvent(c->copy_stream[b], c->emit_ev[b], 0) != cudaSuccess ||
+        cudaMemcpyAsync(dst + t * 50, c->stage[b].p, (size_t)n * 50, cudaMemcpyDeviceToHost, c->copy_stream[b]) != cudaSuccess ||
+        cudaEventRecord(c->stage_ev[b], c->copy_stream[b]) != cudaSuccess) { rc = LMM_E_CUDA; break; }
     used[b] = true;
   }
-  for (int i = 0; i < LMM_NSTAGE; i++) CUDA_TRY(cudaStreamSynchronize(c->copy_stream[i]));
-  CUDA_TRY(cudaStreamSynchronize(c->stream));
-  return LMM_OK;
+  // on every exit no copy may still be writing into the caller's buffer
+  for (int i = 0; i < LMM_NSTAGE; i++)
+    if (cudaStreamSynchronize(c->copy_stream[i]) != cudaSuccess && rc == LMM_OK) rc = LMM_E_CUDA;
+  if (cudaStreamSynchronize(c->stream) != cudaSuccess && rc == LMM_OK) rc = LMM_E_CUDA;
+  return rc;
 }
 
 static DevBuf *buf_of(lmm_ctx *c, int id, size_t *bytes) {

@@ -1042,16 +1042,15 @@ int triangulate_emit(lmm_ctx *c, int64_t first, int64_t count, void *out_dev, cu
   {
     const int64_t live = c->S > 0 ? c->S : 1;
     const double mean = (double)c->n_tri_band / (double)live;
-    while (pcap < PCAP_MAX && mean + 2.0 > pcap - 4) pcap += 160;
+    while (pcap < PCAP_MAX && mean + 2.0 > pcap - 4) pcap = pcap + 160 < PCAP_MAX ? pcap + 160 : PCAP_MAX;
   }
   const size_t smem = (size_t)ring_bytes(pcap) * EW;
-  static bool attr_set = false;
-  static int occ_for[PCAP_MAX / 160 + 1] = {0};
-  if (!attr_set) {
+  // the opt-in shared-memory limit and the occupancy are per device: kept in the context
+  if (!c->emit_attr_set) {
     CUDA_TRY(cudaFuncSetAttribute(k_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, ring_bytes(PCAP_MAX) * EW));
-    attr_set = true;
+    c->emit_attr_set = true;
   }
-  int &occ = occ_for[pcap / 160];
+  int &occ = c->emit_occ[pcap == PCAP_MAX ? 7 : (pcap - PCAP_MIN) / 160];
   if (occ == 0) {
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_emit, EMIT_T, smem));
     if (occ < 1) occ = 1;

@@ -6,7 +6,10 @@ KEYS = ["Duration", "DRAM Throughput", "Memory Throughput", "Compute (SM) Throug
         "Registers Per Thread", "Dynamic Shared Memory Per Block", "Block Limit Registers", "Block Limit Shared Mem",
         "No Eligible", "Warp Cycles Per Issued Instruction", "L1/TEX Hit Rate", "L2 Hit Rate", "Grid Size", "Block Size"]
 RAW = ["dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum", "smsp__inst_executed.sum",
-       "smsp__thread_inst_executed.sum", "sm__warps_active.avg.pct_of_peak_sustained_active"]
+       "smsp__thread_inst_executed.sum", "sm__warps_active.avg.pct_of_peak_sustained_active",
+       "smsp__thread_inst_executed_per_inst_executed.ratio",
+       "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum", "l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum",
+       "l1tex__t_sectors_pipe_lsu_mem_global_op_st.sum", "l1tex__t_requests_pipe_lsu_mem_global_op_st.sum"]
 
 
 KFILTER = []
@@ -50,6 +53,20 @@ def main(rep, out, title, units=None, kernel=None):
         for k in RAW:
             if k in rd:
                 f.write(f"{k:40s} {rd[k]} {ru.get(k, '')}\n")
+        # north_star's meta-mesh evidence: global sectors per request (coalescing) and warp
+        # execution efficiency (active threads per executed instruction / 32)
+        for op in ("ld", "st"):
+            sk, rk = f"l1tex__t_sectors_pipe_lsu_mem_global_op_{op}.sum", f"l1tex__t_requests_pipe_lsu_mem_global_op_{op}.sum"
+            try:
+                sec, req = float(rd[sk].replace(",", "")), float(rd[rk].replace(",", ""))
+                f.write(f"global {op} sectors per request             {sec / req if req else 0:.2f}\n")
+            except (KeyError, ValueError):
+                pass
+        try:
+            r = float(rd["smsp__thread_inst_executed_per_inst_executed.ratio"].replace(",", ""))
+            f.write(f"warp execution efficiency                {100 * r / 32:.1f} %\n")
+        except (KeyError, ValueError):
+            pass
         if units:
             try:
                 rbytes = float(rd["dram__bytes_read.sum"]) * (1e9 if "G" in ru["dram__bytes_read.sum"] else 1e6)
