@@ -32,14 +32,15 @@ extern "C" LMM_API int lmm_debug_phase_cycles(unsigned long long *out) {
 namespace {
 using namespace mm;
 
-// per-bucket capacities <MAXS, MAXJ, MAXV, MAXA, MAXLE, MAXH> (degree 1-4, 5-8, 9-12, 13-16, 17-23, 24-31)
-// (MAXJ = the junction capacity of the degree class, reading R13, as the oracle's)
+// per-bucket workspace capacities <MAXS, MAXJ, MAXV, MAXA, MAXLE, MAXH> (degree 1-4, 5-8, 9-12, 13-16,
+// 17-23, 24-31), sized for occupancy: a node that needs more (e.g. many coincident junctions)
+// is meta-meshed by the spill kernel (spill.cu) -- the capacities never change a result
 #define LMM_B00_ARGS 5, 24, 10, 14, 28, 10
 #define LMM_B0_ARGS 9, 96, 18, 26, 52, 18
-#define LMM_B1_ARGS 13, 192, 26, 38, 76, 26
-#define LMM_B1b_ARGS 17, 240, 34, 50, 100, 34
-#define LMM_B2_ARGS 24, 336, 48, 71, 142, 48
-#define LMM_B3_ARGS 32, 448, 64, 95, 190, 64
+#define LMM_B1_ARGS 13, 96, 26, 38, 76, 26
+#define LMM_B1b_ARGS 17, 96, 34, 50, 100, 34
+#define LMM_B2_ARGS 24, 96, 48, 71, 142, 48
+#define LMM_B3_ARGS 32, 128, 64, 95, 190, 64
 
 struct MMParams {
   const float4 *node;

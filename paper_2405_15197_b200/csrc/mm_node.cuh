@@ -8,11 +8,16 @@
 namespace mm {
 
 // packed fp32 pairs (sm_100 add/mul .f32x2, round-to-nearest per lane)
+// (register-pair moves: no integer shifts between the packed operations)
 __device__ __forceinline__ unsigned long long f2u(float2 a) {
-  return (unsigned long long)__float_as_uint(a.x) | ((unsigned long long)__float_as_uint(a.y) << 32);
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a.x), "f"(a.y));
+  return r;
 }
 __device__ __forceinline__ float2 u2f(unsigned long long u) {
-  return make_float2(__uint_as_float((unsigned)u), __uint_as_float((unsigned)(u >> 32)));
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(u));
+  return r;
 }
 __device__ __forceinline__ float2 mul2(float2 a, float2 b) {
   unsigned long long r;
