@@ -59,12 +59,16 @@ def make_config(name: str, rank: int = 0, world: int = 1):
         desc = (f"BCC {n}x{n}x{n} cells per GPU (global {n}x{n}x{n * world}, {8 * n ** 3 * world / 1e9:.3f}B struts), "
                 f"uniform radius 0.05, pitch 1")
     elif fam == "stoch":
-        # configs[2]: stochastic Voronoi-style lattice, degrees 3..30, ~1e8 struts at n = 290; ranks
-        # get independent lattices (seed = rank), so there is nothing to exchange
-        lat = synth.stochastic(n, seed=rank)
-        masks = (None, None)
-        desc = (f"stochastic Voronoi-style lattice per GPU: jittered {n}^3 grid, Zipf target degrees 3-30, "
-                "cone radii U(0.02, 0.04), >=25 deg between struts at a node (synth.stochastic, seed = rank)")
+        # configs[2]: ONE stochastic Voronoi-style lattice, degrees 3..30, ~1e8 struts per GPU at n = 290,
+        # n x n x (n * world) nodes; rank r gets its z-slab plus a 4-layer halo (struts span up to 2
+        # layers, so the far ends of its struts see their whole neighbourhood)
+        k_top = n * world - 1
+        k_lo, k_hi = P.window(rank, world, k_top, halo=4) if world > 1 else (0, k_top)
+        lat = synth.stochastic_window(n, n * world, k_lo, k_hi, seed=0)
+        masks = P.emit_masks(lat.ijk[:, 2], lat.ends, rank, world, k_top) if world > 1 else (None, None)
+        desc = (f"stochastic Voronoi-style lattice {n}x{n}x{n} nodes per GPU (global {n}x{n}x{n * world}): jittered grid, "
+                "Zipf target degrees 3-30, cone radii U(0.02, 0.04), >=25 deg between struts at a node "
+                "(synth.stochastic_window: blocks of 10 layers + seams, spatially partitioned along z)")
     elif name == "bcc10":
         lat = synth.bcc(10, 10, 10)
         masks = (None, None)
@@ -140,7 +144,7 @@ def _sample_lattice(config: str, n: int):
         return synth.bcc(n, n, n), f"bcc {n}x{n}x{n}"
     if config.startswith("stoch"):
         side = int(round((n ** 3 * 8) ** (1 / 3)))
-        return synth.stochastic(side, seed=0), f"stochastic {side}^3"
+        return synth.stochastic_window(side, side, 0, side - 1, seed=0), f"stochastic {side}^3"
     return synth.graded_radii(synth.octet(n, n, n), 0.03, 0.06, axis=0), f"octet {n}x{n}x{n} graded"
 
 

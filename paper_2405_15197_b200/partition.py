@@ -23,7 +23,9 @@ def slab(rank: int, world: int, k_top: int):
 
 
 def window(rank: int, world: int, k_top: int, halo: int = 2):
-    """Inclusive z range [k_lo, k_hi] of rank's local lattice (slab + halo layers)."""
+    """Inclusive z range [k_lo, k_hi] of rank's local lattice (slab + halo layers).  The halo is
+    twice the z reach of a strut: 2 layers for the octet/BCC windows (struts span one layer),
+    4 for the stochastic lattice (struts span up to two)."""
     lo, hi = slab(rank, world, k_top)
     return max(0, lo - halo), min(k_top, hi - 1 + halo)
 

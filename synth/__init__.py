@@ -7,7 +7,7 @@ and the corresponding radii r_i^0, r_i^1").  Both `oracle/` and the product
 package may import it; it imports neither.
 """
 from .lattices import (Lattice, bcc, octet, octet_window, cubic, star, single_strut, chain,
-                       jitter, graded_radii, voronoi_like, bcc_slab, bcc_window, stochastic)
+                       jitter, graded_radii, voronoi_like, bcc_slab, bcc_window, stochastic, stochastic_window)
 
 __all__ = ["Lattice", "bcc", "octet", "octet_window", "cubic", "star", "single_strut", "chain",
-           "jitter", "graded_radii", "voronoi_like", "bcc_slab", "bcc_window", "stochastic"]
+           "jitter", "graded_radii", "voronoi_like", "bcc_slab", "bcc_window", "stochastic", "stochastic_window"]

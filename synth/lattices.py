@@ -279,6 +279,9 @@ def _stoch_lib():
         P = ctypes.c_void_p
         lib.stoch_struts.restype = ctypes.c_int64
         lib.stoch_struts.argtypes = [P, ctypes.c_int64, P, P, ctypes.c_double, ctypes.c_int64, P]
+        i64 = ctypes.c_int64
+        lib.stoch_zone.restype = i64
+        lib.stoch_zone.argtypes = [P, i64, i64, i64, i64, i64, P, P, ctypes.c_double, i64, P, P, i64, P]
         _STOCH_LIB = lib
     return _STOCH_LIB
 
@@ -344,4 +347,85 @@ def bcc_window(nx: int, ny: int, nz: int, k_lo: int, k_hi: int, pitch: float = 1
     lat = _finish(xyz, np.concatenate(ends), np.full(len(g), radius), f"bccwin{nx}x{ny}x{nz}[{k_lo}:{k_hi}]")
     lat.ijk = g.astype(np.int64)
     lat.gid = (lat.ijk[:, 0] * (2 * ny + 1) + lat.ijk[:, 1]) * (2 * nz + 1) + lat.ijk[:, 2]
+    return lat
+
+
+def _hash_uniform(gid: np.ndarray, seed: int, stream: int) -> np.ndarray:
+    """Counter-based uniform [0, 1) per global node id (splitmix64 of (seed, stream, gid)), so any
+    window of a lattice regenerates the same node attributes."""
+    with np.errstate(over="ignore"):
+        z = (gid.astype(np.uint64) * np.uint64(0x9E3779B97F4A7C15) + np.uint64((seed * 1_000_003 + stream) & 0xFFFFFFFF)
+             * np.uint64(0xD1B54A32D192ED03))
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        z = z ^ (z >> np.uint64(31))
+    return (z >> np.uint64(11)).astype(np.float64) * (1.0 / 9007199254740992.0)
+
+
+STOCH_BLOCK = 10     # layers per independently generated block of stochastic_window
+
+
+def stochastic_window(side: int, nz: int, k_lo: int, k_hi: int, seed: int = 0, deg_min: int = 3, deg_max: int = 30,
+                      r_min: float = 0.02, r_max: float = 0.04, min_angle_deg: float = 25.0, zipf: float = 1.1,
+                      block: int = STOCH_BLOCK) -> Lattice:
+    """The layers k in [k_lo, k_hi] of ONE stochastic Voronoi-style lattice on a side x side x nz
+    jittered grid (BASELINE.json configs[2]; the multi-GPU spatial blocks of it), with the struts
+    among them.  Node attributes -- jitter U(-0.3, 0.3), Zipf target degree on [deg_min, deg_max],
+    radius U(r_min, r_max) -- are counter-based functions of the global id
+    gid = (k * side + j) * side + i.  Struts: the greedy of stochastic() (descending target, nearest
+    neighbours in the 5x5x5 surrounding cells, >= min_angle_deg between struts at a node) runs on
+    each block of `block` layers independently, then on each block seam (2 layers either side)
+    for the struts crossing it, continuing from the blocks' degrees.  So the lattice is local:
+    a window needs only the blocks within 2 layers of it, and two windows agree on every node and
+    strut they share.  Nodes ascend in gid, struts in (gid, gid)."""
+    k_lo, k_hi = max(0, k_lo), min(nz - 1, k_hi)
+    lib = _stoch_lib()
+    b_lo, b_hi = max(0, k_lo - 2) // block, min(nz - 1, k_hi + 2) // block
+    c_lo, c_hi = b_lo * block, min(nz, (b_hi + 1) * block)          # covered layers [c_lo, c_hi)
+    nzc = c_hi - c_lo
+    nxy = side * side
+    gid = np.arange(c_lo * nxy, c_hi * nxy, dtype=np.int64)
+    i, j, k = gid % side, (gid // side) % side, gid // nxy
+    xyz = np.ascontiguousarray(np.stack([i, j, k], 1).astype(np.float64))
+    for a in range(3):
+        xyz[:, a] += 0.6 * _hash_uniform(gid, seed, a) - 0.3
+    ks = np.arange(deg_min, deg_max + 1)
+    p = 1.0 / (ks - deg_min + 1.0) ** zipf
+    cdf = np.cumsum(p / p.sum())
+    target = ks[np.minimum(np.searchsorted(cdf, _hash_uniform(gid, seed, 3), side="right"), len(ks) - 1)].astype(np.int32)
+    radius = r_min + (r_max - r_min) * _hash_uniform(gid, seed, 4)
+    n = len(gid)
+    deg = np.zeros(n, np.uint8)
+    nbr = np.zeros((n, 31), np.int32)
+    cos_lim = float(np.cos(np.deg2rad(min_angle_deg)))
+    ends_all = []
+
+    def zone(z0, z1, seam):
+        """greedy on global layers [z0, z1) of the covered grid; seam layer or -1"""
+        a0, a1 = (z0 - c_lo) * nxy, (z1 - c_lo) * nxy
+        t = target[a0:a1]
+        order = (np.lexsort((np.arange(a1 - a0), -t)) + a0).astype(np.int64)   # descending target, then gid
+        cap = int(t.astype(np.int64).sum() // 2) + 1
+        ends = np.zeros((cap, 2), np.int64)
+        S = lib.stoch_zone(xyz.ctypes.data, side, side, nzc, z0 - c_lo, z1 - c_lo, target.ctypes.data, order.ctypes.data,
+                           cos_lim, (seam - c_lo) if seam >= 0 else -1, deg.ctypes.data, nbr.ctypes.data, cap,
+                           ends.ctypes.data)
+        if S < 0:
+            raise RuntimeError(f"stochastic_window zone generator failed ({S})")
+        ends_all.append(ends[:S])
+
+    for b in range(b_lo, b_hi + 1):                          # blocks, each on its own
+        zone(b * block, min(nz, (b + 1) * block), -1)
+    for b in range(b_lo + 1, b_hi + 1):                      # seams between covered blocks
+        s0 = b * block
+        zone(max(c_lo, s0 - 2), min(c_hi, s0 + 2), s0)
+    ends = np.concatenate(ends_all) if ends_all else np.zeros((0, 2), np.int64)
+    keep = (k >= k_lo) & (k <= k_hi)
+    newid = -np.ones(n, np.int64)
+    newid[keep] = np.arange(int(keep.sum()))
+    e = newid[ends]
+    e = e[(e >= 0).all(1)]
+    lat = _finish(xyz[keep], e, radius[keep], f"stochwin{side}x{side}x{nz}[{k_lo}:{k_hi}]")
+    lat.ijk = np.stack([i[keep], j[keep], k[keep]], 1).astype(np.int64)
+    lat.gid = gid[keep]
     return lat

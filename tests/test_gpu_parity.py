@@ -187,7 +187,7 @@ def test_csr_offsets_are_the_degree_prefix_sum(built):
     assert np.array_equal(ent[:, 0].astype(np.int64), o_st)
 
 
-@pytest.mark.parametrize("family", ["octet", "bcc"])
+@pytest.mark.parametrize("family", ["octet", "bcc", "stoch"])
 def test_virtual_ranks_union_equals_global_gpu(family):
     """The multi-GPU path on one device: slab windows with halo recompute + emit masks.  The
     union of the per-rank STL outputs equals the single-lattice output bitwise (as a set),
@@ -195,16 +195,19 @@ def test_virtual_ranks_union_equals_global_gpu(family):
     from paper_2405_15197_b200 import MetaMesher
     from paper_2405_15197_b200 import partition as P
     nx, ny, nz = 4, 3, 6
-    k_top = 2 * nz
+    k_top, halo = 2 * nz, 2
     gen = (lambda lo, hi: synth.octet_window(nx, ny, nz, lo, hi, radius=0.03, r_max=0.06)) if family == "octet" \
         else (lambda lo, hi: synth.bcc_window(nx, ny, nz, lo, hi, radius=0.05))
+    if family == "stoch":   # configs[2]: one stochastic lattice, 10 x 10 x 30 nodes, 4-layer halos
+        k_top, halo = 29, 4
+        gen = lambda lo, hi: synth.stochastic_window(10, 30, lo, hi, seed=0)
     full = gen(0, k_top)
     mm = MetaMesher(0).load_lattice(full).build()
     T = mm.triangulate(5e-3)
     ref = mm.triangles(0, T)
     parts, counts = [], []
     for r in range(3):
-        k_lo, k_hi = P.window(r, 3, k_top)
+        k_lo, k_hi = P.window(r, 3, k_top, halo)
         lat = gen(k_lo, k_hi)
         nm, sm = P.emit_masks(lat.ijk[:, 2], lat.ends, r, 3, k_top)
         m = MetaMesher(0).load_lattice(lat).build().set_emit_mask(nm, sm)

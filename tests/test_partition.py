@@ -112,3 +112,48 @@ def test_allgather_of_counts_gives_global_offsets_gloo():
     total = og.triangulate(1e-2)
     assert out[0][2] == out[1][2] == total
     assert out[0][1] == 0 and out[1][1] == out[0][0]
+
+
+# ---- configs[2]: ONE stochastic lattice split into z-slabs (bench.make_config("stochN", r, W)) ----
+@pytest.mark.parametrize("world", [2, 3])
+def test_stochastic_slabs_partition_one_lattice(world):
+    """bench.make_config("stoch12", r, world) over all ranks: every node of the ONE global
+    stochastic lattice (12 x 12 x 12*world) is owned exactly once, every strut emitted exactly
+    once, and both ends of an owned strut -- and every owned node -- see their full global
+    neighbourhood in the rank's window (so their meta-meshes equal the single-lattice ones)."""
+    import bench
+    n = 12
+    full = synth.stochastic_window(n, n * world, 0, n * world - 1, seed=0)
+    gstrut = {(int(full.gid[a]), int(full.gid[b])) for a, b in full.ends}
+    gdeg = dict(zip(full.gid.tolist(), full.degrees().tolist()))
+    owned_nodes, owned_struts = [], []
+    for r in range(world):
+        lat, (nm, sm), _ = bench.make_config(f"stoch{n}", r, world)
+        owned_nodes += list(lat.gid[nm.astype(bool)])
+        owned_struts += [(int(lat.gid[a]), int(lat.gid[b])) for a, b in lat.ends[sm.astype(bool)]]
+        deg = lat.degrees()
+        for v in np.unique(lat.ends[sm.astype(bool)]):
+            assert deg[v] == gdeg[int(lat.gid[v])]
+        for v in np.nonzero(nm)[0]:
+            assert deg[v] == gdeg[int(lat.gid[v])]
+        # the window's positions / radii / struts are those of the global lattice
+        idx = np.searchsorted(full.gid, lat.gid)
+        assert np.array_equal(lat.xyz, full.xyz[idx]) and np.array_equal(lat.node_r, full.node_r[idx])
+    assert sorted(owned_nodes) == sorted(full.gid.tolist())
+    assert len(owned_struts) == len(set(owned_struts)) == len(gstrut)
+    assert set(owned_struts) == gstrut
+    assert full.degrees().max() <= 30 and np.percentile(full.degrees(), 50) <= 6   # skewed 3..30
+
+
+def test_stochastic_windows_agree_with_the_global_lattice():
+    """Any z-window of stochastic_window equals the global lattice restricted to its layers
+    (blocks of 10 layers generated independently + seam passes: the generator is local)."""
+    g = synth.stochastic_window(14, 37, 0, 36, seed=3)
+    nxy = 14 * 14
+    ge = {tuple(e) for e in g.gid[g.ends].tolist()}
+    for lo, hi in [(0, 9), (5, 23), (18, 36), (9, 10)]:
+        w = synth.stochastic_window(14, 37, lo, hi, seed=3)
+        we = {tuple(e) for e in w.gid[w.ends].tolist()}
+        inside = {e for e in ge if lo * nxy <= e[0] < (hi + 1) * nxy and lo * nxy <= e[1] < (hi + 1) * nxy}
+        assert we == inside
+        assert np.array_equal(w.xyz, g.xyz[w.gid - g.gid[0]])

@@ -6,11 +6,16 @@ import pytest
 import synth
 
 
-def test_stochastic_degrees_angles_and_determinism():
-    a = synth.stochastic(12, seed=3)
-    b = synth.stochastic(12, seed=3)
+@pytest.mark.parametrize("gen", ["stochastic", "stochastic_window"])
+def test_stochastic_degrees_angles_and_determinism(gen):
+    """configs[2]'s generators: skewed degrees 3..30, >= 25 deg between struts at a node,
+    deterministic per seed (stochastic_window: the windowable one bench.py uses)."""
+    make = (lambda sd: synth.stochastic(12, seed=sd)) if gen == "stochastic" else \
+        (lambda sd: synth.stochastic_window(12, 24, 0, 23, seed=sd))
+    a = make(3)
+    b = make(3)
     assert np.array_equal(a.ends, b.ends) and np.array_equal(a.xyz, b.xyz) and np.array_equal(a.node_r, b.node_r)
-    assert not np.array_equal(a.ends, synth.stochastic(12, seed=4).ends)
+    assert not np.array_equal(a.ends, make(4).ends)
     deg = a.degrees()
     assert deg.max() <= 30 and deg.max() >= 20          # high-degree hubs exist
     assert np.median(deg) <= 6                          # ... but most nodes are low-degree (skew)
