@@ -412,7 +412,7 @@ def main():
                    "n_nodes_local": N, "global_output_offset_rank0": offsets["base"],
                    "triangles_per_step": int(T), "parallelism": f"dp{world} (one spatial block per GPU)",
                    "l2": "output chunks of 13.4 GB >> 126 MB L2 (no flush needed)",
-                   "error_nodes": st["n_error_nodes"],
+                   "error_nodes": st["n_error_nodes"], "spilled_nodes": st["n_spilled_nodes"],
                    "error_codes": {str(i): int(x) for i, x in enumerate(st["err_hist"]) if i and x}},
         "metamesh_struts_per_s": S_own * args.steps / (mm_ms / 1e3) if mm_ms else None,
         "triangles_per_s": T_all / (ms_max / 1e3),

@@ -52,7 +52,11 @@ typedef enum {
 enum { LMM_HOST = 0, LMM_DEVICE = 1 };
 
 /* Per-node meta-mesh status codes (lmm_stats.err_hist index); identical meanings to
- * the oracle's ORC_E_* codes. */
+ * the oracle's ORC_E_* codes.  DEGREE = degree > 63.  JCAP/CCAP/ACAP/QCAP mark a bucket
+ * workspace exceeded inside lmm_build_metamesh; such nodes are meta-meshed again by the spill
+ * kernel, so they are not reported afterwards (ACAP would remain only for a node of more than
+ * 1023 vertices, which degree <= 63 cannot reach).  CHAIN/HOLE/ANGLE/UNREF/EMPTY are reported
+ * only if the topology closes at no vertex resolution delta_c * 2^level, level 0..4. */
 enum {
   LMM_NODE_OK = 0, LMM_NODE_DEGREE = 1, LMM_NODE_STRUT = 2, LMM_NODE_JCAP = 3,
   LMM_NODE_CCAP = 4, LMM_NODE_ACAP = 5, LMM_NODE_CONIC = 6, LMM_NODE_UNREF = 7,
@@ -69,6 +73,8 @@ typedef struct {
   int64_t n_error_nodes;
   int64_t err_hist[LMM_NODE_NCODES];
   int64_t degree_hist[33];  /* nodes by degree 0..31, [32] = degree > 31 */
+  int64_t n_spilled_nodes;  /* nodes meta-meshed by the spill kernel (degree 32..63, a bucket
+                               workspace exceeded, or re-decided at a coarser resolution) */
 } lmm_stats;
 
 /* Create a context on CUDA device `device`, enqueuing on `cuda_stream`
@@ -94,9 +100,13 @@ LMM_API int lmm_load_lattice(lmm_ctx *ctx, const float *xyz, int64_t n_nodes,
                              int where);
 
 /* Build the meta-mesh of every node: degree histogram + degree-bucketed schedule,
- * then the per-node kernel (sides, triple junctions, vertex clusters, arcs via Eq. 7,
- * arc loops per strut end, hole contours).  Nodes the model cannot represent get a
- * non-zero status (see lmm_stats); they contribute no triangles. */
+ * then the per-node kernels (sides, triple junctions, vertex clusters, arcs via Eq. 7,
+ * arc loops per strut end, hole contours): lane groups per node for degree <= 31, a CTA
+ * per node (spill kernel) for degree 32..63, for nodes that exceed their bucket's
+ * workspace and for nodes re-decided at a coarser vertex resolution (R10).
+ * Nodes the model cannot represent (degree > 63, a strut too short or degenerate, an
+ * unbounded conic carrying a vertex, a topology that does not close at any resolution)
+ * get a non-zero status (see lmm_stats); they contribute no triangles. */
 LMM_API int lmm_build_metamesh(lmm_ctx *ctx);
 
 /* Totals and histograms of the current meta-mesh (synchronises). */

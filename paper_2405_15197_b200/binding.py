@@ -32,7 +32,8 @@ class _Stats(C.Structure):
     _fields_ = [("n_nodes", C.c_int64), ("n_struts", C.c_int64), ("n_vertices", C.c_int64),
                 ("n_arcs", C.c_int64), ("n_elliptical_arcs", C.c_int64), ("n_circular_arcs", C.c_int64),
                 ("n_loop_entries", C.c_int64), ("n_holes", C.c_int64), ("n_error_nodes", C.c_int64),
-                ("err_hist", C.c_int64 * 14), ("degree_hist", C.c_int64 * 33)]
+                ("err_hist", C.c_int64 * 14), ("degree_hist", C.c_int64 * 33),
+                ("n_spilled_nodes", C.c_int64)]
 
 
 _lib = None

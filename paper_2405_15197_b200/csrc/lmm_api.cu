@@ -251,6 +251,7 @@ LMM_API int lmm_metamesh_stats(lmm_ctx *c, lmm_stats *out) {
     out->n_circular_arcs += hdr[n].w;   // hole entries = cap arcs
   }
   out->n_elliptical_arcs = out->n_arcs - out->n_circular_arcs;
+  out->n_spilled_nodes = c->n_spill;
   free(hdr);
   return LMM_OK;
 }

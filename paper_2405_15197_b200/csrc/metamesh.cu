@@ -90,7 +90,10 @@ struct alignas(16) WS_A : WSCore<MAXS, MAXV> {
   int jlab[MAXJ];
 };
 
-constexpr int QL = 3;   // arc-interval midpoints queued per lane and round (part B)
+#ifndef LMM_QL
+#define LMM_QL 3
+#endif
+constexpr int QL = LMM_QL;   // arc-interval midpoints queued per lane and round (part B)
 
 template <int MAXS, int MAXJ, int MAXV, int MAXA, int MAXLE, int MAXH>
 struct alignas(16) WS_B : WSCore<MAXS, MAXV> {
@@ -143,7 +146,11 @@ template <int G> __device__ __forceinline__ int first_err(cg::thread_block_tile<
 
 
 
-#define MAXQ 16
+// vertices on one conic held per lane in part B (more: QCAP, the node goes to the spill kernel)
+#ifndef LMM_MAXQ
+#define LMM_MAXQ 16
+#endif
+#define MAXQ LMM_MAXQ
 #define MAXLOOP 32
 
 // side records between the parts: 5 float4 per CSR entry
