@@ -33,6 +33,9 @@ def _lat(name):
         "voronoi": lambda: synth.voronoi_like(300, seed=3, radius=0.05),
         # configs[2] shape: skewed degrees 3..30, cones; configs[3] shape: a BCC spatial block
         "stochastic9": lambda: synth.stochastic(9, seed=7),
+        # the sharp-angle family: struts down to 10 degrees apart at a node (long strut-strut
+        # intersections, near-parabolic sections, short-strut limits)
+        "sharp10": lambda: synth.stochastic_window(9, 9, 0, 8, seed=21, min_angle_deg=10.0),
         "bccwin": lambda: synth.bcc_window(4, 3, 5, 3, 8),
         # a strut ringed by 16 neighbours: its loop has 16 entries (> the emit pass's arc cache,
         # so its band takes the windowed path)
@@ -44,7 +47,7 @@ def _lat(name):
 
 
 NAMES = ["single", "cone", "chain-bent", "star-bcc", "cubic3", "bcc3", "octet2", "octet2-graded", "bcc3-jitter",
-         "cubic4-graded-jitter", "voronoi", "stochastic9", "bccwin", "crown16", "bcc10"]
+         "cubic4-graded-jitter", "voronoi", "stochastic9", "sharp10", "bccwin", "crown16", "bcc10"]
 
 
 @pytest.fixture(scope="module")
@@ -257,14 +260,16 @@ def test_random_lattices_parity(seed):
     mm.close()
 
 
-@pytest.mark.parametrize("seed", list(range(6)))
+@pytest.mark.parametrize("seed", list(range(8)))
 def test_medium_random_lattices_parity(seed):
-    """Stress at medium size (10-40k struts): every node of a stochastic / jittered graded
-    lattice bit-exact in topology, and the whole STL within tolerance."""
+    """Stress at medium size (10-40k struts): every node of a stochastic / jittered graded /
+    sharp-angle (10 deg) lattice bit-exact in topology, and the whole STL within tolerance."""
     from paper_2405_15197_b200 import MetaMesher, decode_node
     lat = [lambda: synth.stochastic(16 + seed, seed=1000 + seed, r_min=0.015, r_max=0.05),
            lambda: synth.jitter(synth.graded_radii(synth.octet(7, 6, 6), 0.02, 0.06, seed % 3), 0.05, 1000 + seed),
-           lambda: synth.jitter(synth.graded_radii(synth.bcc(12, 10, 9), 0.03, 0.07, seed % 3), 0.08, 1000 + seed)][seed % 3]()
+           lambda: synth.jitter(synth.graded_radii(synth.bcc(12, 10, 9), 0.03, 0.07, seed % 3), 0.08, 1000 + seed),
+           # sharp-angle family: >= 10 degrees between struts at a node
+           lambda: synth.stochastic_window(16 + seed, 16 + seed, 0, 15 + seed, seed=2000 + seed, min_angle_deg=10.0)][seed % 4]()
     mm = MetaMesher(0).load_lattice(lat).build()
     orc = oracle.Oracle.from_lattice(lat)
     assert orc.metamesh() == mm.stats()["n_error_nodes"]
