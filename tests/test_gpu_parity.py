@@ -11,7 +11,7 @@ import pytest
 
 import oracle
 import synth
-from _parity import GEOM_TOL, assert_node_parity, assert_triangles_close
+from _parity import GEOM_TOL, GEOM_TOL_SHARP, assert_node_parity, assert_triangles_close
 
 pytestmark = pytest.mark.gpu
 
@@ -68,9 +68,7 @@ def built():
     return get
 
 
-# binary32 conditioning allowance of the 10-degree family: its near-parabolic Eq. 7 sections
-# (|a| ~ 10 R) carry errors up to 1.25e-4 r_min in (o, a, b) and on the arc (R13)
-GEOM_TOL_BY_NAME = {"sharp10": 1.5e-4}
+GEOM_TOL_BY_NAME = {"sharp10": GEOM_TOL_SHARP}   # the 10-degree family (tests/_parity.py)
 
 
 @pytest.mark.parametrize("name", NAMES)
@@ -121,7 +119,7 @@ def _triangulation_parity(built, name, ce):
     tri = mm.triangles(0, T).astype(np.float64)
     ref = orc.write_triangles()
     r = float(lat.node_r.min())
-    assert_triangles_close(tri, ref, r, (name, ce))
+    assert_triangles_close(tri, ref, r, (name, ce), GEOM_TOL_BY_NAME.get(name, GEOM_TOL))
     # facet normals agree wherever the facet is not tiny
     # facet normals: error bounded by vertex error / shortest altitude
     v1, v2, v3 = ref[:, 1], ref[:, 2], ref[:, 3]
@@ -279,10 +277,11 @@ def test_medium_random_lattices_parity(seed):
     orc = oracle.Oracle.from_lattice(lat)
     assert orc.metamesh() == mm.stats()["n_error_nodes"]
     bufs = mm.buffers()
-    tol = GEOM_TOL * float(lat.node_r.min())
+    gt = GEOM_TOL_SHARP if seed % 4 == 3 else GEOM_TOL
+    tol = gt * float(lat.node_r.min())
     for n in range(lat.n_nodes):
         assert_node_parity(decode_node(bufs, n), orc.node(n), tol, n)
     T = mm.triangulate(2e-3)
     assert T == orc.triangulate(2e-3)
-    assert_triangles_close(mm.triangles(0, T), orc.write_triangles(), float(lat.node_r.min()), seed)
+    assert_triangles_close(mm.triangles(0, T), orc.write_triangles(), float(lat.node_r.min()), seed, gt)
     mm.close()
