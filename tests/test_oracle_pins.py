@@ -243,7 +243,9 @@ def _incident(lat, n):
 ], ids=["bcc-jitter", "octet-graded-jitter", "voronoi"])
 def test_arc_points_lie_on_the_union_boundary(oracle_mod, lat):
     """Brute force: every sampled point of every arc lies on the surfaces of both sides it
-    separates and inside no other strut (hull_sd), and junction vertices likewise."""
+    separates and inside no other strut (hull_sd); every vertex lies exactly on three of the
+    sides of its tie mask (its representative triple junction), within the clustering radius
+    of the others, and not inside any side outside its mask beyond the tie tolerance."""
     o = oracle_mod.Oracle.from_lattice(lat)
     assert o.metamesh() == 0
     off, cs = o.csr()
@@ -274,6 +276,21 @@ def test_arc_points_lie_on_the_union_boundary(oracle_mod, lat):
                 for k in range(1, len(sides)):
                     if k not in (lo, hi):
                         assert sd(k, y) > -1e-9
+        for q in range(r["nv"]):
+            y = r["v_pos64"][q]
+            mask = int(r["v_mask"][q])
+            dist = lambda k: abs(np.linalg.norm(y) - R) if k == 0 else abs(sd(k, y))
+            tied = sorted(dist(k) for k in range(len(sides)) if (mask >> k) & 1)
+            assert len(tied) >= 2
+            if len(tied) >= 3:
+                assert tied[2] < 1e-9, (n, q, tied)           # a triple junction exactly
+            else:                                             # the seam point of a closed arc
+                assert tied[1] < 1e-9, (n, q, tied)
+            assert tied[-1] < 2e-3 * R, (n, q, tied)           # the rest of its cluster
+            for k in range(len(sides)):
+                if not (mask >> k) & 1:
+                    out = (np.linalg.norm(y) - R) if k == 0 else sd(k, y)
+                    assert out > -2e-4 * R, (n, q, k, out)
 
 
 @pytest.mark.parametrize("seed", range(3))
