@@ -9,8 +9,15 @@ B.LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "liblmm_ph
 lib = B.load_library()
 lib.lmm_debug_phase_cycles.argtypes = [C.c_void_p]
 cfg = sys.argv[1] if len(sys.argv) > 1 else "octet40"
-n = int(cfg[5:]) if cfg.startswith("octet") else int(cfg[3:])
-lat = synth.graded_radii(synth.octet(n, n, n), 0.03, 0.06, 0) if cfg.startswith("octet") else synth.bcc(n, n, n)
+import re
+fam, n = re.fullmatch(r"(octet|bcc|stoch)(\d+)", cfg).groups()
+n = int(n)
+if fam == "octet":
+    lat = synth.graded_radii(synth.octet(n, n, n), 0.03, 0.06, 0)
+elif fam == "bcc":
+    lat = synth.bcc(n, n, n)
+else:
+    lat = synth.stochastic_window(n, n, 0, n - 1, seed=0)
 xyz, ends, rend = (torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in (lat.xyz, lat.ends, lat.r_end))
 h = B.lmm_create(0, torch.cuda.current_stream().cuda_stream)
 B.lmm_load_lattice(h, xyz, ends, rend)
@@ -19,7 +26,7 @@ torch.cuda.synchronize()
 out = (C.c_ulonglong * 16)()
 lib.lmm_debug_phase_cycles(out)
 names = ["sides", "junctions", "clustering", "arcs(rest)", "drop+unref", "loops", "holes", "write",
-         "arcs:pairs", "arcs:conic+int", "arcs:validity", "arcs:assemble", "p13", "p14", "p15", "p16"]
+         "arcs:pairs", "arcs:conic+int", "arcs:validity", "arcs:assemble", "live pairs", "p14", "p15", "p16"]
 tot = sum(out)
 print(cfg, lat.n_nodes, "nodes; cycles per node (lane-0 warps):", tot / lat.n_nodes)
 for k, v in zip(names, out):
