@@ -410,7 +410,8 @@ def main():
         "data": "synthetic",
         "config": {"workload": desc, "chord_error": args.ce, "n_struts": int(S_all), "n_struts_local": S,
                    "n_nodes_local": N, "global_output_offset_rank0": offsets["base"],
-                   "triangles_per_step": int(T), "parallelism": f"dp{world} (one spatial block per GPU)",
+                   "triangles_per_step": int(T), "triangles_per_step_all_ranks": int(T_all),
+                   "parallelism": f"dp{world} (one spatial block per GPU)",
                    "l2": "output chunks of 13.4 GB >> 126 MB L2 (no flush needed)",
                    "error_nodes": st["n_error_nodes"], "spilled_nodes": st["n_spilled_nodes"],
                    "error_codes": {str(i): int(x) for i, x in enumerate(st["err_hist"]) if i and x}},
