@@ -70,7 +70,7 @@ struct lmm_ctx {
   DevBuf ring_n;     // int [2S] points per ring (CSR entry), count pass
   int64_t H = 0, n_tri = 0, n_tri_band = 0;
   bool emit_attr_set = false;   // k_emit's opt-in shared-memory limit set on this context's device
-  int emit_occ[8] = {0};        // k_emit CTAs per SM by point-cache size class
+  int emit_occ[32] = {0};       // k_emit CTAs per SM by point-cache size (pcap / 32)
   bool tri_ok = false;
   // scratch
   DevBuf tmp64;      // int64 scan scratch

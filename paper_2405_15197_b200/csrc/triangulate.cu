@@ -404,6 +404,23 @@ constexpr int GRP = 56;           // triangles per aligned group (2800 B; 28 lan
 constexpr int MAXRE = 32;         // ring entries per ring (>= MAXLOOP of the meta-mesh)
 constexpr int MAXRA = 8;          // arc records (and entry start vertices) cached per ring
 
+constexpr int GW = 64;            // triangles per group of the CTA-window path (32 lanes x 2 records)
+
+// a loop entry of a span window as the point pass reads it (built in place from the raw arc
+// record + start vertex that cp.async staged in the same slot)
+struct __align__(16) PtEnt {
+  float t0, dq;               // Eq. 12: t = t0 + jj * dq, dq = dt / N (fast division, as arc_pt)
+  float ox, oy, oz, ax, ay, az, bx, by, bz;   // Eq. 1 arc frame (node-local)
+  float cx, cy, cz;           // node centre of the ring
+  int nf;                     // N | fwd << 16
+  int P0;                     // cache position of the entry's point j = 0
+  int wj;                     // points j >= wj sit `off` lower (ring-B rotation wraps inside the entry)
+  int dupj;                   // point j == dupj is also stored at its position + off (ring closure copy)
+  int off;                    // nA (ring A) / nB (ring B)
+  int pad;                    // est: the entry's first point in the window's flattened point order
+};
+static_assert(sizeof(PtEnt) == 80, "window entry is 80 bytes");
+
 // per-warp shared memory: fixed part, then the point cache (pcap x float2, pcap x float)
 struct __align__(16) WarpRing {
   ArcRec arc[2][MAXRA];
@@ -497,6 +514,19 @@ __device__ __forceinline__ ArcRec lds_arc(const ArcRec *p) {
   return a;
 }
 
+// Eq. 12 interior point jj of an arc with N segments, translated by the node centre o.  The
+// one formula of every emit path, every operation rounded as written, so the two bands and the
+// hole fan that share an arc produce the same bits (watertight seams).
+__device__ __forceinline__ f3 arc_pt(const ArcRec &A, int N, int jj, float ox, float oy, float oz) {
+  float t = __fmaf_rn((float)jj, __fdividef(A.dt, (float)N), A.t0);
+  t = __fmaf_rn(-LMM_TWO_PI_F, rintf(__fmul_rn(t, 1.0f / LMM_TWO_PI_F)), t);
+  float sn, cs;
+  __sincosf(t, &sn, &cs);
+  return F3(__fadd_rn(ox, __fmaf_rn(A.ax, sn, __fmaf_rn(A.bx, cs, A.ox))),
+            __fadd_rn(oy, __fmaf_rn(A.ay, sn, __fmaf_rn(A.by, cs, A.oy))),
+            __fadd_rn(oz, __fmaf_rn(A.az, sn, __fmaf_rn(A.bz, cs, A.oz))));
+}
+
 // Eq. 12 point idx of ring r, whose loop entry is e; endpoints are the shared vertices
 __device__ __forceinline__ f3 ring_point_e(const WarpRing &w, int r, const RingRef &R, int e, int idx) {
   LoopRec L;
@@ -512,13 +542,9 @@ __device__ __forceinline__ f3 ring_point_e(const WarpRing &w, int r, const RingR
     p = F3(q.x, q.y, q.z);
   } else {
     const ArcRec A = e < MAXRA ? lds_arc(&w.arc[r][e]) : load_arc(R.arcs + le_arc(L.arc_fwd));
-    float t = A.t0 + (float)jj * __fdividef(A.dt, (float)N);
-    t = t - LMM_TWO_PI_F * rintf(t * (1.0f / LMM_TWO_PI_F));
-    float sn, cs;
-    __sincosf(t, &sn, &cs);
-    p = F3(fmaf(A.ax, sn, fmaf(A.bx, cs, A.ox)), fmaf(A.ay, sn, fmaf(A.by, cs, A.oy)), fmaf(A.az, sn, fmaf(A.bz, cs, A.oz)));
+    return arc_pt(A, N, jj, R.ox, R.oy, R.oz);
   }
-  return F3(R.ox + p.x, R.oy + p.y, R.oz + p.z);
+  return F3(__fadd_rn(R.ox, p.x), __fadd_rn(R.oy, p.y), __fadd_rn(R.oz, p.z));
 }
 
 // point idx of ring r, its entry found by a scan of the entry starts (windowed bands, holes)
@@ -545,12 +571,7 @@ __device__ __forceinline__ f3 ring_point_formula(const WarpRing &w, int r, const
   const int j = idx - le_cum(L.cum);
   const int jj = fwd ? j : N - j;
   const ArcRec A = lds_arc(&w.arc[r][e]);
-  float t = A.t0 + (float)jj * __fdividef(A.dt, (float)N);
-  t = t - LMM_TWO_PI_F * rintf(t * (1.0f / LMM_TWO_PI_F));
-  float sn, cs;
-  __sincosf(t, &sn, &cs);
-  return F3(R.ox + fmaf(A.ax, sn, fmaf(A.bx, cs, A.ox)), R.oy + fmaf(A.ay, sn, fmaf(A.by, cs, A.oy)),
-            R.oz + fmaf(A.az, sn, fmaf(A.bz, cs, A.oz)));
+  return arc_pt(A, N, jj, R.ox, R.oy, R.oz);
 }
 
 __device__ __forceinline__ void put_point(const Pts &pt, int k, f3 p) { pt.xy[k] = make_float2(p.x, p.y); pt.z[k] = p.z; }
@@ -740,11 +761,12 @@ __device__ void emit_band_whole(const TriParams &P, WarpRing &w, const Pts &pt, 
 }
 
 template <class Prefetch>
-__device__ void emit_band(const TriParams &P, WarpRing &w, const Pts &pt, const BandRec &H, int64_t base, int64_t first, int64_t last,
-                          unsigned char *out, int lane, Prefetch prefetch) {
+__device__ void emit_band(const TriParams &P, WarpRing &w, const Pts &pt, const BandRec &H, int64_t base, int64_t first,
+                          int64_t lo, int64_t hi, unsigned char *out, int lane, Prefetch prefetch) {
+  // triangles [lo, hi) of the band; output record t at out + (t - first) * REC
   const int nA = H.nA, nB = H.nB, kB = H.kB;
-  const int64_t ta = base > first ? base : first;
-  const int64_t tb = base + nA + nB < last ? base + nA + nB : last;
+  const int64_t ta = base > lo ? base : lo;
+  const int64_t tb = base + nA + nB < hi ? base + nA + nB : hi;
   if (ta >= tb) { prefetch(0); prefetch(1); prefetch(2); prefetch(3); return; }
   RingRef RA, RB;
   RA.arcs = P.arc + H.aA;
@@ -890,6 +912,504 @@ __device__ void emit_hole(const TriParams &P, WarpRing &w, const Pts &pt, int g,
   }
 }
 
+__device__ __forceinline__ int nth_bit(unsigned m, int n) {   // position of the n-th (0-based) set bit
+  int p = 0;
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) {
+    const int c = __popc(m & ((1u << s) - 1u));
+    if (n >= c) { n -= c; m >>= s; p += s; }
+  }
+  return p;
+}
+__device__ __forceinline__ unsigned mask_ge(int x) { return x >= 32 ? 0u : (x <= 0 ? 0xffffffffu : (0xffffffffu << x)); }
+__device__ __forceinline__ unsigned mask_le(int x) { return x < 0 ? 0u : (x >= 31 ? 0xffffffffu : ((2u << x) - 1u)); }
+
+struct NoPrefetch {
+  __device__ void operator()(int) const {}
+};
+
+
+// ---------------------------------------------------------------------------------
+// CTA-window emission of the band region (bands short against the window: k_emit_span)
+//
+// A CTA owns the band triangles [T0, T1) of a span (T0 - first a multiple of GW, so every
+// group of GW records starts on the 16-byte output grid) and walks its bands in windows:
+// up to SNB whole bands (warp 0 reads their records lane-parallel, lane = band) whose points
+// fit the CTA's point cache and whose loop entries fit SEC (thread = entry).  Every thread
+// stages its entry's loop record, arc record and start vertex by cp.async and turns them
+// into the Eq. 12 parameters and cache placement of the entry's points; the window's points
+// are then computed flattened over the CTA (the entry of a point from a bitmap of entry
+// starts), and every complete group of GW triangles -- whatever bands its records belong
+// to -- is assembled by one warp (lane = 2 records; band = slot from a redux of band
+// starts; ring positions from the prefix counts of the merge bits) and leaves as one TMA
+// bulk copy from the warp's staging buffer.  The group that a window leaves incomplete
+// waits for the next window: the points its records still need move to the front of the
+// cache.  A band too large for a window goes through emit_band (warp 0).
+// ---------------------------------------------------------------------------------
+constexpr int SNB = 32;           // bands per window (warp 0 lanes)
+constexpr int SEC = EMIT_T;       // loop entries per window (one per thread)
+constexpr int SMW = 48;           // merge-bit / point-bitmap words per window
+constexpr int SPCW_MAX = 1280;    // point cache of a CTA window (runtime-sized)
+constexpr int SPAN_CTA = 16384;   // band triangles per CTA span (a multiple of GW)
+enum { ACT_WINDOW = 0, ACT_DONE = 1, ACT_LONG = 2 };
+#ifndef LMM_SPAN_MINB
+#define LMM_SPAN_MINB 6
+#endif
+
+struct __align__(16) SpanSm {
+  PtEnt ent[SEC];                     // raw arc (48) | start vertex (16) | loop entry (16), then the entry
+  uint4 stage[EW][GW * REC / 16];     // per-warp staging buffers
+  // per window (double-buffered: the current one and the one built ahead)
+  int s_ta[2][SNB], s_XA[2][SNB], s_XB[2][SNB];   // band k: first record; A_i at XA + C(q), B_j at XB + q - C(q)
+  uint32_t mw[2][SMW];                // merge bits of the window's records (bits before the window cleared)
+  int mp[2][SMW];                     //   exclusive prefix popcounts
+  long long wb0[2];                   // global word of mw[b][0]
+  int w_ta0[2], w_tend[2], w_K[2], w_Pn[2], w_Ew[2];   // first record, end, bands, points, entries
+  // the built window's bands, for its entry set-up
+  int b_pos[SNB], b_flx[SNB], b_kB[SNB], b_nA[SNB], b_nB[SNB], b_e0[SNB], b_cntA[SNB], b_fA[SNB], b_fB[SNB];
+  unsigned b_aA[SNB], b_aB[SNB], b_pA[SNB], b_pB[SNB];
+  float b_c[SNB][6];
+  uint8_t e_band[SEC];
+  uint32_t bm[SMW];                   // flattened point p starts an entry
+  int act, gnext;
+};
+__host__ __device__ constexpr int span_bytes(int pcw) { return (int)((sizeof(SpanSm) + (size_t)pcw * 12 + 15) / 16 * 16); }
+
+// staged bytes [b0, b1) of a group -> dst + [b0, b1) (dst 16-byte aligned), as flush_group
+__device__ __forceinline__ void flush_stage(uint4 *stage, int b0, int b1, unsigned char *dst, int lane) {
+  __syncwarp();
+  const int v0 = (b0 + 15) >> 4, v1 = b1 >> 4;
+  const uint16_t *s16 = reinterpret_cast<const uint16_t *>(stage);
+  uint16_t *d16 = reinterpret_cast<uint16_t *>(dst);
+  if (v0 <= v1) {
+    if (v1 > v0) {
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      __syncwarp();
+      if (lane == 0) {
+        const unsigned sa = (unsigned)__cvta_generic_to_shared(stage + v0);
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n"
+                     ::"l"(dst + 16 * v0), "r"(sa), "r"(16 * (v1 - v0)) : "memory");
+        asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+      }
+    }
+    const int h = (v0 << 3) - (b0 >> 1);
+    if (lane < h) d16[(b0 >> 1) + lane] = s16[(b0 >> 1) + lane];
+    const int t0 = v1 << 3, tn = (b1 >> 1) - t0;
+    if (lane < tn) d16[t0 + lane] = s16[t0 + lane];
+  } else {
+    const int n = (b1 - b0) >> 1;
+    if (lane < n) d16[(b0 >> 1) + lane] = s16[(b0 >> 1) + lane];
+  }
+  __syncwarp();
+}
+
+// a window as its groups read it (per warp, set once per window): band k's first record,
+// XA and XB in lane k's registers
+struct WinG {
+  const uint32_t *mw;   // merge bits, bits before the window cleared
+  const int *mp;        //   their exclusive prefix popcounts
+  int bgo;              // bit of record q = q + bgo
+  int lo, hi, nslot;    // records [lo, hi), bands
+  int ta, XA, XB;       // lane k: band k
+};
+
+// records [max(g, lo), min(g + GW, hi)) of group g (relative to T0), by one warp; d = the lane's
+// two records in the warp's staging buffer
+__device__ __forceinline__ void cta_group(const WinG &W, const Pts &pt, uint4 *stage, uint32_t *d, unsigned char *dst, int g,
+                                          int lane) {
+  const unsigned FULL = 0xffffffffu, lt = (1u << lane) - 1u;
+  const int r0 = 2 * lane;
+  const int q0 = g + r0, q1 = q0 + 1;
+  const bool full = W.lo <= g && W.hi >= g + GW;
+  const bool va = full || (q0 >= W.lo && q0 < W.hi), vb = full || (q1 >= W.lo && q1 < W.hi);
+  const int bg = g + W.bgo;
+  const int b0 = bg + r0, b1 = b0 + 1;
+  const bool aa = va && ((W.mw[b0 >> 5] >> (b0 & 31)) & 1u);
+  const bool ab = vb && ((W.mw[b1 >> 5] >> (b1 & 31)) & 1u);
+  const unsigned ma = __ballot_sync(FULL, aa), mb = __ballot_sync(FULL, ab);
+  const int Cg = W.mp[bg >> 5] + __popc(W.mw[bg >> 5] & ~mask_ge(bg & 31));
+  const int I0 = Cg + __popc(ma & lt) + __popc(mb & lt), I1 = I0 + (aa ? 1 : 0);
+  // bands: kg holds g; band starts inside (g, g + GW)
+  const int kg = __popc(__ballot_sync(FULL, lane < W.nslot && W.ta <= g)) - 1;
+  const int dp = W.ta - g;
+  const bool inb = lane < W.nslot && dp > 0 && dp < GW;
+  int XA0, XB0, XA1, XB1;
+  if (__ballot_sync(FULL, inb) == 0u) {   // one band holds the whole group
+    XA0 = XA1 = __shfl_sync(FULL, W.XA, kg & 31);
+    XB0 = XB1 = __shfl_sync(FULL, W.XB, kg & 31);
+  } else {
+    const unsigned lo32 = __reduce_or_sync(FULL, inb && dp < 32 ? 1u << dp : 0u);
+    const unsigned hi32 = __reduce_or_sync(FULL, inb && dp >= 32 ? 1u << (dp - 32) : 0u);
+    const int k0 = kg + __popc(lo32 & mask_le(r0)) + __popc(hi32 & mask_le(r0 - 32));
+    const int k1 = kg + __popc(lo32 & mask_le(r0 + 1)) + __popc(hi32 & mask_le(r0 - 31));
+    XA0 = __shfl_sync(FULL, W.XA, k0 & 31); XB0 = __shfl_sync(FULL, W.XB, k0 & 31);
+    XA1 = __shfl_sync(FULL, W.XA, k1 & 31); XB1 = __shfl_sync(FULL, W.XB, k1 & 31);
+  }
+  const int pa = XA0 + I0, pb = XB0 + q0 - I0;
+  const int pa1 = XA1 + I1, pb1 = XB1 + q1 - I1;
+  {
+    uint32_t f[12];
+    if (va) tri_words(get_point(pt, pa), get_point(pt, aa ? pa + 1 : pb + 1), get_point(pt, pb), f);
+    stage_wait(lane);   // the warp's previous bulk copy has read the staging buffer
+    if (va) put_first(d, f);
+  }
+  if (vb) {
+    uint32_t f[12];
+    tri_words(get_point(pt, pa1), get_point(pt, ab ? pa1 + 1 : pb1 + 1), get_point(pt, pb1), f);
+    put_second(d, f);
+  }
+  if (full) {
+    __syncwarp();
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    __syncwarp();
+    if (lane == 0) {
+      const unsigned sa = (unsigned)__cvta_generic_to_shared(stage);
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(dst), "r"(sa), "n"(GW * REC) : "memory");
+      asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+    }
+  } else {
+    const int wlo = W.lo > g ? W.lo : g, whi = W.hi < g + GW ? W.hi : g + GW;
+    flush_stage(stage, (wlo - g) * REC, (whi - g) * REC, dst, lane);
+  }
+}
+
+__global__ void __launch_bounds__(EMIT_T, LMM_SPAN_MINB) k_emit_span(TriParams P, int64_t first, int64_t count, unsigned char *out,
+                                                         int64_t nspan, int span, int pcw) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  SpanSm &S = *reinterpret_cast<SpanSm *>(smem);
+  const unsigned FULL = 0xffffffffu;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  const int BIG = 0x3fffffff;
+  Pts pt;
+  pt.xy = reinterpret_cast<float2 *>(smem + sizeof(SpanSm));
+  pt.z = reinterpret_cast<float *>(pt.xy + pcw);
+  pt.cap = pcw;
+  const int64_t last = first + count;
+  const int64_t bend = last < P.n_tri_band ? last : P.n_tri_band;
+  for (int64_t u = blockIdx.x; u < nspan; u += gridDim.x) {
+    const int64_t T0 = first + u * span;
+    const int64_t T1 = T0 + span < bend ? T0 + span : bend;
+    int64_t snext = 0;   // warp 0: the next candidate band
+    enum { B_OK, B_END, B_NOFIT };
+    // warp 0: build the window of whole bands from snext into buffer wb -- slots, merge words,
+    // band parameters -- and start the cp.async of its loop entries, arcs and start vertices
+    auto build = [&](int wb) -> int {
+      for (;;) {
+        const int64_t c = snext + lane;
+        int64_t b = INT64_MAX, e = INT64_MAX;
+        if (c < P.S) { b = P.strut_off[c]; e = P.strut_off[c + 1]; }
+        const unsigned stopm = __ballot_sync(FULL, b >= T1);
+        const int nst = stopm ? __ffs(stopm) - 1 : 32;
+        const bool live = lane < nst && e > b;
+        const unsigned livem = __ballot_sync(FULL, live);
+        if (!livem) {
+          if (nst < 32) return B_END;   // every further band starts at or after T1
+          snext += 32;
+          continue;
+        }
+        int nA = 0, nB = 0, kB = 0, lAc = 0, lBc = 0;
+        unsigned aA = 0u, aB = 0u, pA = 0u, pB = 0u;
+        float4 x2 = make_float4(0.f, 0.f, 0.f, 0.f), x3 = x2;
+        if (live) {
+          const float4 *q = reinterpret_cast<const float4 *>(P.brec + c);
+          const float4 x0 = __ldg(q), x1 = __ldg(q + 1);
+          x2 = __ldg(q + 2); x3 = __ldg(q + 3);
+          nA = __float_as_int(x0.x); nB = __float_as_int(x0.y); kB = __float_as_int(x0.z); lAc = __float_as_int(x0.w);
+          lBc = __float_as_int(x1.x); aA = __float_as_uint(x1.y); aB = __float_as_uint(x1.z); pA = __float_as_uint(x1.w);
+          pB = __float_as_uint(x2.x);
+        }
+        const int npts = live ? min(nA + nB + 2, 2047) : 0;
+        const int nent = live ? min(rec_cnt(lAc) + rec_cnt(lBc), 255) : 0;
+        int v = npts | (nent << 16);
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(FULL, v, o);
+          if (lane >= o) v += y;
+        }
+        const int cp = v & 0xffff, ce = v >> 16;
+        const int rk = __popc(livem & lt);
+        const bool fit = live && cp <= pcw && ce <= SEC && rk < SNB;
+        const unsigned fitm = __ballot_sync(FULL, fit);
+        if (!fitm) return B_NOFIT;
+        const int lastf = 31 - __clz(fitm);
+        const int pos = cp - npts;
+        const int cex = ce - nent;
+        int i0 = 0;
+        if (fit && b < T0) i0 = merge_rank(P, b, T0);
+        const int own = fit ? nA - i0 : 0;
+        int ca = own;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(FULL, ca, o);
+          if (lane >= o) ca += y;
+        }
+        const int cAn = ca - own;   // A-advances of the window before the band
+        const int ta0 = __shfl_sync(FULL, (int)((b > T0 ? b : T0) - T0), __ffs(fitm) - 1);
+        if (fit) {
+          const int ta = (int)((b > T0 ? b : T0) - T0);
+          S.s_ta[wb][rk] = ta;
+          S.s_XA[wb][rk] = pos + i0 - cAn;
+          S.s_XB[wb][rk] = pos + nA + 1 + (b < T0 ? (int)(T0 - b) - i0 : 0) - ta + cAn;
+          S.b_pos[rk] = pos; S.b_flx[rk] = cp - npts - 2 * rk; S.b_kB[rk] = kB; S.b_nA[rk] = nA; S.b_nB[rk] = nB;
+          S.b_e0[rk] = cex; S.b_cntA[rk] = rec_cnt(lAc); S.b_fA[rk] = rec_first(lAc); S.b_fB[rk] = rec_first(lBc);
+          S.b_aA[rk] = aA; S.b_aB[rk] = aB; S.b_pA[rk] = pA; S.b_pB[rk] = pB;
+          S.b_c[rk][0] = x2.y; S.b_c[rk][1] = x2.z; S.b_c[rk][2] = x2.w;
+          S.b_c[rk][3] = x3.x; S.b_c[rk][4] = x3.y; S.b_c[rk][5] = x3.z;
+          for (int x = 0; x < nent; x++) S.e_band[cex + x] = (uint8_t)rk;
+        }
+        const int K = __popc(fitm);
+        const int Ew = __shfl_sync(FULL, ce, lastf);
+        int tend;
+        {
+          const int64_t el = __shfl_sync(FULL, e, lastf);
+          tend = (int)((el < T1 ? el : T1) - T0);
+        }
+        snext += lastf + 1;
+        // merge bits of the window's records (bits before ta0 cleared) and their prefix counts,
+        // from the word of its first group
+        const int g0 = ta0 & ~(GW - 1);
+        const long long wb0 = (T0 + g0) >> 5;
+        const long long wl = (T0 + tend - 1) >> 5;
+        uint32_t mwv[2];
+#pragma unroll
+        for (int r = 0; r < 2; r++) {
+          const int i = lane + 32 * r;
+          uint32_t m = wb0 + i <= wl ? __ldg(&P.mbits[wb0 + i]) : 0u;
+          const long long cut = T0 + ta0 - 32 * (wb0 + i);
+          if (cut >= 32) m = 0u;
+          else if (cut > 0) m &= 0xffffffffu << cut;
+          mwv[r] = m;
+        }
+        int x0 = __popc(mwv[0]), x1 = __popc(mwv[1]);
+        const int s0 = x0, s1 = x1;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y0 = __shfl_up_sync(FULL, x0, o), y1 = __shfl_up_sync(FULL, x1, o);
+          if (lane >= o) { x0 += y0; x1 += y1; }
+        }
+        const int tot0 = __shfl_sync(FULL, x0, 31);
+        if (lane < SMW) { S.mw[wb][lane] = mwv[0]; S.mp[wb][lane] = x0 - s0; }
+        if (lane + 32 < SMW) { S.mw[wb][lane + 32] = mwv[1]; S.mp[wb][lane + 32] = tot0 + x1 - s1; }
+        if (lane == 0) { S.wb0[wb] = wb0; S.w_ta0[wb] = ta0; S.w_tend[wb] = tend; S.w_K[wb] = K; }
+        {
+          const int Pn = __shfl_sync(FULL, cp, lastf) - 2 * K;
+          if (lane == 0) { S.w_Pn[wb] = Pn; S.w_Ew[wb] = Ew; }
+        }
+        __syncwarp();
+        // stage the loop entries, then (once they are in) their arcs and start vertices
+        for (int e2 = lane; e2 < Ew; e2 += 32) {
+          const int k = S.e_band[e2];
+          const int x = e2 - S.b_e0[k];
+          const bool rB = x >= S.b_cntA[k];
+          const unsigned ab = rB ? S.b_aB[k] : S.b_aA[k];
+          cp_async<16>(reinterpret_cast<float4 *>(&S.ent[e2]) + 4,
+                       P.loop + 2 * (int64_t)ab + (rB ? S.b_fB[k] + x - S.b_cntA[k] : S.b_fA[k] + x));
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+        asm volatile("cp.async.wait_all;\n" ::: "memory");
+        for (int e2 = lane; e2 < Ew; e2 += 32) {
+          const int k = S.e_band[e2];
+          const bool rB = e2 - S.b_e0[k] >= S.b_cntA[k];
+          float4 *slot = reinterpret_cast<float4 *>(&S.ent[e2]);
+          const LoopRec L = *reinterpret_cast<const LoopRec *>(slot + 4);
+          const float4 *ar = reinterpret_cast<const float4 *>(P.arc + (rB ? S.b_aB[k] : S.b_aA[k]) + le_arc(L.arc_fwd));
+          cp_async<16>(slot, ar);
+          cp_async<16>(slot + 1, ar + 1);
+          cp_async<16>(slot + 2, ar + 2);
+          cp_async<16>(slot + 3, P.vert + 2 * (int64_t)(rB ? S.b_pB[k] : S.b_pA[k]) + le_vid(L.cum));
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+        return B_OK;
+      }
+    };
+    // warp 0, no window built ahead: bands too large for a window go through the band path
+    // until a window is built or the span is done; returns the action for all warps
+    auto settle = [&](int st, int wb) -> int {
+      for (;;) {
+        if (st == B_OK) return ACT_WINDOW;
+        if (st == B_END) return ACT_DONE;
+        int64_t sl;
+        int te;
+        {
+          const int64_t c = snext + lane;
+          int64_t b = INT64_MAX, e = INT64_MAX;
+          if (c < P.S) { b = P.strut_off[c]; e = P.strut_off[c + 1]; }
+          const unsigned livem = __ballot_sync(FULL, b < T1 && e > b);
+          const int cl = __ffs(livem) - 1;   // a live band exists (NOFIT)
+          sl = snext + cl;
+          const int64_t el = __shfl_sync(FULL, e, cl);
+          te = (int)((el < T1 ? el : T1) - T0);
+        }
+        (void)te;
+        WarpRing &w = *reinterpret_cast<WarpRing *>(&S.ent[0]);
+        BandRec &lrec = *reinterpret_cast<BandRec *>(&S.b_c[0][0]);
+        long long &lbase = *reinterpret_cast<long long *>(&S.b_pos[0]);
+        stage_wait(lane);
+        fetch_rec(P, (int)sl, lrec, lbase, lane);
+        cp_async_wait_warp();
+        fetch_entries(P, w, lrec, lane);
+        cp_async_wait_warp();
+        fetch_arcs(P, w, lrec, lane);
+        cp_async_wait_warp();
+        emit_band(P, w, pt, lrec, lbase, first, T0, T1, out, lane, NoPrefetch());
+        stage_wait(lane);
+        __syncwarp();
+        snext = sl + 1;
+        st = build(wb);
+      }
+    };
+    int wb = 0;
+    if (warp == 0) {
+      snext = P.cmap[T0 / TPC];
+      for (;;) {
+        const int64_t c = snext + 1 + lane;
+        const unsigned m = __ballot_sync(FULL, c < P.S && P.strut_off[c] <= T0);
+        snext += __popc(m);
+        if (m != FULL) break;
+      }
+      const int act = settle(build(0), 0);
+      asm volatile("cp.async.wait_all;\n" ::: "memory");
+      if (lane == 0) S.act = act;
+      if (lane < SMW) S.bm[lane] = 0u;
+      if (lane + 32 < SMW) S.bm[lane + 32] = 0u;
+    }
+    __syncthreads();
+    while (S.act == ACT_WINDOW) {
+      const int Ew = S.w_Ew[wb], Pn = S.w_Pn[wb];
+      // ======== the window's entries (thread = entry): Eq. 12 parameters, point placement ========
+      float4 vq = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (tid < Ew) {
+        const int k = S.e_band[tid];
+        const bool rB = tid - S.b_e0[k] >= S.b_cntA[k];
+        const float4 *slot = reinterpret_cast<const float4 *>(&S.ent[tid]);
+        const LoopRec L = *reinterpret_cast<const LoopRec *>(slot + 4);
+        const ArcRec A = lds_arc(reinterpret_cast<const ArcRec *>(slot));
+        vq = slot[3];
+        const int N = le_N(L.arc_fwd), ci = le_cum(L.cum);
+        const int pos = S.b_pos[k], nA = S.b_nA[k], nB = S.b_nB[k], kB = S.b_kB[k];
+        PtEnt E;
+        E.t0 = A.t0; E.dq = __fdividef(A.dt, (float)N);
+        E.ox = A.ox; E.oy = A.oy; E.oz = A.oz; E.ax = A.ax; E.ay = A.ay; E.az = A.az;
+        E.bx = A.bx; E.by = A.by; E.bz = A.bz;
+        E.cx = S.b_c[k][rB ? 3 : 0]; E.cy = S.b_c[k][rB ? 4 : 1]; E.cz = S.b_c[k][rB ? 5 : 2];
+        E.nf = N | (le_fwd(L.arc_fwd) << 16);
+        if (!rB) {
+          E.P0 = pos + ci; E.wj = BIG; E.dupj = ci == 0 ? 0 : -1; E.off = nA;
+        } else {
+          const int bs = pos + nA + 1;
+          E.off = nB;
+          if (ci >= kB) { E.P0 = bs + ci - kB; E.wj = BIG; E.dupj = ci == kB ? 0 : -1; }
+          else {
+            E.P0 = bs + ci - kB + nB;
+            if (ci + N > kB) { E.wj = kB - ci; E.dupj = kB - ci; } else { E.wj = BIG; E.dupj = -1; }
+          }
+        }
+        const int est = S.b_flx[k] + (rB ? nA : 0) + ci;
+        E.pad = est;
+        S.ent[tid] = E;
+        atomicOr(&S.bm[est >> 5], 1u << (est & 31));
+      }
+      __syncthreads();
+      // ======== the window's points, flattened (entry of point p from the entry-start bitmap) ========
+      {
+        // exclusive prefix popcounts of the bitmap, per warp in registers (lane i: words i, i + 32)
+        const uint32_t m0 = lane < SMW ? S.bm[lane] : 0u, m1 = lane + 32 < SMW ? S.bm[lane + 32] : 0u;
+        int x0 = __popc(m0), x1 = __popc(m1);
+        const int s0 = x0, s1 = x1;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y0 = __shfl_up_sync(FULL, x0, o), y1 = __shfl_up_sync(FULL, x1, o);
+          if (lane >= o) { x0 += y0; x1 += y1; }
+        }
+        x0 -= s0;
+        x1 += __shfl_sync(FULL, x0 + s0, 31) - s1;
+        for (int pb = warp * 32; pb < Pn; pb += EMIT_T) {
+          const int p = pb + lane;
+          const int wd = p >> 5;   // warp-uniform
+          const int bpv = __shfl_sync(FULL, wd < 32 ? x0 : x1, wd & 31);
+          const uint32_t bmv = __shfl_sync(FULL, wd < 32 ? m0 : m1, wd & 31);
+          if (p < Pn) {
+            const int e = bpv + __popc(bmv & mask_le(lane)) - 1;
+            const float4 *q = reinterpret_cast<const float4 *>(&S.ent[e]);
+            const float4 e0 = q[0], e1 = q[1], e2 = q[2], e3 = q[3];
+            const int4 e4 = reinterpret_cast<const int4 *>(q)[4];   // wj dupj off est
+            const int j = p - e4.w;
+            const int nf = __float_as_int(e3.z), P0 = __float_as_int(e3.w);
+            const int N = nf & 0xffff;
+            const int jj = (nf >> 16) ? j : N - j;
+            float t = __fmaf_rn((float)jj, e0.y, e0.x);
+            t = __fmaf_rn(-LMM_TWO_PI_F, rintf(__fmul_rn(t, 1.0f / LMM_TWO_PI_F)), t);
+            float sn, cs;
+            __sincosf(t, &sn, &cs);
+            // e0 = t0 dq ox oy, e1 = oz ax ay az, e2 = bx by bz cx, e3 = cy cz nf P0 (PtEnt)
+            const f3 pq = F3(__fadd_rn(e2.w, __fmaf_rn(e1.y, sn, __fmaf_rn(e2.x, cs, e0.z))),
+                             __fadd_rn(e3.x, __fmaf_rn(e1.z, sn, __fmaf_rn(e2.y, cs, e0.w))),
+                             __fadd_rn(e3.y, __fmaf_rn(e1.w, sn, __fmaf_rn(e2.z, cs, e1.x))));
+            const int ps = P0 + j - (j >= e4.x ? e4.z : 0);
+            put_point(pt, ps, pq);
+            if (j == e4.y) put_point(pt, ps + e4.z, pq);
+          }
+        }
+      }
+      __syncthreads();
+      // entry start points are the shared meta-mesh vertices, bit for bit (watertight seams)
+      if (tid < Ew) {
+        const PtEnt &E = S.ent[tid];
+        const f3 q = F3(__fadd_rn(E.cx, vq.x), __fadd_rn(E.cy, vq.y), __fadd_rn(E.cz, vq.z));
+        put_point(pt, E.P0, q);
+        if (E.dupj == 0) put_point(pt, E.P0 + E.off, q);
+      }
+      if (tid == 0) S.gnext = 0;
+      __syncthreads();
+      // ======== the window's groups (first and last partial): warp 0 first builds the next
+      // window and starts its fetches; the groups are taken from a counter ========
+      {
+        WinG W;
+        W.mw = S.mw[wb]; W.mp = S.mp[wb];
+        W.bgo = (int)(T0 - 32 * S.wb0[wb]);
+        W.lo = S.w_ta0[wb]; W.hi = S.w_tend[wb]; W.nslot = S.w_K[wb];
+        W.ta = lane < W.nslot ? S.s_ta[wb][lane] : BIG;
+        W.XA = S.s_XA[wb][lane]; W.XB = S.s_XB[wb][lane];
+        const int g0 = W.lo & ~(GW - 1);
+        const int ng = (W.hi - g0 + GW - 1) / GW;
+        uint4 *stage = S.stage[warp];
+        uint32_t *d = reinterpret_cast<uint32_t *>(stage) + 25 * lane;
+        unsigned char *dst0 = out + (T0 + g0 - first) * REC;
+        if (warp == 0) {
+          if (lane < SMW) S.bm[lane] = 0u;
+          if (lane + 32 < SMW) S.bm[lane + 32] = 0u;
+          // (a band too large for a window waits for the barrier: the band path uses the point cache)
+          const int st = build(wb ^ 1);
+          if (lane == 0) S.act = st == B_OK ? ACT_WINDOW : (st == B_END ? ACT_DONE : ACT_LONG);
+        }
+        for (;;) {
+          int m = 0;
+          if (lane == 0) m = atomicAdd(&S.gnext, 1);
+          m = __shfl_sync(FULL, m, 0);
+          if (m >= ng) break;
+          cta_group(W, pt, stage, d, dst0 + (int64_t)m * GW * REC, g0 + m * GW, lane);
+        }
+        if (warp == 0) asm volatile("cp.async.wait_all;\n" ::: "memory");   // the next window's entry data
+      }
+      __syncthreads();
+      wb ^= 1;
+      if (S.act == ACT_LONG) {
+        if (warp == 0) {
+          const int act = settle(B_NOFIT, wb);
+          asm volatile("cp.async.wait_all;\n" ::: "memory");
+          if (lane == 0) S.act = act;
+          if (lane < SMW) S.bm[lane] = 0u;
+          if (lane + 32 < SMW) S.bm[lane + 32] = 0u;
+        }
+        __syncthreads();
+      }
+    }
+    __syncthreads();
+  }
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+}
+
 // units: bands [s0, s1) then holes [g0, g1) intersecting [first, last)
 __global__ void __launch_bounds__(EMIT_T, 8) k_emit(TriParams P, int64_t first, int64_t count, unsigned char *out,
                                                  int64_t s0, int64_t s1, int64_t g0, int64_t g1, int pcap) {
@@ -921,7 +1441,7 @@ __global__ void __launch_bounds__(EMIT_T, 8) k_emit(TriParams P, int64_t first, 
     if (u < nb) {
       const bool more = u + nw < nb;
       BandRec &nx = rec[warp][cb ^ 1];
-      emit_band(P, w, pt, rec[warp][cb], rbase[warp][cb], first, last, out, lane, [&](int stage) {
+      emit_band(P, w, pt, rec[warp][cb], rbase[warp][cb], first, first, last, out, lane, [&](int stage) {
         if (stage == 0) {
           if (more) fetch_rec(P, (int)(s0 + u + nw), nx, rbase[warp][cb ^ 1], lane);
           return;
@@ -1033,11 +1553,10 @@ int triangulate_count(lmm_ctx *c) {
   return LMM_OK;
 }
 
-int triangulate_emit(lmm_ctx *c, int64_t first, int64_t count, void *out_dev, cudaStream_t st) {
-  if (count <= 0) return LMM_OK;
-  TriParams P = make_params(c);
-  // point cache sized to the bands of this triangulation: whole-band emission when a band's
-  // rings fit, at the occupancy the cache allows (160 points: 8 CTAs/SM)
+// the band path of k_emit for [first, last) (bands grid-strided per warp, then holes): s0/s1
+// = bands, g0/g1 = holes intersecting the range (from the chunk map)
+static int launch_band_path(lmm_ctx *c, const TriParams &P, int64_t first, int64_t count, void *out_dev,
+                            cudaStream_t st, bool bands) {
   int pcap = PCAP_MIN;
   {
     const int64_t live = c->S > 0 ? c->S : 1;
@@ -1045,9 +1564,9 @@ int triangulate_emit(lmm_ctx *c, int64_t first, int64_t count, void *out_dev, cu
     while (pcap < PCAP_MAX && mean + 2.0 > pcap - 4) pcap = pcap + 160 < PCAP_MAX ? pcap + 160 : PCAP_MAX;
   }
   const size_t smem = (size_t)ring_bytes(pcap) * EW;
-  // the opt-in shared-memory limit and the occupancy are per device: kept in the context
   if (!c->emit_attr_set) {
     CUDA_TRY(cudaFuncSetAttribute(k_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, ring_bytes(PCAP_MAX) * EW));
+    CUDA_TRY(cudaFuncSetAttribute(k_emit_span, cudaFuncAttributeMaxDynamicSharedMemorySize, span_bytes(SPCW_MAX)));
     c->emit_attr_set = true;
   }
   int &occ = c->emit_occ[pcap == PCAP_MAX ? 7 : (pcap - PCAP_MIN) / 160];
@@ -1055,8 +1574,6 @@ int triangulate_emit(lmm_ctx *c, int64_t first, int64_t count, void *out_dev, cu
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_emit, EMIT_T, smem));
     if (occ < 1) occ = 1;
   }
-  // bands and holes intersecting [first, last): the chunk map at the chunk holding
-  // `first` bounds the first unit, the one of the chunk after `last - 1` the last unit
   const int64_t last = first + count;
   const int64_t nch = (c->n_tri + TPC - 1) / TPC;
   int64_t s0 = c->S, s1 = c->S, g0 = c->H, g1 = c->H;
@@ -1067,7 +1584,7 @@ int triangulate_emit(lmm_ctx *c, int64_t first, int64_t count, void *out_dev, cu
   if (cn < nch) CUDA_TRY(cudaMemcpyAsync(hm + 1, (int *)c->cmap.p + cn, sizeof(int), cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
   const int64_t cna = cn * TPC;
-  if (first < c->n_tri_band) {
+  if (bands && first < c->n_tri_band) {
     s0 = hm[0];
     s1 = (cn < nch && cna < c->n_tri_band) ? (int64_t)hm[1] + 1 : c->S;
   }
@@ -1077,13 +1594,52 @@ int triangulate_emit(lmm_ctx *c, int64_t first, int64_t count, void *out_dev, cu
   }
   if (s1 < s0) s1 = s0;
   if (g1 < g0) g1 = g0;
-  int64_t units = (s1 - s0) + (g1 - g0);
+  const int64_t units = (s1 - s0) + (g1 - g0);
+  if (units <= 0) return LMM_OK;
   int64_t grid = (int64_t)c->n_sm * occ;
-  int64_t need = (units + EW - 1) / EW;
+  const int64_t need = (units + EW - 1) / EW;
   if (grid > need) grid = need;
   if (grid < 1) grid = 1;
-  KTimer t(c, LMM_K_EMIT);
   (c->n_launch++), k_emit<<<(unsigned)grid, EMIT_T, smem, st>>>(P, first, count, (unsigned char *)out_dev, s0, s1, g0, g1, pcap);
   CUDA_TRY(cudaGetLastError());
+  return LMM_OK;
+}
+
+int triangulate_emit(lmm_ctx *c, int64_t first, int64_t count, void *out_dev, cudaStream_t st) {
+  if (count <= 0) return LMM_OK;
+  TriParams P = make_params(c);
+  KTimer t(c, LMM_K_EMIT);
+  // CTA windows when several mean bands fit a window (short bands: per-band work dominates the
+  // band path), else the band path; hole fans always take the band path
+  const int64_t live = c->S > 0 ? c->S : 1;
+  const double mean = (double)c->n_tri_band / (double)live;
+  int pcw = 768;
+  if (const char *ev = getenv("LMM_SPCW")) { const int v = atoi(ev); if (v >= 256 && v <= SPCW_MAX) pcw = v; }
+  int span = SPAN_CTA;
+  if (const char *ev = getenv("LMM_SPAN")) { const int v = atoi(ev); if (v >= GW && v % GW == 0) span = v; }
+  // (measured on octet100: CE 1e-2, 48 triangles per band: CTA windows 19.1 ms vs band path
+  // 24.1 ms; CE 1e-3, 144 per band: 44.2 vs 42.8 ms)
+  bool use_span = mean <= 100.0;
+  if (const char *ev = getenv("LMM_EMIT_PATH")) use_span = atoi(ev) == 1 ? true : (atoi(ev) == 0 ? false : use_span);
+  const int64_t last = first + count;
+  if (!use_span || first >= c->n_tri_band) return launch_band_path(c, P, first, count, out_dev, st, true);
+  if (!c->emit_attr_set) {
+    CUDA_TRY(cudaFuncSetAttribute(k_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, ring_bytes(PCAP_MAX) * EW));
+    CUDA_TRY(cudaFuncSetAttribute(k_emit_span, cudaFuncAttributeMaxDynamicSharedMemorySize, span_bytes(SPCW_MAX)));
+    c->emit_attr_set = true;
+  }
+  const size_t smem = (size_t)span_bytes(pcw);
+  int &occ = c->emit_occ[8 + pcw / 128];
+  if (occ == 0) {
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_emit_span, EMIT_T, smem));
+    if (occ < 1) occ = 1;
+  }
+  const int64_t bend = last < c->n_tri_band ? last : c->n_tri_band;
+  const int64_t nspan = (bend - first + span - 1) / span;
+  int64_t grid = (int64_t)c->n_sm * occ;
+  if (grid > nspan) grid = nspan;
+  (c->n_launch++), k_emit_span<<<(unsigned)grid, EMIT_T, smem, st>>>(P, first, bend - first, (unsigned char *)out_dev, nspan, span, pcw);
+  CUDA_TRY(cudaGetLastError());
+  if (last > c->n_tri_band) return launch_band_path(c, P, first, count, out_dev, st, false);   // the hole fans
   return LMM_OK;
 }
