@@ -927,6 +927,7 @@ __device__ __forceinline__ unsigned mask_le(int x) { return x < 0 ? 0u : (x >= 3
 struct NoPrefetch {
   __device__ void operator()(int) const {}
 };
+__device__ __forceinline__ void prefetch_l2(const void *p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 
 
 // ---------------------------------------------------------------------------------
@@ -968,11 +969,13 @@ struct __align__(16) SpanSm {
   // the built window's bands, for its entry set-up
   int b_pos[SNB], b_flx[SNB], b_kB[SNB], b_nA[SNB], b_nB[SNB], b_e0[SNB], b_cntA[SNB], b_fA[SNB], b_fB[SNB];
   unsigned b_aA[SNB], b_aB[SNB], b_pA[SNB], b_pB[SNB];
-  float b_c[SNB][6];
+  alignas(16) float b_c[SNB][6];      // node centres (doubles as the band path's record)
   uint8_t e_band[SEC];
   uint32_t bm[SMW];                   // flattened point p starts an entry
   int act, gnext;
 };
+static_assert(offsetof(SpanSm, ent) % 16 == 0 && offsetof(SpanSm, stage) % 16 == 0 && offsetof(SpanSm, b_c) % 16 == 0,
+              "cp.async / bulk-copy operands are 16-byte aligned");
 __host__ __device__ constexpr int span_bytes(int pcw) { return (int)((sizeof(SpanSm) + (size_t)pcw * 12 + 15) / 16 * 16); }
 
 // staged bytes [b0, b1) of a group -> dst + [b0, b1) (dst 16-byte aligned), as flush_group
@@ -1099,6 +1102,9 @@ __global__ void __launch_bounds__(EMIT_T, LMM_SPAN_MINB) k_emit_span(TriParams P
         const int64_t c = snext + lane;
         int64_t b = INT64_MAX, e = INT64_MAX;
         if (c < P.S) { b = P.strut_off[c]; e = P.strut_off[c + 1]; }
+        // the next candidates towards L2 for the build after this one
+        if (lane < 16) prefetch_l2(P.brec + snext + 32 + 2 * lane);
+        else if (lane < 19) prefetch_l2(P.strut_off + snext + 32 + 16 * (lane - 16));
         const unsigned stopm = __ballot_sync(FULL, b >= T1);
         const int nst = stopm ? __ffs(stopm) - 1 : 32;
         const bool live = lane < nst && e > b;
@@ -1383,9 +1389,10 @@ __global__ void __launch_bounds__(EMIT_T, LMM_SPAN_MINB) k_emit_span(TriParams P
           const int st = build(wb ^ 1);
           if (lane == 0) S.act = st == B_OK ? ACT_WINDOW : (st == B_END ? ACT_DONE : ACT_LONG);
         }
+        const unsigned gna = (unsigned)__cvta_generic_to_shared(&S.gnext);
         for (;;) {
           int m = 0;
-          if (lane == 0) m = atomicAdd(&S.gnext, 1);
+          if (lane == 0) asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(m) : "r"(gna) : "memory");
           m = __shfl_sync(FULL, m, 0);
           if (m >= ng) break;
           cta_group(W, pt, stage, d, dst0 + (int64_t)m * GW * REC, g0 + m * GW, lane);
