@@ -1,6 +1,7 @@
 """Parity at BASELINE.json's full single-GPU sizes, in the launch configuration bench.py
 times (the meta-mesh of every node in one lmm_build_metamesh, the triangles emitted into a
-device buffer in bench.py's 2^28-triangle chunks), CE = 1e-3:
+device buffer in bench.py's 2^28-triangle chunks), CE = 1e-3 (and octet100 at CE 1e-2, whose
+48-triangle bands take the CTA-window emit path):
   octet100 -- configs[1]: 100^3-cell graded octet truss, 24.12M struts (the headline bench);
   bcc250   -- configs[3]: one GPU's 250^3-cell block of the 1B-strut BCC lattice, 125M struts;
   stoch290 -- configs[2]: stochastic lattice, degrees 3..30, 102M struts;
@@ -31,8 +32,9 @@ N_NODES_SAMPLE = 4000
 N_STRUTS_SAMPLE = 4000
 
 
-@pytest.fixture(scope="module", params=[("octet100", 1e-3), ("bcc250", 1e-3), ("stoch290", 1e-3), ("octet160", 1e-4)],
-                ids=["octet100", "bcc250", "stoch290", "octet160-ce1e-4"])
+@pytest.fixture(scope="module", params=[("octet100", 1e-3), ("bcc250", 1e-3), ("stoch290", 1e-3), ("octet160", 1e-4),
+                                        ("octet100", 1e-2)],
+                ids=["octet100", "bcc250", "stoch290", "octet160-ce1e-4", "octet100-ce1e-2"])
 def full(request):
     import torch
     from paper_2405_15197_b200 import MetaMesher
