@@ -80,6 +80,11 @@ struct alignas(16) WSCore {
   uint32_t vmask[MAXV];
 };
 
+// junction pre-test (part_a) for the buckets of at least this many sides (degree >= 13 by
+// default: on the degree 9-12 octet nodes the pre-test costs more than it saves)
+#ifndef LMM_PRE_MAXS
+#define LMM_PRE_MAXS 17
+#endif
 template <int MAXS, int MAXJ, int MAXV, int MAXA, int MAXLE, int MAXH>
 struct alignas(16) WS_A : WSCore<MAXS, MAXV> {
   // side k as broadcast pairs for the two-root junction test: (wx,wx,wy,wy), (wz,wz,-e,-e)
@@ -88,6 +93,12 @@ struct alignas(16) WS_A : WSCore<MAXS, MAXV> {
   float4 jp[MAXJ];   // junction x, y, z; .w = vertex id once clustered (roots)
   uint32_t jabc[MAXJ];
   int jlab[MAXJ];
+  // warp-per-node buckets: the roots that pass a pre-test against the triple's nearest sides,
+  // queued (ring buffer) for the full side test in batches of 32 (see part_a)
+  static constexpr int QA = MAXS >= LMM_PRE_MAXS ? 96 : 1;
+  uint32_t nn[MAXS];     // the two struts nearest in direction to strut k (bytes 0, 1)
+  float4 jq[QA];         // queued root: x, y, z, solver tau
+  uint32_t jqc[QA];      // its jabc code | sphere << 26 | SHORT << 27
 };
 
 #ifndef LMM_QL
@@ -250,7 +261,120 @@ __device__ void part_a(cg::thread_block_tile<G> &g, WS &ws, const MMParams &P, i
 
   PHASE_MARK(1);
   // ---- 2. triple junctions, lexicographic (a<b<c), root-minor ---------------------
-  if (status == 0 && d > 0) {
+  // Warp-per-node buckets: a root's validity is an AND over the sides, so each root is first
+  // tested against the (up to six) struts nearest in direction to its triple's sides -- its
+  // likely violators -- and only the survivors, queued in (triple, root) order, take the full
+  // side loop, 32 at a time.  Same operations on the same values: the decisions, the junction
+  // order and the first error are those of the all-sides test below.
+  constexpr bool PRE = G == 32 && WS::QA > 1;
+  if constexpr (PRE) {
+    if (status == 0 && d > 0) {
+      #pragma unroll 1
+      for (int k = 1 + lane; k <= d; k += G) {
+        const f3 uk = nd.U(k);
+        float b1 = -3.0f, b2 = -3.0f;
+        int i1 = k, i2 = k;
+        for (int m = 1; m <= d; m++) {
+          if (m == k) continue;
+          const float cm = f_dot(uk, nd.U(m));
+          if (cm > b1) { b2 = b1; i2 = i1; b1 = cm; i1 = m; }
+          else if (cm > b2) { b2 = cm; i2 = m; }
+        }
+        ws.nn[k] = (uint32_t)i1 | ((uint32_t)i2 << 8);
+      }
+      if (lane == 0) {
+        ws.nn[0] = 0u;
+        ws.wp[0][0] = make_float4(0.f, 0.f, 0.f, 0.f);
+        ws.wp[0][1] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      g.sync();
+      const int ntri = ns * (ns - 1) * (ns - 2) / 6;
+      const uint32_t *t3 = P.tri3 + ns * (ns - 1) * (ns - 2) * (ns - 3) / 24;
+      constexpr int QC = WS::QA;
+      int qh = 0, nq = 0;   // queue head and length (warp-uniform)
+      const unsigned lt = (1u << lane) - 1u;
+      // the full side test of queued roots [qh, qh + cnt) (one per lane), appended in order
+      auto drain_q = [&](int cnt) -> int {
+        const int qi = qh + lane >= QC ? qh + lane - QC : qh + lane;
+        bool v = false;
+        uint32_t qc = 0u;
+        float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (lane < cnt) {
+          q = ws.jq[qi];
+          qc = ws.jqc[qi];
+          const bool sphere = (qc >> 26) & 1u;
+          const uint32_t excl = (1u << (qc & 0xff)) | (1u << ((qc >> 8) & 0xff)) | (1u << ((qc >> 16) & 0xff));
+          const float tau = sphere ? 0.0f : q.w;
+          const f3 y = F3(q.x, q.y, q.z);
+          uint32_t viol = 0u, mb = 2u;
+          for (int m = 1; m <= d; m++, mb <<= 1) viol |= (nd.hs(m, y) - tau > delta) ? mb : 0u;
+          v = !(viol & ~excl);
+        }
+        const unsigned vm = g.ballot(v);
+        const int pos = nj + __popc(vm & lt);
+        int e = 0;
+        if (v) e = pos >= MAXJ ? LMM_NODE_JCAP : (((qc >> 27) & 1u) ? LMM_NODE_SHORT : 0);
+        const int fe = first_err<G>(g, e);
+        if (fe) return fe;
+        if (v) {
+          ws.jp[pos] = make_float4(q.x, q.y, q.z, 0.0f);
+          ws.jabc[pos] = qc & 0x03ffffffu;
+        }
+        nj += __popc(vm);
+        qh = qh + cnt >= QC ? qh + cnt - QC : qh + cnt;
+        nq -= cnt;
+        return 0;
+      };
+      #pragma unroll 1
+      for (int base = 0; base < ntri && status == 0; base += G) {
+        const int t = base + lane;
+        const uint32_t code = __ldg(&t3[t < ntri ? t : ntri - 1]);
+        const int a = code & 0xff, b = (code >> 8) & 0xff, c = code >> 16;
+        f3 y[2];
+        float tau[2];
+        const bool solved = nd.junction_bf(a, b, c, y, tau) && t < ntri;
+        const uint32_t excl = (1u << a) | (1u << b) | (1u << c);
+        const bool sphere = a == 0;
+        bool v0 = solved && (sphere || !(tau[0] < -delta)), v1 = solved && (sphere || !(tau[1] < -delta));
+        {   // pre-test: the nearest struts of a, b, c, both roots in packed f32x2 operations
+          const float2 Yx = make_float2(y[0].x, y[1].x), Yy = make_float2(y[0].y, y[1].y), Yz = make_float2(y[0].z, y[1].z);
+          const float2 nT = sphere ? make_float2(0.0f, 0.0f) : make_float2(-tau[0], -tau[1]);
+          const uint32_t l3 = ws.nn[a] | (ws.nn[b] << 16), lc = ws.nn[c];
+          uint32_t w0 = 0u, w1 = 0u;
+          #pragma unroll
+          for (int r = 0; r < 6; r++) {
+            const int m = r < 4 ? (l3 >> (8 * r)) & 0xff : (lc >> (8 * (r - 4))) & 0xff;
+            const float2 h = side_h2(ws.wp[m][0], ws.wp[m][1], Yx, Yy, Yz, nT);
+            w0 |= h.x > delta ? 1u << m : 0u;
+            w1 |= h.y > delta ? 1u << m : 0u;
+          }
+          v0 = v0 && !(w0 & ~excl);
+          v1 = v1 && !(w1 & ~excl);
+        }
+        const unsigned m0 = g.ballot(v0), m1 = g.ballot(v1);
+        if (m0 | m1) {
+          const float lm = fminf(fminf(ws.lim[a], ws.lim[b]), ws.lim[c]);
+          int qp = qh + nq + __popc(m0 & lt) + __popc(m1 & lt);
+          qp = qp >= QC ? qp - QC : qp;
+          const uint32_t cf = code | (sphere ? (1u << 26) : 0u);
+          if (v0) {
+            ws.jq[qp] = make_float4(y[0].x, y[0].y, y[0].z, tau[0]);
+            ws.jqc[qp] = cf | (fabsf(tau[0]) <= delta ? (1u << 25) : 0u) | (tau[0] > lm ? (1u << 27) : 0u);
+          }
+          if (v1) {
+            const int q1 = qp + (v0 ? 1 : 0) >= QC ? qp + (v0 ? 1 : 0) - QC : qp + (v0 ? 1 : 0);
+            ws.jq[q1] = make_float4(y[1].x, y[1].y, y[1].z, tau[1]);
+            ws.jqc[q1] = cf | (1u << 24) | (fabsf(tau[1]) <= delta ? (1u << 25) : 0u) | (tau[1] > lm ? (1u << 27) : 0u);
+          }
+          nq += __popc(m0) + __popc(m1);
+          g.sync();
+          while (nq >= G && status == 0) status = drain_q(G);
+        }
+      }
+      if (status == 0 && nq > 0) status = drain_q(nq);
+    }
+  }
+  if (!PRE && status == 0 && d > 0) {
     const int ntri = ns * (ns - 1) * (ns - 2) / 6;
     const uint32_t *t3 = P.tri3 + ns * (ns - 1) * (ns - 2) * (ns - 3) / 24;   // triples of ns sides
     #pragma unroll 1

@@ -1,0 +1,14 @@
+#!/bin/bash
+O=gpurun_out/mc2; mkdir -p $O
+for F in "" "-DLMM_PRE_MAXS=13"; do
+  export LMM_NVCC_EXTRA="$F"
+  python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1 || { echo build failed; continue; }
+  for c in octet100 stoch290; do
+    timeout 900 python bench.py --config $c --steps 3 --warmup 2 --no-cpu-baseline --e2e-steps 0 > $O/b.json 2>/dev/null
+    python - $O/b.json "[$F] $c" <<'PY'
+import json,sys
+d=json.loads(open(sys.argv[1]).read().strip().splitlines()[-1]); k=d["kernel_ms_per_step"]
+print(sys.argv[2], "value %.4g" % d["value"], "ms/step %.1f" % d["ms_per_step"], "mm %.2f" % k["metamesh"])
+PY
+  done
+done
