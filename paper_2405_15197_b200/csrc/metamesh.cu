@@ -85,6 +85,9 @@ struct alignas(16) WSCore {
 #ifndef LMM_PRE_MAXS
 #define LMM_PRE_MAXS 17
 #endif
+#ifndef LMM_PRE_NN
+#define LMM_PRE_NN 2   // nearest struts per side in the pre-test (1..3)
+#endif
 template <int MAXS, int MAXJ, int MAXV, int MAXA, int MAXLE, int MAXH>
 struct alignas(16) WS_A : WSCore<MAXS, MAXV> {
   // side k as broadcast pairs for the two-root junction test: (wx,wx,wy,wy), (wz,wz,-e,-e)
@@ -96,7 +99,7 @@ struct alignas(16) WS_A : WSCore<MAXS, MAXV> {
   // warp-per-node buckets: the roots that pass a pre-test against the triple's nearest sides,
   // queued (ring buffer) for the full side test in batches of 32 (see part_a)
   static constexpr int QA = MAXS >= LMM_PRE_MAXS ? 96 : 1;
-  uint32_t nn[MAXS];     // the two struts nearest in direction to strut k (bytes 0, 1)
+  uint32_t nn[MAXS];     // the three struts nearest in direction to strut k (bytes 0, 1, 2)
   float4 jq[QA];         // queued root: x, y, z, solver tau
   uint32_t jqc[QA];      // its jabc code | sphere << 26 | SHORT << 27
 };
@@ -272,15 +275,16 @@ __device__ void part_a(cg::thread_block_tile<G> &g, WS &ws, const MMParams &P, i
       #pragma unroll 1
       for (int k = 1 + lane; k <= d; k += G) {
         const f3 uk = nd.U(k);
-        float b1 = -3.0f, b2 = -3.0f;
-        int i1 = k, i2 = k;
+        float b1 = -3.0f, b2 = -3.0f, b3 = -3.0f;
+        int i1 = k, i2 = k, i3 = k;
         for (int m = 1; m <= d; m++) {
           if (m == k) continue;
           const float cm = f_dot(uk, nd.U(m));
-          if (cm > b1) { b2 = b1; i2 = i1; b1 = cm; i1 = m; }
-          else if (cm > b2) { b2 = cm; i2 = m; }
+          if (cm > b1) { b3 = b2; i3 = i2; b2 = b1; i2 = i1; b1 = cm; i1 = m; }
+          else if (cm > b2) { b3 = b2; i3 = i2; b2 = cm; i2 = m; }
+          else if (cm > b3) { b3 = cm; i3 = m; }
         }
-        ws.nn[k] = (uint32_t)i1 | ((uint32_t)i2 << 8);
+        ws.nn[k] = (uint32_t)i1 | ((uint32_t)i2 << 8) | ((uint32_t)i3 << 16);
       }
       if (lane == 0) {
         ws.nn[0] = 0u;
@@ -339,11 +343,12 @@ __device__ void part_a(cg::thread_block_tile<G> &g, WS &ws, const MMParams &P, i
         {   // pre-test: the nearest struts of a, b, c, both roots in packed f32x2 operations
           const float2 Yx = make_float2(y[0].x, y[1].x), Yy = make_float2(y[0].y, y[1].y), Yz = make_float2(y[0].z, y[1].z);
           const float2 nT = sphere ? make_float2(0.0f, 0.0f) : make_float2(-tau[0], -tau[1]);
-          const uint32_t l3 = ws.nn[a] | (ws.nn[b] << 16), lc = ws.nn[c];
+          const uint32_t la = ws.nn[a], lb = ws.nn[b], lc = ws.nn[c];
           uint32_t w0 = 0u, w1 = 0u;
           #pragma unroll
-          for (int r = 0; r < 6; r++) {
-            const int m = r < 4 ? (l3 >> (8 * r)) & 0xff : (lc >> (8 * (r - 4))) & 0xff;
+          for (int r = 0; r < 3 * LMM_PRE_NN; r++) {
+            const uint32_t lw = r < LMM_PRE_NN ? la : (r < 2 * LMM_PRE_NN ? lb : lc);
+            const int m = (lw >> (8 * (r % LMM_PRE_NN))) & 0xff;
             const float2 h = side_h2(ws.wp[m][0], ws.wp[m][1], Yx, Yy, Yz, nT);
             w0 |= h.x > delta ? 1u << m : 0u;
             w1 |= h.y > delta ? 1u << m : 0u;

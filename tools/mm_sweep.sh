@@ -1,9 +1,10 @@
 #!/bin/bash
-O=gpurun_out/mc2; mkdir -p $O
-for F in "" "-DLMM_PRE_MAXS=13"; do
+# meta-mesh build variants: mm_sweep.sh "configs" "flags1" "flags2" ...
+O=gpurun_out/mms; mkdir -p $O; CF=$1; shift
+for F in "$@"; do
   export LMM_NVCC_EXTRA="$F"
   python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1 || { echo build failed; continue; }
-  for c in octet100 stoch290; do
+  for c in $CF; do
     timeout 900 python bench.py --config $c --steps 3 --warmup 2 --no-cpu-baseline --e2e-steps 0 > $O/b.json 2>/dev/null
     python - $O/b.json "[$F] $c" <<'PY'
 import json,sys
