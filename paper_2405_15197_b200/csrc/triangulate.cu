@@ -753,7 +753,17 @@ __device__ void emit_band_whole(const TriParams &P, WarpRing &w, const Pts &pt, 
         put_second(d, g);
       }
     }
-    flush_group(w, (lo_q - gq) * REC, (hi_q - gq) * REC, out + (base + gq - first) * REC, lane);
+    if (gq >= qb && gq + GRP <= qe) {   // a whole group: one bulk copy, no head or tail
+      __syncwarp();
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      __syncwarp();
+      if (lane == 0) {
+        const unsigned sa = (unsigned)__cvta_generic_to_shared(w.stage);
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n"
+                     ::"l"(out + (base + gq - first) * REC), "r"(sa), "n"(GRP * REC) : "memory");
+        asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+      }
+    } else flush_group(w, (lo_q - gq) * REC, (hi_q - gq) * REC, out + (base + gq - first) * REC, lane);
     if (!second) { prefetch(2); second = true; }
   }
   if (!second) prefetch(2);
