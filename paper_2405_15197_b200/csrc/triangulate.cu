@@ -723,7 +723,9 @@ __device__ void emit_band_whole(const TriParams &P, WarpRing &w, const Pts &pt, 
     const int qa = gq + 2 * lane, qb2 = qa + 1;
     const int lo_q = gq > qb ? gq : qb;
     const int hi_q = gq + GRP < qe ? gq + GRP : qe;
-    const bool va = qa >= lo_q && qa < hi_q, vb = qb2 >= lo_q && qb2 < hi_q;
+    const bool whole = gq >= qb && gq + GRP <= qe;
+    const bool va = whole ? lane < GRP / 2 : (qa >= lo_q && qa < hi_q);
+    const bool vb = whole ? lane < GRP / 2 : (qb2 >= lo_q && qb2 < hi_q);
     // bit of step q: word (sb + q) >> 5 of the band's words, from the owning lane
     const int ba = sb + (va ? qa : 0), bb = sb + (vb ? qb2 : 0);
     const uint32_t wa = __shfl_sync(0xffffffffu, mword, ba >> 5), wb = __shfl_sync(0xffffffffu, mword, bb >> 5);
@@ -753,7 +755,7 @@ __device__ void emit_band_whole(const TriParams &P, WarpRing &w, const Pts &pt, 
         put_second(d, g);
       }
     }
-    if (gq >= qb && gq + GRP <= qe) {   // a whole group: one bulk copy, no head or tail
+    if (whole) {   // a whole group: one bulk copy, no head or tail
       __syncwarp();
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
       __syncwarp();
