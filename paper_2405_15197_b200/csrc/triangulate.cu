@@ -846,7 +846,17 @@ __device__ void emit_band(const TriParams &P, WarpRing &w, const Pts &pt, const 
         if (va) { tri(qa, ia, aa, f); put_first(d, f); }
         if (vb) { tri(qb2, ia + (aa ? 1 : 0), ab, f); put_second(d, f); }
       }
-      flush_group(w, (lo_q - gq) * REC, (hi_q - gq) * REC, out + (base + gq - first) * REC, lane);
+      if (gq >= q0 && gq + GRP <= q1) {   // a whole group: one bulk copy, no head or tail
+        __syncwarp();
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+          const unsigned sa = (unsigned)__cvta_generic_to_shared(w.stage);
+          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n"
+                       ::"l"(out + (base + gq - first) * REC), "r"(sa), "n"(GRP * REC) : "memory");
+          asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+        }
+      } else flush_group(w, (lo_q - gq) * REC, (hi_q - gq) * REC, out + (base + gq - first) * REC, lane);
     }
     __syncwarp();
   }
