@@ -1,10 +1,9 @@
 #!/bin/bash
 # diagnostic build of liblmm with per-phase clock64 instrumentation of the meta-mesh kernel
+# (tools/liblmm_phase.so), then the normal build again
 set -e
-D=$(mktemp -d); R=$(cd "$(dirname "$0")/.." && pwd)
-A="-gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -Xcompiler -fPIC"
-for f in lmm_api lattice scan triangulate; do /usr/local/cuda/bin/nvcc $A -c $R/paper_2405_15197_b200/csrc/$f.cu -o $D/$f.o & done
-/usr/local/cuda/bin/nvcc $A -fmad=false -DLMM_PHASE_TIMING -c $R/paper_2405_15197_b200/csrc/metamesh.cu -o $D/metamesh.o
-wait
-/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $R/tools/liblmm_phase.so $D/*.o
-rm -rf $D
+R=$(cd "$(dirname "$0")/.." && pwd)
+cd $R
+LMM_NVCC_EXTRA="-DLMM_PHASE_TIMING" python -c "import __graft_entry__ as g; g.build()" > /dev/null
+cp paper_2405_15197_b200/lib/liblmm.so tools/liblmm_phase.so
+python -c "import __graft_entry__ as g; g.build()" > /dev/null
