@@ -934,15 +934,6 @@ __device__ void emit_hole(const TriParams &P, WarpRing &w, const Pts &pt, int g,
   }
 }
 
-__device__ __forceinline__ int nth_bit(unsigned m, int n) {   // position of the n-th (0-based) set bit
-  int p = 0;
-#pragma unroll
-  for (int s = 16; s >= 1; s >>= 1) {
-    const int c = __popc(m & ((1u << s) - 1u));
-    if (n >= c) { n -= c; m >>= s; p += s; }
-  }
-  return p;
-}
 __device__ __forceinline__ unsigned mask_ge(int x) { return x >= 32 ? 0u : (x <= 0 ? 0xffffffffu : (0xffffffffu << x)); }
 __device__ __forceinline__ unsigned mask_le(int x) { return x < 0 ? 0u : (x >= 31 ? 0xffffffffu : ((2u << x) - 1u)); }
 
@@ -1258,18 +1249,13 @@ __global__ void __launch_bounds__(EMIT_T, LMM_SPAN_MINB) k_emit_span(TriParams P
         if (st == B_OK) return ACT_WINDOW;
         if (st == B_END) return ACT_DONE;
         int64_t sl;
-        int te;
         {
           const int64_t c = snext + lane;
           int64_t b = INT64_MAX, e = INT64_MAX;
           if (c < P.S) { b = P.strut_off[c]; e = P.strut_off[c + 1]; }
           const unsigned livem = __ballot_sync(FULL, b < T1 && e > b);
-          const int cl = __ffs(livem) - 1;   // a live band exists (NOFIT)
-          sl = snext + cl;
-          const int64_t el = __shfl_sync(FULL, e, cl);
-          te = (int)((el < T1 ? el : T1) - T0);
+          sl = snext + __ffs(livem) - 1;   // a live band exists (NOFIT)
         }
-        (void)te;
         WarpRing &w = *reinterpret_cast<WarpRing *>(&S.ent[0]);
         BandRec &lrec = *reinterpret_cast<BandRec *>(&S.b_c[0][0]);
         long long &lbase = *reinterpret_cast<long long *>(&S.b_pos[0]);
