@@ -194,10 +194,13 @@ def test_csr_offsets_are_the_degree_prefix_sum(built):
 
 
 @pytest.mark.parametrize("family", ["octet", "bcc", "stoch"])
-def test_virtual_ranks_union_equals_global_gpu(family):
+@pytest.mark.parametrize("path", ["0", "1"], ids=["band-path", "cta-windows"])
+def test_virtual_ranks_union_equals_global_gpu(family, path, monkeypatch):
     """The multi-GPU path on one device: slab windows with halo recompute + emit masks.  The
     union of the per-rank STL outputs equals the single-lattice output bitwise (as a set),
-    so the global mesh is seamless across rank boundaries."""
+    so the global mesh is seamless across rank boundaries -- through either emit path (the
+    masked struts are empty bands inside the CTA windows)."""
+    monkeypatch.setenv("LMM_EMIT_PATH", path)
     from paper_2405_15197_b200 import MetaMesher
     from paper_2405_15197_b200 import partition as P
     nx, ny, nz = 4, 3, 6
