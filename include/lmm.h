@@ -132,7 +132,11 @@ LMM_API int lmm_triangulate(lmm_ctx *ctx, double chord_error, int64_t *n_triangl
  * strut's band; then nodes ascending, each node's hole fans) as 50-byte binary-STL
  * facet records (normal f32x3, v1, v2, v3 f32x3 each, uint16 attribute = 0), packed, into
  * out[0 .. 50*count).  `out` is host or device memory per `where`; device `out` must be
- * 16-byte aligned.  Host output is staged through pinned buffers in chunks. */
+ * 16-byte aligned.  Host output is staged through pinned buffers in chunks.
+ * The band region is emitted by one of two kernels that write identical bytes (DESIGN.md
+ * Sec. 6): warp per band when the mean band exceeds 100 triangles, else CTA windows of
+ * whole bands; environment overrides for tuning only: LMM_EMIT_PATH=0|1 (band | windows),
+ * LMM_SPCW (window points, 256..1280), LMM_SPAN (band triangles per CTA, multiple of 64). */
 LMM_API int lmm_write_triangles(lmm_ctx *ctx, int64_t first, int64_t count, void *out, int where);
 
 /* Wait for all work enqueued by the context. */
