@@ -279,7 +279,7 @@ def main():
 
     sweep = [float(x) for x in args.ce_sweep.split(",") if x] if args.ce_sweep else None
     ces = sweep or [args.ce]
-    per_ce = {}
+    per_ce, per_ce_path = {}, {}
 
     def load_and_build():
         B.lmm_load_lattice(h, xyz_d, ends_d, rend_d)
@@ -302,6 +302,7 @@ def main():
             for f in range(0, Tc, EMIT_CHUNK):
                 B.lmm_write_triangles(h, f, min(EMIT_CHUNK, Tc - f), out)
             per_ce[ce] = Tc
+            per_ce_path[ce] = B.lmm_emit_path(h)
             T += Tc
         return T
 
@@ -388,12 +389,18 @@ def main():
     achieved = emit_bytes / (emit_ms / 1e3) / 1e9 if emit_ms > 0 else None
     mm_ms = kt["csr"][0] + kt["bucket"][0] + kt["metamesh"][0]
     tri_ms = kt["count"][0] + kt["scan"][0] + kt["emit"][0]
+    # the kernel that emitted the band region (k_emit: warp per band; k_emit_span: CTA windows)
+    kinds = sorted({"k_emit_span" if per_ce_path.get(ce) == 1 else "k_emit" for ce in ces})
+    emit_kernel = "+".join(kinds)
     traffic, bpt = None, None
     try:
         with open(os.path.join(ROOT, "profiles", "emit_traffic.json")) as f:
-            bpt = json.load(f).get("bytes_per_triangle")
+            tj = json.load(f)
+        bk = tj.get("by_kernel", {})
+        bpt = (bk.get(emit_kernel, {}).get("bytes_per_triangle", tj.get("bytes_per_triangle")) if len(kinds) == 1
+               else tj.get("bytes_per_triangle"))
         traffic = bpt * float(T) * args.steps / emit_n if emit_n else None   # DRAM bytes per launch
-    except (OSError, ValueError, TypeError):
+    except (OSError, ValueError, TypeError, AttributeError):
         pass
     res = {
         "metric": METRIC,
@@ -419,7 +426,7 @@ def main():
         "triangles_per_s": T_all / (ms_max / 1e3),
         "triangulate_triangles_per_s": T * args.steps / (tri_ms / 1e3) if tri_ms else None,
         "kernel_ms_per_step": {k: v[0] / args.steps for k, v in kt.items()},
-        "roofline": {"bound": "hbm", "kernel": "k_emit", "achieved": achieved, "peak": peak, "unit": "GB/s",
+        "roofline": {"bound": "hbm", "kernel": emit_kernel, "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak if achieved else None, "peak_source": src,
                      "traffic": traffic, "traffic_bytes_per_triangle": bpt, "algorithmic_bytes_per_triangle": STL,
                      "launches": emit_n, "avg_launch_ms": emit_ms / emit_n if emit_n else None},

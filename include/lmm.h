@@ -189,6 +189,10 @@ LMM_API int lmm_reset_kernel_times(lmm_ctx *ctx);
 /* Number of CUDA kernels this context has launched so far (monotone counter). */
 LMM_API int lmm_launch_count(lmm_ctx *ctx, int64_t *n);
 
+/* The kernel that emitted the band region in the last lmm_write_triangles: 0 = warp per band
+ * (k_emit), 1 = CTA windows of whole bands (k_emit_span), -1 = none yet. */
+LMM_API int lmm_emit_path(lmm_ctx *ctx, int *path);
+
 LMM_API const char *lmm_error_string(int status);
 LMM_API const char *lmm_version(void);
 

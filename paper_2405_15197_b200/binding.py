@@ -63,12 +63,14 @@ def load_library():
     lib.lmm_kernel_times.argtypes = [P, C.POINTER(C.c_double), C.POINTER(i64)]
     lib.lmm_reset_kernel_times.argtypes = [P]
     lib.lmm_launch_count.argtypes = [P, C.POINTER(i64)]
+    lib.lmm_emit_path.argtypes = [P, C.POINTER(i32)]
     lib.lmm_error_string.argtypes = [i32]
     lib.lmm_error_string.restype = C.c_char_p
     lib.lmm_version.restype = C.c_char_p
     for name in ("lmm_create", "lmm_load_lattice", "lmm_build_metamesh", "lmm_metamesh_stats", "lmm_triangulate",
                  "lmm_write_triangles", "lmm_sync", "lmm_buffer_size", "lmm_copy_buffer", "lmm_timing",
-                 "lmm_kernel_times", "lmm_reset_kernel_times", "lmm_launch_count", "lmm_set_emit_mask"):
+                 "lmm_kernel_times", "lmm_reset_kernel_times", "lmm_launch_count", "lmm_set_emit_mask",
+                 "lmm_emit_path"):
         getattr(lib, name).restype = i32
     _lib = lib
     return lib
@@ -208,6 +210,13 @@ def lmm_kernel_times(h) -> dict:
 
 def lmm_reset_kernel_times(h):
     _check(load_library().lmm_reset_kernel_times(h))
+
+
+def lmm_emit_path(h) -> int:
+    """0: the band region was emitted warp per band (k_emit); 1: by CTA windows (k_emit_span)."""
+    v = C.c_int32()
+    _check(load_library().lmm_emit_path(h, C.byref(v)))
+    return int(v.value)
 
 
 def lmm_launch_count(h) -> int:

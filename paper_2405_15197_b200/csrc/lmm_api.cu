@@ -418,4 +418,10 @@ LMM_API int lmm_launch_count(lmm_ctx *c, int64_t *n) {
   return LMM_OK;
 }
 
+LMM_API int lmm_emit_path(lmm_ctx *c, int *path) {
+  if (!c || !path) return LMM_E_ARG;
+  *path = c->emit_path;
+  return LMM_OK;
+}
+
 }  // extern "C"

@@ -1637,6 +1637,7 @@ int triangulate_emit(lmm_ctx *c, int64_t first, int64_t count, void *out_dev, cu
   bool use_span = mean <= 100.0;
   if (const char *ev = getenv("LMM_EMIT_PATH")) use_span = atoi(ev) == 1 ? true : (atoi(ev) == 0 ? false : use_span);
   const int64_t last = first + count;
+  if (first < c->n_tri_band) c->emit_path = use_span ? 1 : 0;
   if (!use_span || first >= c->n_tri_band) return launch_band_path(c, P, first, count, out_dev, st, true);
   if (!c->emit_attr_set) {
     CUDA_TRY(cudaFuncSetAttribute(k_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, ring_bytes(PCAP_MAX) * EW));
