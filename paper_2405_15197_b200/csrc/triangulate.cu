@@ -1577,6 +1577,10 @@ static int launch_band_path(lmm_ctx *c, const TriParams &P, int64_t first, int64
     const int64_t live = c->S > 0 ? c->S : 1;
     const double mean = (double)c->n_tri_band / (double)live;
     while (pcap < PCAP_MAX && mean + 2.0 > pcap - 4) pcap = pcap + 160 < PCAP_MAX ? pcap + 160 : PCAP_MAX;
+    if (const char *ev = getenv("LMM_PCAP")) {   // tuning override: 152, 312, 472 or 640
+      const int v = atoi(ev);
+      if (v == 152 || v == 312 || v == 472 || v == PCAP_MAX) pcap = v;
+    }
   }
   const size_t smem = (size_t)ring_bytes(pcap) * EW;
   if (!c->emit_attr_set) {
