@@ -48,6 +48,7 @@ def meshes():
 
 
 def _emit(mm, T, setting, ranges=()):
+    from paper_2405_15197_b200 import binding as B
     path, pcw, span = setting
     keys = {"LMM_EMIT_PATH": path, "LMM_SPCW": pcw, "LMM_SPAN": span}
     old = {k: os.environ.get(k) for k in keys}
@@ -58,6 +59,7 @@ def _emit(mm, T, setting, ranges=()):
             else:
                 os.environ[k] = v
         full = mm.triangles(0, T)
+        assert B.lmm_emit_path(mm.h) == int(path)   # the kernel that wrote the band region
         parts = [mm.triangles(a, b - a) for a, b in ranges]
     finally:
         for k, v in old.items():
