@@ -398,6 +398,9 @@ __global__ void k_chunk_map_holes(TriParams P) {
 // and arc records (after its last group).  No registers are held across a band and no
 // block-level barriers are used.
 constexpr int EW = EMIT_T / 32;   // warps per CTA
+#ifndef LMM_EMIT_BAND_MINB
+#define LMM_EMIT_BAND_MINB 7   // k_emit CTAs per SM the registers are sized for (72 registers)
+#endif
 constexpr int PCAP_MIN = 152;     // ring points cached per band (both rings), runtime-sized
 constexpr int PCAP_MAX = 640;     //   from the mean band size (triangulate_emit)
 constexpr int GRP = 56;           // triangles per aligned group (2800 B; 28 lanes x 2 records)
@@ -1426,7 +1429,7 @@ __global__ void __launch_bounds__(EMIT_T, LMM_SPAN_MINB) k_emit_span(TriParams P
 }
 
 // units: bands [s0, s1) then holes [g0, g1) intersecting [first, last)
-__global__ void __launch_bounds__(EMIT_T, 8) k_emit(TriParams P, int64_t first, int64_t count, unsigned char *out,
+__global__ void __launch_bounds__(EMIT_T, LMM_EMIT_BAND_MINB) k_emit(TriParams P, int64_t first, int64_t count, unsigned char *out,
                                                  int64_t s0, int64_t s1, int64_t g0, int64_t g1, int pcap) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ BandRec rec[EW][2];
