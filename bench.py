@@ -31,7 +31,7 @@ import synth  # noqa: E402
 
 METRIC = "struts/s meta-meshing and triangles/s triangulation at 1/2/4/8 B200; % HBM peak"
 STL = 50
-EMIT_CHUNK = 1 << 28
+EMIT_CHUNK = 1 << int(os.environ.get("LMM_BENCH_CHUNK_LOG2", "28"))   # triangles per device output chunk
 
 
 def make_config(name: str, rank: int = 0, world: int = 1):
