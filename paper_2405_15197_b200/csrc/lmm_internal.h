@@ -70,7 +70,7 @@ struct lmm_ctx {
   DevBuf ring_n;     // int [2S] points per ring (CSR entry), count pass
   int64_t H = 0, n_tri = 0, n_tri_band = 0;
   bool emit_attr_set = false;   // k_emit's opt-in shared-memory limit set on this context's device
-  int emit_occ[32] = {0};       // k_emit CTAs per SM by point-cache size (pcap / 32)
+  int emit_occ[64] = {0};       // CTAs per SM: k_emit by point-cache size [0, 32), k_emit_span by window [40, 51)
   int emit_path = -1;           // band region of the last emission: 0 k_emit, 1 k_emit_span
   bool tri_ok = false;
   // scratch

@@ -1580,9 +1580,9 @@ static int launch_band_path(lmm_ctx *c, const TriParams &P, int64_t first, int64
     const int64_t live = c->S > 0 ? c->S : 1;
     const double mean = (double)c->n_tri_band / (double)live;
     while (pcap < PCAP_MAX && mean + 2.0 > pcap - 4) pcap = pcap + 160 < PCAP_MAX ? pcap + 160 : PCAP_MAX;
-    if (const char *ev = getenv("LMM_PCAP")) {   // tuning override: 152, 312, 472 or 640
+    if (const char *ev = getenv("LMM_PCAP")) {   // tuning override: PCAP_MIN + 16 k (< PCAP_MAX) or PCAP_MAX
       const int v = atoi(ev);
-      if (v == 152 || v == 312 || v == 472 || v == PCAP_MAX) pcap = v;
+      if (v == PCAP_MAX || (v >= PCAP_MIN && v < PCAP_MAX && (v - PCAP_MIN) % 16 == 0)) pcap = v;
     }
   }
   const size_t smem = (size_t)ring_bytes(pcap) * EW;
@@ -1591,7 +1591,7 @@ static int launch_band_path(lmm_ctx *c, const TriParams &P, int64_t first, int64
     CUDA_TRY(cudaFuncSetAttribute(k_emit_span, cudaFuncAttributeMaxDynamicSharedMemorySize, span_bytes(SPCW_MAX)));
     c->emit_attr_set = true;
   }
-  int &occ = c->emit_occ[pcap == PCAP_MAX ? 7 : (pcap - PCAP_MIN) / 160];
+  int &occ = c->emit_occ[pcap == PCAP_MAX ? 31 : (pcap - PCAP_MIN) / 16];   // one slot per cache size
   if (occ == 0) {
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_emit, EMIT_T, smem));
     if (occ < 1) occ = 1;
@@ -1652,7 +1652,7 @@ int triangulate_emit(lmm_ctx *c, int64_t first, int64_t count, void *out_dev, cu
     c->emit_attr_set = true;
   }
   const size_t smem = (size_t)span_bytes(pcw);
-  int &occ = c->emit_occ[8 + pcw / 128];
+  int &occ = c->emit_occ[40 + pcw / 128];
   if (occ == 0) {
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_emit_span, EMIT_T, smem));
     if (occ < 1) occ = 1;
