@@ -136,7 +136,8 @@ LMM_API int lmm_triangulate(lmm_ctx *ctx, double chord_error, int64_t *n_triangl
  * The band region is emitted by one of two kernels that write identical bytes (DESIGN.md
  * Sec. 6): warp per band when the mean band exceeds 100 triangles, else CTA windows of
  * whole bands; environment overrides for tuning only: LMM_EMIT_PATH=0|1 (band | windows),
- * LMM_SPCW (window points, 256..1280), LMM_SPAN (band triangles per CTA, multiple of 64). */
+ * LMM_SPCW (window points, 256..1280), LMM_SPAN (band triangles per CTA, multiple of 64),
+ * LMM_PCAP (band-path point cache, 152 + 16 k below 640, or 640; default from the mean band). */
 LMM_API int lmm_write_triangles(lmm_ctx *ctx, int64_t first, int64_t count, void *out, int where);
 
 /* Wait for all work enqueued by the context. */
